@@ -1,0 +1,137 @@
+"""CPU oracle for the conv hot path of arXiv 2305.08819 — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline``
+leg and ``--impl reference``) may import this package.  The product path
+(``paper_2305_08819_b200``) never imports it, and the two share no code: this
+wrapper marshals numpy arrays into ``liboracle.so`` (built from
+``conv_oracle.c``), which computes the plain definitions O1-O3 with double
+accumulation (see the C file for the paper/SPEC passages each follows).
+
+Inputs are float32 arrays (the same host arrays the GPU path receives); outputs
+are float64.
+
+Pins: every function here is pinned by ``tests/test_oracle_pins.py`` against
+things other than itself — closed forms, the trilinear adjoint identity, 1x1 conv
+= BLAS matmul, delta kernels = shifts, exact finite differences of a bilinear
+form, SPEC's worked values (tests/golden/), and torch's CPU float64 conv as an
+independent library routine.  No function is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "conv_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc -O2 -fopenmp (plain C, no vectorisation tricks needed)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + ".tmp%d" % os.getpid()
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c99",
+                               _SRC, "-o", tmp])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        fp = ctypes.POINTER(ctypes.c_float)
+        dp = ctypes.POINTER(ctypes.c_double)
+        ints = [ctypes.c_int] * 11
+        for name, a, b in (("oracle_conv2d_fwd", fp, fp), ("oracle_conv2d_bwd_data", fp, fp),
+                           ("oracle_conv2d_bwd_filter", fp, fp)):
+            f = getattr(lib, name)
+            f.argtypes = [a, b, dp] + ints
+            f.restype = ctypes.c_int
+        lib.oracle_out_hw.argtypes = [ctypes.c_int] * 8 + [ctypes.POINTER(ctypes.c_int)] * 2
+        lib.oracle_out_hw.restype = ctypes.c_int
+        lib.oracle_num_threads.restype = ctypes.c_int
+        lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
+        _lib = lib
+    return _lib
+
+
+def _f32(a):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def out_hw(IH, IW, FH, FW, sh, sw, ph, pw):
+    lib = _load()
+    oh, ow = ctypes.c_int(), ctypes.c_int()
+    if lib.oracle_out_hw(IH, IW, FH, FW, sh, sw, ph, pw, ctypes.byref(oh), ctypes.byref(ow)):
+        raise ValueError("invalid conv geometry")
+    return oh.value, ow.value
+
+
+def conv2d_fwd(X, W, stride=(1, 1), padding=(1, 1)):
+    """Y[N,OH,OW,OC] (float64) = X[N,IH,IW,IC] (*) W[OC,FH,FW,IC]  (O1)."""
+    X, xp = _f32(X)
+    W, wp = _f32(W)
+    N, IH, IW, IC = X.shape
+    OC, FH, FW, IC2 = W.shape
+    assert IC == IC2
+    OH, OW = out_hw(IH, IW, FH, FW, stride[0], stride[1], padding[0], padding[1])
+    Y = np.empty((N, OH, OW, OC), np.float64)
+    rc = _load().oracle_conv2d_fwd(xp, wp, Y.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                   N, IH, IW, IC, OC, FH, FW, stride[0], stride[1],
+                                   padding[0], padding[1])
+    if rc:
+        raise ValueError("oracle_conv2d_fwd: bad arguments")
+    return Y
+
+
+def conv2d_bwd_data(dY, W, input_hw, stride=(1, 1), padding=(1, 1)):
+    """dX[N,IH,IW,IC] (float64) = dY (*)^T W  (O2), IH,IW given explicitly (reading L5)."""
+    dY, dyp = _f32(dY)
+    W, wp = _f32(W)
+    N, OH, OW, OC = dY.shape
+    OC2, FH, FW, IC = W.shape
+    assert OC == OC2
+    IH, IW = input_hw
+    if out_hw(IH, IW, FH, FW, stride[0], stride[1], padding[0], padding[1]) != (OH, OW):
+        raise ValueError("dY extent does not match the forward output of input_hw")
+    dX = np.empty((N, IH, IW, IC), np.float64)
+    rc = _load().oracle_conv2d_bwd_data(dyp, wp, dX.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                        N, IH, IW, IC, OC, FH, FW, stride[0], stride[1],
+                                        padding[0], padding[1])
+    if rc:
+        raise ValueError("oracle_conv2d_bwd_data: bad arguments")
+    return dX
+
+
+def conv2d_bwd_filter(X, dY, kernel_hw, stride=(1, 1), padding=(1, 1)):
+    """dW[OC,FH,FW,IC] (float64) = sum_{n,oh,ow} dY x X-patch  (O3)."""
+    X, xp = _f32(X)
+    dY, dyp = _f32(dY)
+    N, IH, IW, IC = X.shape
+    N2, OH, OW, OC = dY.shape
+    assert N == N2
+    FH, FW = kernel_hw
+    if out_hw(IH, IW, FH, FW, stride[0], stride[1], padding[0], padding[1]) != (OH, OW):
+        raise ValueError("dY extent does not match the forward output")
+    dW = np.empty((OC, FH, FW, IC), np.float64)
+    rc = _load().oracle_conv2d_bwd_filter(xp, dyp, dW.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                          N, IH, IW, IC, OC, FH, FW, stride[0], stride[1],
+                                          padding[0], padding[1])
+    if rc:
+        raise ValueError("oracle_conv2d_bwd_filter: bad arguments")
+    return dW
+
+
+def num_threads() -> int:
+    return int(_load().oracle_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    _load().oracle_set_num_threads(int(n))
