@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""bench.py — images/s of the conv fwd+bwd step of the paper's CIFAR-10 networks on B200.
+
+Default workload (BASELINE.json configs[4], the metric's "images/s at 1/2/4/8 B200"):
+ResNet-18 CIFAR-10 conv layers, fwd + deconv (dX) + dW, GLOBAL batch 4096 sharded over
+the N ranks (strong scaling), dW all-reduced (SUM) over NCCL.  At N=1 this is the whole
+4096-image step on one GPU.  One "step" = every conv of the network forward, then dX
+(all but the stem) and dW in reverse (all §8(a) rows: A0-A8).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                  [--net resnet18|vgg16|googlenet|alexnet] [--global-batch B] [--math 3xtf32|tf32]
+
+Under torchrun (N>1) every rank runs its shard; rank 0 prints ONE JSON line.
+`--impl reference` times the CPU oracle (the reference arm for this tier) on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "conv TFLOP/s (fwd/dX/dW) on Cifar-10 layer shapes; images/s at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="smconv", choices=["smconv", "reference"])
+    ap.add_argument("--net", default="resnet18")
+    ap.add_argument("--global-batch", type=int, default=None)
+    ap.add_argument("--math", default="3xtf32", choices=["3xtf32", "tf32"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--bucket-mb", type=float, default=16.0)
+    ap.add_argument("--layers-out", default=os.path.join(ROOT, "gpurun_out", "bench_layers.json"))
+    a = ap.parse_args()
+    if a.global_batch is None:
+        a.global_batch = {"resnet18": 4096, "vgg16": 128, "googlenet": 256, "alexnet": 256}.get(a.net, 512)
+    return a
+
+
+def peaks():
+    p = {}
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        src = "measured"
+    except Exception:
+        src = "fallback"
+    hbm = float(p.get("hbm_gbs", 6650.0))
+    bf16 = float(p.get("bf16_tflops", 1590.0))
+    bf16_s = float(p.get("bf16_tflops_sustained", 1400.0))
+    # guide's nominal dense ratio tf32 : bf16 = 1.1 : 2.25 (B200_PROFILING.md)
+    r = 1.1 / 2.25
+    return {"src": src, "hbm_gbs": hbm, "tf32_burst": bf16 * r, "tf32_sustained": bf16_s * r}
+
+
+# ---------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", "clocks_%d.csv" % os.getpid())
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + q, "--format=csv,noheader,nounits",
+                                          "-i", ",".join(str(g) for g in self.gpus), "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            c = [x.strip() for x in line.split(",")]
+            if len(c) < 9:
+                continue
+            try:
+                sm.append(float(c[1]))
+                mx = float(c[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, c[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------- oracle legs
+def oracle_images_per_s(net, n_img, seed=0):
+    """Run the CPU oracle over the conv-only chain of `net` for n_img images (fwd all layers,
+    dX all but the stem, dW all); returns (seconds, threads)."""
+    import numpy as np
+
+    import oracle
+    from paper_2305_08819_b200 import nets, synth
+    L = nets.NETS[net]()
+    X = {}
+    t0 = time.perf_counter()
+    g = synth.rng(5, 0, salt=seed)
+    for i, l in enumerate(L):
+        W = synth.filters(g, l.OC, l.FH, l.FW, l.IC, l.ic_logical)
+        x = synth.activations(g, n_img, l.IH, l.IW, l.IC, l.ic_logical, stem=(i == 0))
+        y = oracle.conv2d_fwd(x, W, (l.sh, l.sw), (l.ph, l.pw))
+        X[i] = (x, W, y.astype(np.float32))
+    for i in reversed(range(len(L))):
+        l = L[i]
+        x, W, y = X[i]
+        dy = synth.activations(g, n_img, l.OH, l.OW, l.OC)
+        if i > 0:
+            oracle.conv2d_bwd_data(dy, W, (l.IH, l.IW), (l.sh, l.sw), (l.ph, l.pw))
+        oracle.conv2d_bwd_filter(x, dy, (l.FH, l.FW), (l.sh, l.sw), (l.ph, l.pw))
+    return time.perf_counter() - t0, oracle.num_threads()
+
+
+def cpu_baseline(net, target_s=15.0):
+    oracle_mod = __import__("oracle")
+    oracle_mod.build()
+    t1, thr = oracle_images_per_s(net, 1, seed=1)
+    n = max(1, min(256, int(target_s / max(t1, 1e-3))))
+    t, thr = oracle_images_per_s(net, n, seed=2)
+    return {"value": n / t, "unit": "images/s", "cores": thr, "kind": "oracle",
+            "sample": "%d image(s) through all %d %s convs (fwd, dX, dW; plain C double-accumulated "
+                      "direct loops, OpenMP over outputs), %.1f s" % (n, len(__import__(
+                          "paper_2305_08819_b200.nets", fromlist=["x"]).NETS[net]()), net, t)}
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    per_step = 2
+    t_first, thr = oracle_images_per_s(a.net, 1, seed=9)
+    per_step = max(1, min(16, int(6.0 / max(t_first, 1e-3))))
+    for w in range(a.warmup):
+        oracle_images_per_s(a.net, per_step, seed=10 + w)
+    times = []
+    for k in range(a.steps):
+        t, thr = oracle_images_per_s(a.net, per_step, seed=100 + k)
+        times.append(t)
+    tot = sum(times)
+    v = per_step * a.steps / tot
+    out = {"metric": METRIC, "value": v, "unit": "images/s", "n_gpus": a.gpus, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": 1000 * tot / a.steps, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": "%s-cifar10 conv stack fwd+dX+dW, oracle sample %d img/step (of global batch %d)"
+                                  % (a.net, per_step, a.global_batch), "global_batch": a.global_batch},
+           "cpu_baseline": {"value": v, "unit": "images/s", "cores": thr, "kind": "oracle",
+                            "sample": "%d image(s) per step through every %s conv" % (per_step, a.net)},
+           "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------- GPU arm
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_08819_b200 import build, nets
+    from paper_2305_08819_b200 import dp
+    from paper_2305_08819_b200 import smconv as sm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        print("warning: --gpus %d but WORLD_SIZE %d" % (a.gpus, world), file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    build.build()
+    sm.lib()
+    if a.global_batch % world:
+        raise SystemExit("global batch %d not divisible by %d ranks" % (a.global_batch, world))
+    B = a.global_batch // world
+    step = dp.ConvNetStep(a.net, B, dev, math=a.math, seed=1 + 0 * rank, bucket_mb=a.bucket_mb)
+    # every rank needs the same filters: seed is rank-independent; activations differ per shard
+    torch.cuda.synchronize()
+
+    def barrier():
+        if pg is not None:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(a.warmup):
+        step.step(pg)
+    torch.cuda.synchronize()
+    barrier()
+
+    clock = ClockSampler(list(range(world)) if rank == 0 else [])
+    if rank == 0:
+        clock.start()
+        time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    events = []
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.steps):
+        step.step(pg, events=events)
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if pg is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    clocks = clock.stop() if rank == 0 else None
+
+    # per-call durations inside the timed region (events on the launching stream)
+    per = {}
+    pend = {}
+    for key, ev in events:
+        k = key[:2]
+        if key[2] == 0:
+            pend[k] = ev
+        else:
+            per.setdefault(k, []).append(pend.pop(k).elapsed_time(ev))
+    layer_rows = []
+    P = peaks()
+    for (op, i), v in per.items():
+        l = step.bufs[i].layer
+        avg = sum(v) / len(v)
+        fl = nets.flops(l, B, valid=True)
+        by = nets.bytes_compulsory(l, B, op)
+        layer_rows.append({"op": op, "layer": l.name, "i": i, "ms": avg, "flops": fl, "bytes": by,
+                           "tflops": fl / avg / 1e9, "gbs": by / avg / 1e6,
+                           "plan": sm.plan_describe({"fwd": 0, "dx": 1, "dw": 2}[op], l.dims(B), step.math)})
+    layer_rows.sort(key=lambda r: -r["ms"])
+    top = layer_rows[0]
+    mathdiv = 3.0 if a.math == "3xtf32" else 1.0
+    peak_t = P["tf32_sustained"] / mathdiv
+    ridge = peak_t * 1e12 / (P["hbm_gbs"] * 1e9)
+    ai = top["flops"] / top["bytes"]
+    if ai >= ridge:
+        roof = {"bound": "tensor", "achieved": top["tflops"], "peak": peak_t, "unit": "TFLOP/s",
+                "frac": top["tflops"] / peak_t}
+    else:
+        roof = {"bound": "hbm", "achieved": top["gbs"], "peak": P["hbm_gbs"], "unit": "GB/s",
+                "frac": top["gbs"] / P["hbm_gbs"]}
+    roof["traffic"] = None
+    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            tr = json.load(open(tr_path))
+            key = "%s:%s:%s:b%d" % (a.net, top["layer"], top["op"], B)
+            roof["traffic"] = tr.get(key)
+        except Exception:
+            pass
+    roof["kernel"] = "%s %s (%s)" % (top["op"], top["layer"], top["plan"])
+    roof["peak_src"] = "%s; TF32 = bf16_tflops_sustained x 1.1/2.25%s" % (
+        P["src"], " / 3 (3xTF32 issues 3 MMAs per product)" if mathdiv == 3 else "")
+    roof["share_of_step"] = top["ms"] * a.steps / ms
+
+    imgs = a.global_batch * a.steps
+    value = imgs / (ms_max / 1000.0)
+    out = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": "%s-cifar10 conv stack fwd+dX+dW (conv-only chain), global batch %d"
+                                  % (a.net, a.global_batch),
+                      "global_batch": a.global_batch, "per_gpu_batch": B, "math": a.math,
+                      "parallelism": "dp%d" % world, "l2": "inputs larger than L2 (per-step working set "
+                      "%.1f GB >> 126 MB)" % (sum(t.numel() for b in step.bufs for t in (b.X, b.Y) if t is not None)
+                                              * 4 / 1e9),
+                      "conv_tflops_valid": step.flops(True) * world / (ms_max / a.steps / 1000) / 1e12,
+                      "conv_tflops_nominal": step.flops(False) * world / (ms_max / a.steps / 1000) / 1e12},
+           "roofline": roof, "gpu_launches": step.kernels_per_step * a.steps, "clocks": clocks}
+
+    # ---- e2e: host buffers through the public API, H2D of the step inputs + D2H of dW each step
+    if not a.no_e2e:
+        host_in = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in step.inputs]
+        for h, t in zip(host_in, step.inputs):
+            h.copy_(t)
+        host_dw = torch.empty(step.dw_flat.shape, dtype=torch.float32, pin_memory=True)
+        h2d = sum(h.numel() * 4 for h in host_in)
+        d2h = host_dw.numel() * 4
+        barrier()
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(a.steps):
+            for h, t in zip(host_in, step.inputs):
+                t.copy_(h, non_blocking=True)
+            step.step(pg)
+            host_dw.copy_(step.dw_flat, non_blocking=True)
+        f1.record()
+        torch.cuda.synchronize()
+        barrier()
+        t = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+        if pg is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out["e2e"] = {"value": imgs / (float(t.item()) / 1000.0), "unit": "images/s",
+                      "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world}
+
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(a.net)
+    if rank == 0:
+        try:
+            os.makedirs(os.path.dirname(a.layers_out), exist_ok=True)
+            json.dump({"config": out["config"], "layers": layer_rows}, open(a.layers_out, "w"), indent=1)
+        except Exception:
+            pass
+        print(json.dumps(out), flush=True)
+    if pg is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,54 @@
+/*
+ * smconv_ext.h — introspection and test hooks of libsmconv (not needed by ordinary callers).
+ *
+ * SPEC.md:48-51 gives the conv descriptor an `algorithm` override
+ * {auto, general_im2col, small_feature_direct} and SPEC.md:247,843 require the
+ * paths to be equivalent on shapes straddling the small-map threshold
+ * ("smaller than a certain threshold").  Here the override selects a
+ * kernel family of this library; the equivalence is tested in tests/.
+ */
+#ifndef SMCONV_EXT_H
+#define SMCONV_EXT_H
+
+#include <stddef.h>
+#include "smconv.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Kernel families ("variants").  AUTO = the heuristic table's choice. */
+enum {
+    CONV_VARIANT_AUTO = 0,
+    CONV_VARIANT_GENERIC = 1,   /* register-staged implicit GEMM: any IC%4 / OC%4, any geometry */
+    CONV_VARIANT_TMA = 2        /* TMA-staged implicit GEMM: channel extents multiple of 32 */
+};
+
+/* Force a variant for all subsequent calls of `op` in this process (thread-safe);
+ * CONV_VARIANT_AUTO restores the heuristic.  The environment variable
+ * SMCONV_FORCE_VARIANT="<op>:<variant>[,...]" is read once at load time.
+ * Returns CONV_EARG for an unknown op/variant. */
+int conv2d_force_variant(int op, int variant);
+
+/* Plan the call would use, as text: "variant=.. BN=.. splits=.. tiles=.. kernels=..".
+ * Returns CONV_OK and writes at most `len` bytes (NUL-terminated) into `buf`. */
+int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, int FW,
+                         int sh, int sw, int ph, int pw, int math, char* buf, size_t len);
+
+/* Number of kernels one call with these arguments enqueues (for bench gpu_launches). */
+int conv2d_plan_kernels(int op, int N, int IH, int IW, int IC, int OC, int FH, int FW,
+                        int sh, int sw, int ph, int pw, int math);
+
+/* Host-only self test of the library's index arithmetic (fast division); 0 = pass. */
+int smconv_selftest_host(void);
+
+/* TEST-ONLY precision probe: runs tiny tcgen05.mma.kind::tf32
+ * problems whose results reveal how the tensor core rounds fp32 operands to TF32 and
+ * how it rounds accumulation.  `out` is a device buffer of >= 64 floats; results are
+ * documented in csrc/probe.cu.  Synchronous. */
+int smconv_probe_tf32(float* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,175 @@
+// common.cuh — sm_100a device primitives shared by the smconv kernels:
+// mbarriers, tcgen05 (TMEM alloc, MMA kind::tf32, commit, ld), UMMA shared-memory
+// descriptors for the 128-byte-swizzled canonical layouts, TF32 rounding, fast division.
+//
+// Compile with -gencode arch=compute_100a,code=sm_100a (tcgen05 needs the "a" target).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define SMCONV_DEV __device__ __forceinline__
+#define SMCONV_HD __host__ __device__ __forceinline__
+
+namespace smconv {
+
+// ------------------------------------------------------------------ fast division
+// q = floor(n / d) for 0 <= n < 2^31 with one mul.hi (round-up multiplier method).
+struct FastDiv {
+    uint32_t d, mul, shift;
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    uint32_t s = 0;
+    while ((1ull << s) < d) ++s;
+    f.shift = s;
+    f.mul = (uint32_t)((((1ull << 32) * ((1ull << s) - d)) / d) + 1);
+    return f;
+}
+
+SMCONV_HD uint32_t umulhi32(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+    return __umulhi(a, b);
+#else
+    return (uint32_t)(((uint64_t)a * b) >> 32);
+#endif
+}
+
+SMCONV_HD uint32_t fdiv(uint32_t n, const FastDiv& f) { return (umulhi32(n, f.mul) + n) >> f.shift; }
+
+// ------------------------------------------------------------------ shared-memory helpers
+SMCONV_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+SMCONV_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+SMCONV_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+SMCONV_DEV void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+SMCONV_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+                     smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+SMCONV_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "SMCONV_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SMCONV_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Make this thread's generic-proxy shared-memory writes visible to the async proxy
+// (tensor-core operand reads, TMA).  Must precede the release (mbarrier arrive).
+SMCONV_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ------------------------------------------------------------------ tcgen05
+// TMEM allocation: executed by one full warp; writes the TMEM base address to *dst.
+SMCONV_DEV void tmem_alloc(uint32_t* dst, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+SMCONV_DEV void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+SMCONV_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+SMCONV_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// D[tmem] (+)= A[smem] * B[smem]^T, TF32 inputs, FP32 accumulate, issued by ONE thread.
+SMCONV_DEV void mma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+
+// Arrive (once) on an mbarrier when all previously issued tcgen05 ops of this thread complete.
+SMCONV_DEV void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+// 32 lanes x 32 bit, 16 consecutive columns -> 16 registers per thread (thread i = lane base + i).
+SMCONV_DEV void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+
+SMCONV_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Instruction descriptor for kind::tf32 (PTX ISA "Instruction descriptor"):
+// [4,6) D fmt (1=F32), [7,10) A fmt (2=TF32), [10,13) B fmt (2=TF32), 15 A MN-major,
+// 16 B MN-major, [17,23) N>>3, [24,29) M>>4.
+SMCONV_HD constexpr uint32_t idesc_tf32(int M, int N, bool a_mn_major, bool b_mn_major) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// Shared-memory matrix descriptor (sm_100 version bit 46).  Layout types used here:
+//  2 = SWIZZLE_128B        K-major canonical: 8-row x 128-B atoms, 16-B chunk c of row r stored at
+//                          chunk c ^ (r % 8); SBO = byte stride between 8-row groups (LBO unused).
+//  1 = SWIZZLE_128B_BASE32B MN-major canonical for 32-bit (TF32) operands: 128 B (32 elements) along
+//                          MN per K-row, 32-B chunk j of K-row k stored at chunk j ^ (k % 4);
+//                          4-row atoms, SBO = byte stride between 4-row K atoms (512 B when rows are
+//                          contiguous), LBO = byte stride between 32-element MN blocks.
+//  (tcgen05 requires the BASE32B swizzle for MN-major TF32; plain 128B swizzle is K-major only.)
+constexpr uint32_t kLayoutSW128 = 2, kLayoutSW128Base32 = 1;
+
+SMCONV_DEV uint64_t make_sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)layout << 61;
+    return d;
+}
+
+SMCONV_DEV uint64_t make_sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    return make_sdesc(saddr, lbo_bytes, sbo_bytes, kLayoutSW128);
+}
+
+// Byte offsets of one 16-byte chunk inside this library's two tile layouts (both 1024-B aligned):
+//  K-major tile  [R rows][32 k]  : chunk c (k = 4c..4c+3) of row r                 (SWIZZLE_128B)
+//  MN-major tile [32 k][MN cols] : chunk holding mn..mn+3 (mn % 4 == 0) of K-row k (SWIZZLE_128B_BASE32B);
+//                                  each 32-wide MN block is a contiguous 4 KB [32 k][128 B].
+SMCONV_HD uint32_t kmaj_off(uint32_t r, uint32_t c) { return (r >> 3) * 1024u + (r & 7u) * 128u + ((c ^ (r & 7u)) << 4); }
+SMCONV_HD uint32_t mnmaj_off(uint32_t k, uint32_t mn) {
+    return (mn >> 5) * 4096u + k * 128u + (((((mn >> 3) & 3u) ^ (k & 3u))) << 5) + (((mn >> 2) & 1u) << 4);
+}
+
+// ------------------------------------------------------------------ TF32 split
+SMCONV_DEV float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+SMCONV_DEV void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+SMCONV_DEV float4 ldg_f4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+}  // namespace smconv

@@ -1,0 +1,441 @@
+// smconv.cu — host side of libsmconv: the C ABI of include/smconv.h.
+//
+// Validation (SPEC.md:332-340 params-check), output-extent algebra
+// (reading L1), the per-shape plan ("heuristic table", north_star (c)
+// "selected, if feature maps are smaller than a certain threshold"), workspace sizing,
+// and kernel launches on the caller's stream.  No allocation, no printing, no exit.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/smconv.h"
+#include "../../include/smconv_ext.h"
+#include "conv_gen.cuh"
+#include "conv_tma.cuh"
+
+using namespace smconv;
+
+namespace {
+
+thread_local char g_detail[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_detail, sizeof g_detail, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+std::atomic<int> g_force[3] = {{CONV_VARIANT_AUTO}, {CONV_VARIANT_AUTO}, {CONV_VARIANT_AUTO}};
+std::once_flag g_env_once;
+
+void read_env_once() {
+    std::call_once(g_env_once, [] {
+        const char* e = getenv("SMCONV_FORCE_VARIANT");
+        if (!e) return;
+        std::string s(e);
+        size_t i = 0;
+        while (i < s.size()) {
+            size_t j = s.find(',', i);
+            if (j == std::string::npos) j = s.size();
+            std::string item = s.substr(i, j - i);
+            int op = -1, var = -1;
+            if (sscanf(item.c_str(), "%d:%d", &op, &var) == 2 && op >= 0 && op < 3 && var >= 0 && var <= 2)
+                g_force[op].store(var);
+            i = j + 1;
+        }
+    });
+}
+
+struct Dims {
+    int N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw, OH, OW;
+};
+
+const char* op_name(int op) {
+    return op == CONV_OP_FWD ? "conv2d_fwd" : op == CONV_OP_BWD_DATA ? "conv2d_bwd_data" : "conv2d_bwd_filter";
+}
+
+int check_dims(int op, Dims& d, int math) {
+    const char* f = (op >= 0 && op < 3) ? op_name(op) : "conv2d";
+    if (op < 0 || op > 2) return fail(CONV_EARG, "%s: unknown op %d", f, op);
+    if (math != CONV_MATH_FP32_3XTF32 && math != CONV_MATH_TF32)
+        return fail(CONV_EARG, "%s: math=%d is neither CONV_MATH_FP32_3XTF32 (0) nor CONV_MATH_TF32 (1)", f, math);
+    const int pos[9] = {d.N, d.IH, d.IW, d.IC, d.OC, d.FH, d.FW, d.sh, d.sw};
+    const char* nm[9] = {"N", "IH", "IW", "IC", "OC", "FH", "FW", "sh", "sw"};
+    for (int i = 0; i < 9; ++i)
+        if (pos[i] < 1) return fail(CONV_EARG, "%s: %s=%d must be >= 1", f, nm[i], pos[i]);
+    if (d.ph < 0 || d.pw < 0) return fail(CONV_EARG, "%s: padding (%d,%d) must be >= 0", f, d.ph, d.pw);
+    if (conv2d_out_hw(d.IH, d.IW, d.FH, d.FW, d.sh, d.sw, d.ph, d.pw, &d.OH, &d.OW) != CONV_OK)
+        return fail(CONV_EARG, "%s: output extent < 1 for IH=%d IW=%d FH=%d FW=%d s=(%d,%d) p=(%d,%d)", f, d.IH,
+                    d.IW, d.FH, d.FW, d.sh, d.sw, d.ph, d.pw);
+    if (d.IC % 4 || d.OC % 4)
+        return fail(CONV_EALIGN, "%s: IC=%d and OC=%d must be multiples of 4 (last dim padded to 4x)", f, d.IC, d.OC);
+    const long long lim = 1ll << 31;
+    const long long nx = (long long)d.N * d.IH * d.IW * d.IC, ny = (long long)d.N * d.OH * d.OW * d.OC;
+    const long long nw = (long long)d.OC * d.FH * d.FW * d.IC;
+    if (nx >= lim || ny >= lim || nw >= lim)
+        return fail(CONV_EUNSUPPORTED, "%s: tensors must have < 2^31 elements (X %lld, Y %lld, W %lld)", f, nx, ny,
+                    nw);
+    if (d.FH * d.FW > kMaxTaps) return fail(CONV_EUNSUPPORTED, "%s: FH*FW=%d > %d", f, d.FH * d.FW, kMaxTaps);
+    if (d.sh * d.sw > kMaxPhases)
+        return fail(CONV_EUNSUPPORTED, "%s: sh*sw=%d > %d stride phases", f, d.sh * d.sw, kMaxPhases);
+    if (d.ph > 127 || d.pw > 127) return fail(CONV_EUNSUPPORTED, "%s: padding > 127", f);
+    return CONV_OK;
+}
+
+bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+    const char* x = (const char*)a;
+    const char* y = (const char*)b;
+    return x < y + nb && y < x + na;
+}
+
+// ------------------------------------------------------------------ plans
+struct Plan {
+    int variant;  // CONV_VARIANT_GENERIC / CONV_VARIANT_TMA
+    int BN;
+    int planes;
+    int splits;
+    dim3 grid;
+    size_t ws_bytes;
+    long long out_elems;
+    GenParams gp;
+    TmaParams tp;
+};
+
+int pick_bn(int n) {
+    if (n <= 32) return 32;
+    if (n <= 64) return 64;
+    if (n <= 128) return 128;
+    return 256;
+}
+
+// Largest number of k-blocks (x32 reduction elements) one accumulator chain sums before
+// its partial is written out (split-K); bounds TMEM accumulation error.
+constexpr int kMaxKbPerChain = 256;
+constexpr int kSMs = 148;
+
+void fill_common(GenParams& g, const Dims& d) {
+    memset(&g, 0, sizeof g);
+    g.N = d.N; g.IH = d.IH; g.IW = d.IW; g.IC = d.IC; g.OC = d.OC; g.FH = d.FH; g.FW = d.FW;
+    g.sh = d.sh; g.sw = d.sw; g.ph = d.ph; g.pw = d.pw; g.OH = d.OH; g.OW = d.OW;
+    g.fd_N = make_fastdiv(d.N);
+    g.fd_OW = make_fastdiv(d.OW);
+    g.fd_IC = make_fastdiv(d.IC);
+    g.fd_OC = make_fastdiv(d.OC);
+    g.fd_FW = make_fastdiv(d.FW);
+}
+
+// Valid taps of an output position class — used only to estimate K for split choice.
+int est_taps(const Dims& d) {
+    // average number of in-bounds taps per output position (fwd)
+    long long cnt = 0;
+    for (int oh = 0; oh < d.OH; ++oh)
+        for (int fh = 0; fh < d.FH; ++fh) cnt += (unsigned)(oh * d.sh - d.ph + fh) < (unsigned)d.IH;
+    long long cw = 0;
+    for (int ow = 0; ow < d.OW; ++ow)
+        for (int fw = 0; fw < d.FW; ++fw) cw += (unsigned)(ow * d.sw - d.pw + fw) < (unsigned)d.IW;
+    const double avg = (double)cnt / d.OH * (double)cw / d.OW;
+    int t = (int)(avg + 0.999);
+    return t < 1 ? 1 : t;
+}
+
+int make_plan(int op, const Dims& d, int math, Plan& pl) {
+    memset(&pl, 0, sizeof pl);
+    read_env_once();
+    pl.planes = math == CONV_MATH_FP32_3XTF32 ? 2 : 1;
+    int forced = g_force[op].load();
+    const bool tma_ok = tma_supported(op, d.N, d.IC, d.OC, d.FH, d.FW, d.sh, d.sw);
+    pl.variant = forced == CONV_VARIANT_AUTO ? (tma_ok ? CONV_VARIANT_TMA : CONV_VARIANT_GENERIC) : forced;
+    if (pl.variant == CONV_VARIANT_TMA && !tma_ok)
+        return fail(CONV_EUNSUPPORTED, "%s: TMA variant forced but unsupported for this shape", op_name(op));
+
+    GenParams& g = pl.gp;
+    fill_common(g, d);
+    long long out_elems;
+    int m_tiles, n_tiles, nkb_est;
+    if (op == CONV_OP_FWD) {
+        g.M = d.N * d.OH * d.OW;
+        g.Ngemm = d.OC;
+        m_tiles = (g.M + 127) / 128;
+        pl.BN = pick_bn(g.Ngemm);
+        n_tiles = (g.Ngemm + pl.BN - 1) / pl.BN;
+        out_elems = (long long)d.N * d.OH * d.OW * d.OC;
+        nkb_est = (est_taps(d) * d.IC + 31) / 32;
+    } else if (op == CONV_OP_BWD_DATA) {
+        g.Ngemm = d.IC;
+        g.nphase = d.sh * d.sw;
+        m_tiles = 0;
+        for (int rh = 0; rh < d.sh; ++rh)
+            for (int rw = 0; rw < d.sw; ++rw) {
+                const int ph_i = rh * d.sw + rw;
+                const int IHp = (d.IH - rh + d.sh - 1) / d.sh, IWp = (d.IW - rw + d.sw - 1) / d.sw;
+                g.phase_rh[ph_i] = rh;
+                g.phase_rw[ph_i] = rw;
+                g.phase_IHp[ph_i] = IHp;
+                g.phase_IWp[ph_i] = IWp;
+                g.phase_fd_IWp[ph_i] = make_fastdiv(IWp > 0 ? IWp : 1);
+                g.phase_tile0[ph_i] = m_tiles;
+                m_tiles += (IHp * IWp * d.N + 127) / 128;
+            }
+        g.phase_tile0[g.nphase] = m_tiles;
+        pl.BN = pick_bn(g.Ngemm);
+        n_tiles = (g.Ngemm + pl.BN - 1) / pl.BN;
+        out_elems = (long long)d.N * d.IH * d.IW * d.IC;
+        const int taps_per_phase = (est_taps(d) + d.sh * d.sw - 1) / (d.sh * d.sw) * 1;
+        nkb_est = ((taps_per_phase < 1 ? 1 : taps_per_phase) * d.OC + 31) / 32;
+    } else {
+        g.M = d.OC;
+        g.Ngemm = d.FH * d.FW * d.IC;
+        g.P = d.N * d.OH * d.OW;
+        m_tiles = (d.OC + 127) / 128;
+        pl.BN = pick_bn(g.Ngemm);
+        n_tiles = (g.Ngemm + pl.BN - 1) / pl.BN;
+        out_elems = (long long)d.OC * d.FH * d.FW * d.IC;
+        nkb_est = (g.P + 31) / 32;
+    }
+    const int tiles = m_tiles * n_tiles;
+    int splits = 1;
+    if (op == CONV_OP_BWD_FILTER) {
+        const int need_prec = (nkb_est + kMaxKbPerChain - 1) / kMaxKbPerChain;
+        int fill = kSMs / tiles;
+        if (fill < 1) fill = 1;
+        splits = need_prec > fill ? need_prec : fill;
+        if (splits > nkb_est) splits = nkb_est;
+        if (splits < 1) splits = 1;
+        g.kb_per_split = (nkb_est + splits - 1) / splits;
+        splits = (nkb_est + g.kb_per_split - 1) / g.kb_per_split;
+    } else if (tiles < kSMs) {
+        splits = kSMs / tiles;
+        const int maxs = nkb_est / 4 > 1 ? nkb_est / 4 : 1;
+        if (splits > maxs) splits = maxs;
+        if (splits < 1) splits = 1;
+    }
+    g.splits = splits;
+    pl.splits = splits;
+    pl.out_elems = out_elems;
+    pl.ws_bytes = splits > 1 ? (size_t)splits * out_elems * sizeof(float) : 0;
+    g.split_stride = splits > 1 ? out_elems : 0;
+    pl.grid = dim3(m_tiles, n_tiles, splits);
+    if (pl.variant == CONV_VARIANT_TMA) {
+        int rc = tma_make_plan(op, g, pl.BN, pl.planes, pl.tp, pl.grid, g_detail, sizeof g_detail);
+        if (rc) return rc;
+    }
+    return CONV_OK;
+}
+
+// ------------------------------------------------------------------ launches
+template <int OP, int BN, int PLANES>
+int launch_gen_t(const GenParams& g, dim3 grid, cudaStream_t st) {
+    using C = GenCfg<OP, BN, PLANES>;
+    static std::atomic<unsigned long long> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_done.load() & bit)) {
+        if (cudaFuncSetAttribute(conv_gen_kernel<OP, BN, PLANES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::SMEM_BYTES) != cudaSuccess)
+            return fail(CONV_ECUDA, "cudaFuncSetAttribute(smem=%d): %s", C::SMEM_BYTES,
+                        cudaGetErrorString(cudaGetLastError()));
+        attr_done.fetch_or(bit);
+    }
+    conv_gen_kernel<OP, BN, PLANES><<<grid, C::NTHREADS, C::SMEM_BYTES, st>>>(g);
+    return CONV_OK;
+}
+
+template <int OP, int PLANES>
+int launch_gen_bn(int BN, const GenParams& g, dim3 grid, cudaStream_t st) {
+    switch (BN) {
+        case 32: return launch_gen_t<OP, 32, PLANES>(g, grid, st);
+        case 64: return launch_gen_t<OP, 64, PLANES>(g, grid, st);
+        case 128: return launch_gen_t<OP, 128, PLANES>(g, grid, st);
+        default: return launch_gen_t<OP, 256, PLANES>(g, grid, st);
+    }
+}
+
+template <int OP>
+int launch_gen_op(const Plan& pl, const GenParams& g, cudaStream_t st) {
+    return pl.planes == 2 ? launch_gen_bn<OP, 2>(pl.BN, g, pl.grid, st) : launch_gen_bn<OP, 1>(pl.BN, g, pl.grid, st);
+}
+
+int run(int op, const float* A, const float* B, float* out, const Dims& d, int math, void* ws, size_t ws_bytes,
+        conv_stream_t stream_) {
+    cudaStream_t st = (cudaStream_t)stream_;
+    Plan pl;
+    int rc = make_plan(op, d, math, pl);
+    if (rc) return rc;
+    if (pl.ws_bytes > 0 && (ws == nullptr || ws_bytes < pl.ws_bytes))
+        return fail(CONV_EWORKSPACE, "%s: workspace %zu bytes at %p, need %zu (conv2d_workspace_bytes)", op_name(op),
+                    ws_bytes, ws, pl.ws_bytes);
+    if (pl.ws_bytes > 0 && ((uintptr_t)ws & 15)) return fail(CONV_EALIGN, "%s: workspace not 16-B aligned", op_name(op));
+    GenParams g = pl.gp;
+    g.A = A;
+    g.B = B;
+    g.out = pl.splits > 1 ? (float*)ws : out;
+    cudaGetLastError();  // clear sticky-free earlier errors of the caller
+    if (pl.variant == CONV_VARIANT_TMA) {
+        TmaParams tp = pl.tp;
+        rc = tma_launch(op, pl.BN, pl.planes, g, tp, pl.grid, st, g_detail, sizeof g_detail);
+    } else if (op == CONV_OP_FWD) {
+        rc = launch_gen_op<OP_FWD>(pl, g, st);
+    } else if (op == CONV_OP_BWD_DATA) {
+        rc = launch_gen_op<OP_DX>(pl, g, st);
+    } else {
+        rc = launch_gen_op<OP_DW>(pl, g, st);
+    }
+    if (rc) return rc;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: kernel launch failed: %s", op_name(op), cudaGetErrorString(e));
+    if (pl.splits > 1) {
+        const long long n4 = pl.out_elems / 4;
+        int blocks = (int)((n4 + 255) / 256);
+        if (blocks > kSMs * 8) blocks = kSMs * 8;
+        splitk_reduce_kernel<<<blocks, 256, 0, st>>>((const float4*)ws, (float4*)out, n4, pl.splits, n4);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: reduce launch failed: %s", op_name(op), cudaGetErrorString(e));
+    }
+    g_detail[0] = 0;
+    return CONV_OK;
+}
+
+int entry(int op, const float* in0, const float* in1, float* out, Dims d, int math, void* ws, size_t ws_bytes,
+          conv_stream_t st) {
+    int rc = check_dims(op, d, math);
+    if (rc) return rc;
+    const char* f = op_name(op);
+    if (!in0 || !in1 || !out) return fail(CONV_EARG, "%s: NULL tensor pointer", f);
+    if (((uintptr_t)in0 | (uintptr_t)in1 | (uintptr_t)out) & 15)
+        return fail(CONV_EALIGN, "%s: tensor pointers must be 16-byte aligned", f);
+    const size_t bx = (size_t)d.N * d.IH * d.IW * d.IC * 4, by = (size_t)d.N * d.OH * d.OW * d.OC * 4,
+                 bw = (size_t)d.OC * d.FH * d.FW * d.IC * 4;
+    size_t b0, b1, bo;
+    if (op == CONV_OP_FWD) { b0 = bx; b1 = bw; bo = by; }
+    else if (op == CONV_OP_BWD_DATA) { b0 = by; b1 = bw; bo = bx; }
+    else { b0 = bx; b1 = by; bo = bw; }
+    if (overlap(out, bo, in0, b0) || overlap(out, bo, in1, b1))
+        return fail(CONV_EALIAS, "%s: output buffer overlaps an input buffer", f);
+    if (ws && (overlap(ws, ws_bytes, in0, b0) || overlap(ws, ws_bytes, in1, b1) || overlap(ws, ws_bytes, out, bo)))
+        return fail(CONV_EALIAS, "%s: workspace overlaps a tensor", f);
+    if (op == CONV_OP_FWD) return run(op, in0, in1, out, d, math, ws, ws_bytes, st);
+    if (op == CONV_OP_BWD_DATA) return run(op, in0, in1, out, d, math, ws, ws_bytes, st);
+    return run(op, in1, in0, out, d, math, ws, ws_bytes, st);  // dW: A = dY, B = X
+}
+
+Dims mk(int N, int IH, int IW, int IC, int OC, int FH, int FW, int sh, int sw, int ph, int pw) {
+    Dims d;
+    d.N = N; d.IH = IH; d.IW = IW; d.IC = IC; d.OC = OC; d.FH = FH; d.FW = FW;
+    d.sh = sh; d.sw = sw; d.ph = ph; d.pw = pw; d.OH = d.OW = 0;
+    return d;
+}
+
+}  // namespace
+
+extern "C" {
+
+int conv2d_out_hw(int IH, int IW, int FH, int FW, int sh, int sw, int ph, int pw, int* OH, int* OW) {
+    if (IH < 1 || IW < 1 || FH < 1 || FW < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0 || !OH || !OW)
+        return fail(CONV_EARG, "conv2d_out_hw: invalid argument");
+    const long long nh = (long long)IH + 2ll * ph - FH, nw = (long long)IW + 2ll * pw - FW;
+    if (nh < 0 || nw < 0) return fail(CONV_EARG, "conv2d_out_hw: kernel larger than padded input");
+    *OH = (int)(nh / sh + 1);
+    *OW = (int)(nw / sw + 1);
+    return CONV_OK;
+}
+
+size_t conv2d_workspace_bytes(int op, int N, int IH, int IW, int IC, int OC, int FH, int FW, int sh, int sw, int ph,
+                              int pw, int math) {
+    Dims d = mk(N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw);
+    if (check_dims(op, d, math)) return (size_t)-1;
+    Plan pl;
+    if (make_plan(op, d, math, pl)) return (size_t)-1;
+    return pl.ws_bytes;
+}
+
+int conv2d_fwd(const float* X, const float* W, float* Y, int N, int IH, int IW, int IC, int OC, int FH, int FW,
+               int sh, int sw, int ph, int pw, int math, void* ws, size_t ws_bytes, conv_stream_t st) {
+    return entry(CONV_OP_FWD, X, W, Y, mk(N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw), math, ws, ws_bytes, st);
+}
+
+int conv2d_bwd_data(const float* dY, const float* W, float* dX, int N, int IH, int IW, int IC, int OC, int FH, int FW,
+                    int sh, int sw, int ph, int pw, int math, void* ws, size_t ws_bytes, conv_stream_t st) {
+    return entry(CONV_OP_BWD_DATA, dY, W, dX, mk(N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw), math, ws, ws_bytes, st);
+}
+
+int conv2d_bwd_filter(const float* X, const float* dY, float* dW, int N, int IH, int IW, int IC, int OC, int FH,
+                      int FW, int sh, int sw, int ph, int pw, int math, void* ws, size_t ws_bytes, conv_stream_t st) {
+    return entry(CONV_OP_BWD_FILTER, X, dY, dW, mk(N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw), math, ws, ws_bytes,
+                 st);
+}
+
+const char* conv2d_strerror(int code) {
+    switch (code) {
+        case CONV_OK: return "CONV_OK";
+        case CONV_EARG: return "CONV_EARG";
+        case CONV_EALIGN: return "CONV_EALIGN";
+        case CONV_EALIAS: return "CONV_EALIAS";
+        case CONV_EWORKSPACE: return "CONV_EWORKSPACE";
+        case CONV_EUNSUPPORTED: return "CONV_EUNSUPPORTED";
+        case CONV_ECUDA: return "CONV_ECUDA";
+        default: return "CONV_UNKNOWN";
+    }
+}
+
+const char* conv2d_last_error_detail(void) { return g_detail; }
+
+int conv2d_force_variant(int op, int variant) {
+    if (op < 0 || op > 2 || variant < 0 || variant > 2) return fail(CONV_EARG, "conv2d_force_variant: bad op/variant");
+    read_env_once();
+    g_force[op].store(variant);
+    return CONV_OK;
+}
+
+int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, int FW, int sh, int sw, int ph,
+                         int pw, int math, char* buf, size_t len) {
+    Dims d = mk(N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw);
+    int rc = check_dims(op, d, math);
+    if (rc) return rc;
+    Plan pl;
+    rc = make_plan(op, d, math, pl);
+    if (rc) return rc;
+    if (buf && len)
+        snprintf(buf, len, "variant=%s BN=%d planes=%d splits=%d grid=%ux%ux%u ws=%zu kernels=%d",
+                 pl.variant == CONV_VARIANT_TMA ? "tma" : "generic", pl.BN, pl.planes, pl.splits, pl.grid.x,
+                 pl.grid.y, pl.grid.z, pl.ws_bytes, pl.splits > 1 ? 2 : 1);
+    return CONV_OK;
+}
+
+int conv2d_plan_kernels(int op, int N, int IH, int IW, int IC, int OC, int FH, int FW, int sh, int sw, int ph, int pw,
+                        int math) {
+    Dims d = mk(N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw);
+    if (check_dims(op, d, math)) return -1;
+    Plan pl;
+    if (make_plan(op, d, math, pl)) return -1;
+    return pl.splits > 1 ? 2 : 1;
+}
+
+int smconv_selftest_host(void) {
+    // fast division must equal integer division for every divisor / dividend we use
+    const uint32_t ds[] = {1, 2, 3, 4, 5, 6, 7, 8, 9, 11, 12, 16, 17, 25, 31, 32, 33, 64, 100, 121, 128, 192, 255,
+                           256, 257, 480, 512, 528, 832, 1000, 1024, 4096, 65535, 65536, 1000003};
+    for (uint32_t d : ds) {
+        FastDiv f = make_fastdiv(d);
+        uint32_t n = 0;
+        for (int i = 0; i < 200000; ++i) {
+            if (fdiv(n, f) != n / d) return 1;
+            n = (n * 1103515245u + 12345u) & 0x7FFFFFFFu;
+        }
+        for (uint32_t k = 0; k < 4096; ++k) {
+            const uint32_t m = k * d;
+            if (m >= 0x80000000u) break;
+            if (fdiv(m, f) != k || (m && fdiv(m - 1, f) != k - 1)) return 2;
+        }
+        if (fdiv(0x7FFFFFFFu, f) != 0x7FFFFFFFu / d) return 3;
+    }
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,212 @@
+"""Batch-sharded data-parallel conv step (north_star (e)).
+
+One process per GPU.  Rank r of g owns images [r*B/g, (r+1)*B/g) of the batch; the
+filters are replicated.  Forward and deconvolution (dX) are per-image independent, so
+they need no communication; dW is a sum over images, so the only collective is one
+all-reduce(SUM, fp32) of dW (reading L10: SUM, so the result equals the full-batch dW).
+All dW of the step live in ONE flat fp32 buffer in backward order, cut into buckets;
+each bucket's all-reduce is issued (async, NCCL over NVLink/NVSwitch) as soon as the
+last dW kernel writing into it has been enqueued, so it overlaps the rest of the
+backward pass.
+
+The network is a CONV-ONLY chain of the paper's CIFAR-10 layer shapes (nets.py):
+  forward:  X_{l+1} = Y_l along the main path (a 1x1 stride-2 shortcut reads its block's
+            input; its output ends there);
+  backward: dY of the last conv is the synthetic loss gradient; dY_l = dX_{l+1} along the
+            main path; a shortcut shares its block's output gradient.
+BatchNorm / ReLU / residual adds / pooling are outside the hot path
+and are not run; VGG's max-pools are replaced by fresh synthetic activations at each
+stage start (its chain breaks there).  Every conv of the network runs exactly as in a
+training step: fwd for all layers, dX for all but the stem, dW for all.
+"""
+from __future__ import annotations
+
+import math as _math
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+from . import nets, synth
+from . import smconv as sm
+
+
+@dataclass
+class LayerBuf:
+    layer: nets.Layer
+    X: object = None
+    W: object = None
+    Y: object = None
+    dY: object = None
+    dX: object = None
+    dW: object = None          # view into the flat dW buffer
+    x_src: int = -1            # index of the layer whose Y is this layer's X (-1: own buffer)
+    dy_src: int = -1           # index of the layer whose dX is this layer's dY (-1: own buffer)
+    dy_share: int = -1         # shortcut: shares dY with this layer
+    ws: object = None
+    ws_bytes: List[int] = field(default_factory=lambda: [0, 0, 0])
+
+
+def _chain_resnet(layers):
+    """(x_src, dy_src, dy_share) per layer for the conv-only ResNet chain."""
+    n = len(layers)
+    x_src, dy_src, share = [-1] * n, [-1] * n, [-1] * n
+    prev = -1            # layer whose Y is the current activation
+    block_in = -1
+    i = 0
+    while i < n:
+        name = layers[i].name
+        if name.endswith("a"):
+            block_in = prev
+        if name.endswith("sc"):
+            x_src[i] = block_in
+            i += 1
+            continue
+        x_src[i] = prev
+        prev = i
+        i += 1
+    # backward: dY_l = dX of the next main-path layer that consumes Y_l
+    for j in range(n):
+        for k in range(n):
+            if x_src[k] == j and not layers[k].name.endswith("sc"):
+                dy_src[j] = k
+    for j in range(n):
+        if layers[j].name.endswith("sc"):
+            # shortcut output feeds the block output = conv b of the same block
+            b = j + 1
+            share[j] = b
+    return x_src, dy_src, share
+
+
+def _chain_vgg(layers):
+    n = len(layers)
+    x_src, dy_src, share = [-1] * n, [-1] * n, [-1] * n
+    for i in range(1, n):
+        if layers[i].IH == layers[i - 1].OH and layers[i].IC == layers[i - 1].OC:
+            x_src[i] = i - 1
+            dy_src[i - 1] = i
+    return x_src, dy_src, share
+
+
+class ConvNetStep:
+    """Buffers + one fwd/bwd pass of a conv-only network on this rank's batch shard."""
+
+    def __init__(self, net: str, batch: int, device, math: str = "3xtf32", seed: int = 0,
+                 bucket_mb: float = 16.0, chain: bool = True):
+        import torch
+        self.torch = torch
+        self.net = net
+        self.layers = nets.NETS[net]()
+        self.batch = batch
+        self.device = device
+        self.math = sm.MATH[math]
+        L = self.layers
+        if chain and net == "resnet18":
+            xs, ds, sh = _chain_resnet(L)
+        elif chain and net == "vgg16":
+            xs, ds, sh = _chain_vgg(L)
+        else:
+            xs, ds, sh = [-1] * len(L), [-1] * len(L), [-1] * len(L)
+        self.bufs: List[LayerBuf] = []
+        f32 = torch.float32
+        # flat dW buffer in BACKWARD order (bucket = contiguous run of finished layers)
+        sizes = [l.OC * l.FH * l.FW * l.IC for l in L]
+        self.dw_flat = torch.zeros(sum(sizes), dtype=f32, device=device)
+        offs, o = {}, 0
+        for i in reversed(range(len(L))):
+            offs[i] = o
+            o += sizes[i]
+        for i, l in enumerate(L):
+            b = LayerBuf(l, x_src=xs[i], dy_src=ds[i], dy_share=sh[i])
+            X, Wt, dY = synth.torch_layer_inputs(l, batch, device, seed=seed * 1000 + i)
+            b.W = Wt
+            if b.x_src < 0:
+                b.X = X
+            b.Y = torch.empty((batch, l.OH, l.OW, l.OC), dtype=f32, device=device)
+            if i > 0:
+                b.dX = torch.empty((batch, l.IH, l.IW, l.IC), dtype=f32, device=device)
+            if b.dy_src < 0 and b.dy_share < 0:
+                b.dY = dY
+            b.dW = self.dw_flat[offs[i]:offs[i] + sizes[i]].view(l.OC, l.FH, l.FW, l.IC)
+            self.bufs.append(b)
+        for i, b in enumerate(self.bufs):
+            if b.x_src >= 0:
+                b.X = self.bufs[b.x_src].Y
+        for i in reversed(range(len(L))):
+            b = self.bufs[i]
+            if b.dy_share >= 0:
+                b.dY = self.bufs[b.dy_share].dY
+            elif b.dy_src >= 0:
+                b.dY = self.bufs[b.dy_src].dX
+        # external inputs of the step (what a user would upload): chain heads and loss gradients
+        self.inputs = [b.X for b in self.bufs if b.x_src < 0] + \
+                      [b.dY for b in self.bufs if b.dy_src < 0 and b.dy_share < 0]
+        # workspaces (split-K partials), one per layer & op, sized by the library
+        for b in self.bufs:
+            dims = b.layer.dims(batch)
+            b.ws_bytes = [sm.workspace_bytes(op, dims, self.math) for op in range(3)]
+            mx = max(b.ws_bytes)
+            b.ws = torch.empty(max(mx, 16), dtype=torch.uint8, device=device) if mx else None
+        # buckets over the backward-ordered flat buffer
+        self.buckets = []
+        lim = int(bucket_mb * (1 << 20) / 4)
+        start, acc = 0, 0
+        order = list(reversed(range(len(L))))
+        for k, i in enumerate(order):
+            acc += sizes[i]
+            if acc - start >= lim or k == len(order) - 1:
+                self.buckets.append((i, start, acc))   # flush after layer i's dW
+                start = acc
+        self.kernels_per_step = sum(
+            sm.plan_kernels(0, b.layer.dims(batch), self.math) + sm.plan_kernels(2, b.layer.dims(batch), self.math)
+            + (sm.plan_kernels(1, b.layer.dims(batch), self.math) if k > 0 else 0)
+            for k, b in enumerate(self.bufs))
+
+    # ---------------------------------------------------------------- one step
+    def _call(self, op, b: LayerBuf, a, bb, out, stream):
+        ws = b.ws
+        sm.raw_call(op, a.data_ptr(), bb.data_ptr(), out.data_ptr(), b.layer.dims(self.batch), self.math,
+                    ws.data_ptr() if (ws is not None and b.ws_bytes[op]) else 0,
+                    b.ws_bytes[op] if ws is not None else 0, stream)
+
+    def step(self, pg=None, events: Optional[list] = None):
+        """Enqueue fwd for all layers, then dX/dW in reverse with bucketed async all-reduce."""
+        torch = self.torch
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        rec = events is not None
+
+        def mark(key):
+            if rec:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                events.append((key, e))
+
+        for i, b in enumerate(self.bufs):
+            mark(("fwd", i, 0))
+            self._call(0, b, b.X, b.W, b.Y, stream)
+            mark(("fwd", i, 1))
+        handles = []
+        bk = {i: (s, e) for (i, s, e) in self.buckets}
+        for i in reversed(range(len(self.bufs))):
+            b = self.bufs[i]
+            if i > 0:
+                mark(("dx", i, 0))
+                self._call(1, b, b.dY, b.W, b.dX, stream)
+                mark(("dx", i, 1))
+            mark(("dw", i, 0))
+            self._call(2, b, b.X, b.dY, b.dW, stream)
+            mark(("dw", i, 1))
+            if pg is not None and i in bk:
+                s, e = bk[i]
+                handles.append(torch.distributed.all_reduce(self.dw_flat[s:e], async_op=True, group=pg))
+        for h in handles:
+            h.wait()
+
+    def flops(self, valid=True):
+        tot = 0
+        for k, b in enumerate(self.bufs):
+            f = nets.flops(b.layer, self.batch, valid)
+            tot += f * (3 if k > 0 else 2)
+        return tot
+
+
+def input_bytes(step: ConvNetStep) -> int:
+    return sum(t.numel() * 4 for t in step.inputs)

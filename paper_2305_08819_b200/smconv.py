@@ -1,0 +1,225 @@
+"""Thin Python binding of libsmconv (include/smconv.h): argument marshalling only.
+
+Every arithmetic step of the three operators runs in the library's sm_100a kernels;
+torch provides device memory and the current CUDA stream (north_star: "PyTorch is
+used only for device memory, streams and process groups").  There is no CPU
+fallback: if the CUDA library is missing this module raises on import-time use.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsmconv.so")
+
+CONV_OK, CONV_EARG, CONV_EALIGN, CONV_EALIAS, CONV_EWORKSPACE, CONV_EUNSUPPORTED, CONV_ECUDA = range(7)
+CONV_MATH_FP32_3XTF32, CONV_MATH_TF32 = 0, 1
+CONV_OP_FWD, CONV_OP_BWD_DATA, CONV_OP_BWD_FILTER = 0, 1, 2
+CONV_VARIANT_AUTO, CONV_VARIANT_GENERIC, CONV_VARIANT_TMA = 0, 1, 2
+MATH = {"3xtf32": CONV_MATH_FP32_3XTF32, "fp32": CONV_MATH_FP32_3XTF32, "tf32": CONV_MATH_TF32}
+
+EXPORTS = ("conv2d_out_hw", "conv2d_workspace_bytes", "conv2d_fwd", "conv2d_bwd_data", "conv2d_bwd_filter",
+           "conv2d_strerror", "conv2d_last_error_detail")
+EXT_EXPORTS = ("conv2d_force_variant", "conv2d_plan_describe", "conv2d_plan_kernels", "smconv_selftest_host",
+               "smconv_probe_tf32")
+
+
+class ConvError(RuntimeError):
+    def __init__(self, code, detail):
+        self.code = code
+        self.detail = detail
+        super().__init__("%s: %s" % (_strerror(code), detail))
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libsmconv.so (built by paper_2305_08819_b200.build / __graft_entry__.build)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise ImportError("libsmconv.so not built (%s); run `python -c \"import __graft_entry__ as g; "
+                                      "g.build()\"`" % LIB_PATH)
+                L = ctypes.CDLL(LIB_PATH)
+                I, P, Z = ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t
+                L.conv2d_out_hw.argtypes = [I] * 8 + [ctypes.POINTER(I)] * 2
+                L.conv2d_out_hw.restype = I
+                L.conv2d_workspace_bytes.argtypes = [I] * 13
+                L.conv2d_workspace_bytes.restype = Z
+                for f in ("conv2d_fwd", "conv2d_bwd_data", "conv2d_bwd_filter"):
+                    fn = getattr(L, f)
+                    fn.argtypes = [P, P, P] + [I] * 11 + [I, P, Z, P]
+                    fn.restype = I
+                L.conv2d_strerror.argtypes = [I]
+                L.conv2d_strerror.restype = ctypes.c_char_p
+                L.conv2d_last_error_detail.argtypes = []
+                L.conv2d_last_error_detail.restype = ctypes.c_char_p
+                L.conv2d_force_variant.argtypes = [I, I]
+                L.conv2d_force_variant.restype = I
+                L.conv2d_plan_describe.argtypes = [I] * 13 + [ctypes.c_char_p, Z]
+                L.conv2d_plan_describe.restype = I
+                L.conv2d_plan_kernels.argtypes = [I] * 13
+                L.conv2d_plan_kernels.restype = I
+                L.smconv_selftest_host.argtypes = []
+                L.smconv_selftest_host.restype = I
+                L.smconv_probe_tf32.argtypes = [P]
+                L.smconv_probe_tf32.restype = I
+                _lib = L
+    return _lib
+
+
+def _strerror(code):
+    try:
+        return lib().conv2d_strerror(code).decode()
+    except Exception:  # pragma: no cover
+        return "CONV_%d" % code
+
+
+def _check(rc):
+    if rc != CONV_OK:
+        raise ConvError(rc, lib().conv2d_last_error_detail().decode())
+
+
+def out_hw(IH, IW, FH, FW, stride=(1, 1), padding=(1, 1)):
+    oh, ow = ctypes.c_int(), ctypes.c_int()
+    _check(lib().conv2d_out_hw(IH, IW, FH, FW, stride[0], stride[1], padding[0], padding[1],
+                               ctypes.byref(oh), ctypes.byref(ow)))
+    return oh.value, ow.value
+
+
+def workspace_bytes(op, dims, math=CONV_MATH_FP32_3XTF32):
+    n = lib().conv2d_workspace_bytes(op, *dims, math)
+    if n == ctypes.c_size_t(-1).value:
+        buf = ctypes.create_string_buffer(8)
+        rc = lib().conv2d_plan_describe(op, *dims, math, buf, 8)  # recovers the precise status code
+        raise ConvError(rc if rc != CONV_OK else CONV_EARG, lib().conv2d_last_error_detail().decode())
+    return n
+
+
+def plan_describe(op, dims, math=CONV_MATH_FP32_3XTF32):
+    buf = ctypes.create_string_buffer(256)
+    _check(lib().conv2d_plan_describe(op, *dims, math, buf, 256))
+    return buf.value.decode()
+
+
+def plan_kernels(op, dims, math=CONV_MATH_FP32_3XTF32):
+    return int(lib().conv2d_plan_kernels(op, *dims, math))
+
+
+def force_variant(op, variant):
+    _check(lib().conv2d_force_variant(op, variant))
+
+
+def _math(m):
+    return MATH[m] if isinstance(m, str) else int(m)
+
+
+# ------------------------------------------------------------------ torch-facing API
+_ws_cache = {}
+
+
+def _workspace(nbytes, device):
+    import torch
+    if nbytes == 0:
+        return None
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _need(t, name):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+        raise ValueError("%s must be a contiguous float32 CUDA tensor" % name)
+
+
+def raw_call(op, a_ptr, b_ptr, out_ptr, dims, math, ws_ptr, ws_bytes, stream_handle):
+    """Direct C-ABI call with raw device pointers (ints) — used by bench.py's step."""
+    f = (lib().conv2d_fwd, lib().conv2d_bwd_data, lib().conv2d_bwd_filter)[op]
+    _check(f(ctypes.c_void_p(a_ptr), ctypes.c_void_p(b_ptr), ctypes.c_void_p(out_ptr), *dims, math,
+             ctypes.c_void_p(ws_ptr or 0), ws_bytes, ctypes.c_void_p(stream_handle)))
+
+
+def conv2d_fwd(x, w, stride=(1, 1), padding=(1, 1), math="3xtf32", out=None):
+    """Y[N,OH,OW,OC] = X[N,IH,IW,IC] (*) W[OC,FH,FW,IC] (include/smconv.h conv2d_fwd)."""
+    import torch
+    _need(x, "x")
+    _need(w, "w")
+    N, IH, IW, IC = x.shape
+    OC, FH, FW, _ = w.shape
+    OH, OW = out_hw(IH, IW, FH, FW, stride, padding)
+    if out is None:
+        out = torch.empty((N, OH, OW, OC), dtype=torch.float32, device=x.device)
+    dims = (N, IH, IW, IC, OC, FH, FW, stride[0], stride[1], padding[0], padding[1])
+    m = _math(math)
+    nb = workspace_bytes(CONV_OP_FWD, dims, m)
+    ws = _workspace(nb, x.device)
+    st = torch.cuda.current_stream(x.device).cuda_stream
+    _check(lib().conv2d_fwd(_ptr(x), _ptr(w), _ptr(out), *dims, m, _ptr(ws) if ws is not None else None, nb,
+                            ctypes.c_void_p(st)))
+    return out
+
+
+def conv2d_bwd_data(dy, w, input_hw, stride=(1, 1), padding=(1, 1), math="3xtf32", out=None):
+    """dX[N,IH,IW,IC] = dY (*)^T W  — deconvolution (include/smconv.h conv2d_bwd_data)."""
+    import torch
+    _need(dy, "dy")
+    _need(w, "w")
+    N, OH, OW, OC = dy.shape
+    _, FH, FW, IC = w.shape
+    IH, IW = input_hw
+    if out is None:
+        out = torch.empty((N, IH, IW, IC), dtype=torch.float32, device=dy.device)
+    dims = (N, IH, IW, IC, OC, FH, FW, stride[0], stride[1], padding[0], padding[1])
+    if out_hw(IH, IW, FH, FW, stride, padding) != (OH, OW):
+        raise ValueError("dy extent %s does not match input_hw %s" % ((OH, OW), (IH, IW)))
+    m = _math(math)
+    nb = workspace_bytes(CONV_OP_BWD_DATA, dims, m)
+    ws = _workspace(nb, dy.device)
+    st = torch.cuda.current_stream(dy.device).cuda_stream
+    _check(lib().conv2d_bwd_data(_ptr(dy), _ptr(w), _ptr(out), *dims, m, _ptr(ws) if ws is not None else None, nb,
+                                 ctypes.c_void_p(st)))
+    return out
+
+
+def conv2d_bwd_filter(x, dy, kernel_hw, stride=(1, 1), padding=(1, 1), math="3xtf32", out=None):
+    """dW[OC,FH,FW,IC] = sum_{n,oh,ow} dY x X-patch (include/smconv.h conv2d_bwd_filter)."""
+    import torch
+    _need(x, "x")
+    _need(dy, "dy")
+    N, IH, IW, IC = x.shape
+    _, OH, OW, OC = dy.shape
+    FH, FW = kernel_hw
+    if out is None:
+        out = torch.empty((OC, FH, FW, IC), dtype=torch.float32, device=x.device)
+    dims = (N, IH, IW, IC, OC, FH, FW, stride[0], stride[1], padding[0], padding[1])
+    if out_hw(IH, IW, FH, FW, stride, padding) != (OH, OW):
+        raise ValueError("dy extent does not match the forward output")
+    m = _math(math)
+    nb = workspace_bytes(CONV_OP_BWD_FILTER, dims, m)
+    ws = _workspace(nb, x.device)
+    st = torch.cuda.current_stream(x.device).cuda_stream
+    _check(lib().conv2d_bwd_filter(_ptr(x), _ptr(dy), _ptr(out), *dims, m, _ptr(ws) if ws is not None else None, nb,
+                                   ctypes.c_void_p(st)))
+    return out
+
+
+def probe_tf32():
+    """TEST-ONLY: run the tcgen05 TF32 precision probe (csrc/probe.cu); returns 64 floats."""
+    import torch
+    out = torch.full((64,), float("nan"), dtype=torch.float32, device="cuda")
+    _check(lib().smconv_probe_tf32(_ptr(out)))
+    return out.cpu().numpy()

@@ -1,0 +1,130 @@
+"""Host-side checks of the C-ABI library (no GPU needed): it loads, exports every symbol the
+headers declare, its index arithmetic self-test passes, and validation rejects bad calls
+with the documented codes before any CUDA call (SURVEY.md §8(b) contract items 1-5)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def sm():
+    from paper_2305_08819_b200 import build
+    build.build()
+    from paper_2305_08819_b200 import smconv
+    smconv.lib()
+    return smconv
+
+
+def _declared():
+    names = []
+    for h in ("smconv.h", "smconv_ext.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names += re.findall(r"^\s*(?:const\s+)?\w+\**\s+\**(\w+)\s*\(", src, flags=re.M)
+    return names
+
+
+def test_exports_every_declared_symbol(sm):
+    names = _declared()
+    assert {"conv2d_fwd", "conv2d_bwd_data", "conv2d_bwd_filter", "conv2d_out_hw",
+            "conv2d_workspace_bytes", "conv2d_strerror", "conv2d_last_error_detail"} <= set(names)
+    L = ctypes.CDLL(sm.LIB_PATH)
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(sm.EXPORTS + sm.EXT_EXPORTS) <= set(names)
+
+
+def test_library_is_sm100a(sm):
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", sm.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", sm.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass and "LDTM" in sass  # tcgen05.mma / tcgen05.ld
+
+
+def test_selftest_fastdiv(sm):
+    assert sm.lib().smconv_selftest_host() == 0
+
+
+def test_out_hw(sm):
+    assert sm.out_hw(32, 32, 3, 3, (1, 1), (1, 1)) == (32, 32)
+    assert sm.out_hw(32, 32, 3, 3, (2, 2), (1, 1)) == (16, 16)   # SPEC.md:584, floor (L1)
+    assert sm.out_hw(32, 32, 1, 1, (2, 2), (0, 0)) == (16, 16)
+    assert sm.out_hw(32, 32, 11, 11, (4, 4), (5, 5)) == (8, 8)
+    with pytest.raises(sm.ConvError) as e:
+        sm.out_hw(2, 2, 5, 5, (1, 1), (0, 0))
+    assert e.value.code == sm.CONV_EARG
+
+
+def _call(sm, op, a, b, o, dims, math=0, ws=0, nws=0):
+    f = (sm.lib().conv2d_fwd, sm.lib().conv2d_bwd_data, sm.lib().conv2d_bwd_filter)[op]
+    return f(ctypes.c_void_p(a), ctypes.c_void_p(b), ctypes.c_void_p(o), *dims, math,
+             ctypes.c_void_p(ws), nws, None)
+
+
+GOOD = (2, 8, 8, 4, 8, 3, 3, 1, 1, 1, 1)
+A, B, O = 0x100000, 0x200000, 0x300000   # fake, 16-B aligned, disjoint; never dereferenced on the error path
+
+
+@pytest.mark.parametrize("op", [0, 1, 2])
+def test_validation_codes(sm, op):
+    bad = list(GOOD)
+    bad[7] = 0  # stride 0 -> positivity error
+    assert _call(sm, op, A, B, O, bad) == sm.CONV_EARG
+    assert "sh" in sm.lib().conv2d_last_error_detail().decode()
+    bad = list(GOOD)
+    bad[9] = -1
+    assert _call(sm, op, A, B, O, bad) == sm.CONV_EARG
+    bad = list(GOOD)
+    bad[3] = 3  # IC not padded to 4x
+    assert _call(sm, op, A, B, O, bad) == sm.CONV_EALIGN
+    bad = list(GOOD)
+    bad[1], bad[2], bad[9], bad[10] = 2, 2, 0, 0  # 3x3 on 2x2 without padding -> OH < 1
+    assert _call(sm, op, A, B, O, bad) == sm.CONV_EARG
+    assert _call(sm, op, A + 4, B, O, GOOD) == sm.CONV_EALIGN
+    assert _call(sm, op, A, B, A, GOOD) == sm.CONV_EALIAS
+    assert _call(sm, op, A, B, O, GOOD, math=7) == sm.CONV_EARG
+    assert _call(sm, op, 0, B, O, GOOD) == sm.CONV_EARG
+    big = (1 << 16, 64, 64, 64, 64, 3, 3, 1, 1, 1, 1)  # 2^34 elements
+    assert _call(sm, op, A, B, O, big) == sm.CONV_EUNSUPPORTED
+
+
+def test_workspace_contract(sm):
+    # a dW with a long reduction always splits K -> needs workspace; NULL workspace is refused
+    dims = (512, 32, 32, 64, 64, 3, 3, 1, 1, 1, 1)
+    n = sm.workspace_bytes(2, dims)
+    assert n > 0
+    a, b, o = 1 << 40, 2 << 40, 3 << 40
+    assert _call(sm, 2, a, b, o, dims, ws=0, nws=0) == sm.CONV_EWORKSPACE
+    assert _call(sm, 2, a, b, o, dims, ws=4 << 40, nws=n - 16) == sm.CONV_EWORKSPACE
+    assert sm.lib().conv2d_workspace_bytes(0, 0, 8, 8, 4, 8, 3, 3, 1, 1, 1, 1, 0) == ctypes.c_size_t(-1).value
+
+
+def test_strerror(sm):
+    for c, n in enumerate(["CONV_OK", "CONV_EARG", "CONV_EALIGN", "CONV_EALIAS", "CONV_EWORKSPACE",
+                           "CONV_EUNSUPPORTED", "CONV_ECUDA"]):
+        assert sm.lib().conv2d_strerror(c).decode() == n
+    assert sm.lib().conv2d_strerror(99).decode() == "CONV_UNKNOWN"
+
+
+def test_plans_cover_network_shapes(sm):
+    from paper_2305_08819_b200 import nets
+    for name, f in nets.NETS.items():
+        for l in f():
+            for op in (0, 1, 2):
+                for math in (0, 1):
+                    d = sm.plan_describe(op, l.dims(128), math)
+                    assert "variant=" in d
+                    assert sm.plan_kernels(op, l.dims(128), math) in (1, 2)
+
+
+def test_force_variant(sm):
+    sm.force_variant(0, sm.CONV_VARIANT_GENERIC)
+    assert "generic" in sm.plan_describe(0, GOOD)
+    sm.force_variant(0, sm.CONV_VARIANT_AUTO)
+    with pytest.raises(sm.ConvError):
+        sm.force_variant(5, 0)

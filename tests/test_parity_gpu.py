@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances (north_star; reading L8 = normwise max relative error
+max|g - r| / max|r| per output tensor):  3xTF32 <= 1e-5,  TF32 <= 5e-3.
+Integer-valued inputs are exact in TF32 and every partial sum is an integer < 2^24, so
+there the GPU must equal the oracle BIT FOR BIT in both modes (pin P7).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"3xtf32": 1e-5, "tf32": 5e-3}
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import oracle
+    from paper_2305_08819_b200 import build
+    build.build()
+    from paper_2305_08819_b200 import smconv as sm
+    return torch, oracle, sm
+
+
+def normwise(got, ref):
+    den = float(np.max(np.abs(ref)))
+    num = float(np.max(np.abs(got.astype(np.float64) - ref)))
+    return num / den if den > 0 else num
+
+
+def dims_of(s):
+    return s  # (N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw)
+
+
+def gen(s, seed, integer=0, stem=False):
+    from paper_2305_08819_b200 import synth
+    N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw = s
+    OH = (IH + 2 * ph - FH) // sh + 1
+    OW = (IW + 2 * pw - FW) // sw + 1
+    g = synth.rng(9, seed)
+    X = synth.activations(g, N, IH, IW, IC, stem=stem, integer=integer)
+    W = synth.filters(g, OC, FH, FW, IC, integer=integer)
+    dY = synth.activations(g, N, OH, OW, OC, integer=integer)
+    return X, W, dY
+
+
+def gpu_all(env, s, X, W, dY, math):
+    torch, _, sm = env
+    N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw = s
+    x, w, dy = (torch.from_numpy(a).cuda() for a in (X, W, dY))
+    y = sm.conv2d_fwd(x, w, (sh, sw), (ph, pw), math=math)
+    dx = sm.conv2d_bwd_data(dy, w, (IH, IW), (sh, sw), (ph, pw), math=math)
+    dw = sm.conv2d_bwd_filter(x, dy, (FH, FW), (sh, sw), (ph, pw), math=math)
+    torch.cuda.synchronize()
+    return y.cpu().numpy(), dx.cpu().numpy(), dw.cpu().numpy()
+
+
+def oracle_all(env, s, X, W, dY):
+    _, oracle, _ = env
+    N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw = s
+    return (oracle.conv2d_fwd(X, W, (sh, sw), (ph, pw)),
+            oracle.conv2d_bwd_data(dY, W, (IH, IW), (sh, sw), (ph, pw)),
+            oracle.conv2d_bwd_filter(X, dY, (FH, FW), (sh, sw), (ph, pw)))
+
+
+CONFIG1 = (2, 8, 8, 4, 8, 3, 3, 1, 1, 1, 1)
+
+# small-but-multi-tile versions of every distinct VGG-16 / ResNet-18 shape class + edge cases
+SWEEP = [
+    CONFIG1,
+    (4, 32, 32, 4, 64, 3, 3, 1, 1, 1, 1),      # stem (IC 3->4)
+    (2, 32, 32, 64, 64, 3, 3, 1, 1, 1, 1),     # vgg2 / r.l1
+    (4, 16, 16, 64, 128, 3, 3, 1, 1, 1, 1),    # vgg3
+    (4, 16, 16, 128, 128, 3, 3, 1, 1, 1, 1),   # vgg4 / r.l2
+    (8, 8, 8, 128, 256, 3, 3, 1, 1, 1, 1),     # vgg5
+    (8, 8, 8, 256, 256, 3, 3, 1, 1, 1, 1),     # vgg6/7 / r.l3
+    (16, 4, 4, 256, 512, 3, 3, 1, 1, 1, 1),    # vgg8
+    (16, 4, 4, 512, 512, 3, 3, 1, 1, 1, 1),    # vgg9/10 / r.l4
+    (32, 2, 2, 512, 512, 3, 3, 1, 1, 1, 1),    # vgg11-13
+    (128, 2, 2, 512, 512, 3, 3, 1, 1, 1, 1),   # vgg11-13 at a batch-folded tile (N % 128 == 0)
+    (4, 32, 32, 64, 128, 3, 3, 2, 2, 1, 1),    # r.l2a 3x3 s2
+    (4, 32, 32, 64, 128, 1, 1, 2, 2, 0, 0),    # r.l2 shortcut 1x1 s2
+    (8, 16, 16, 128, 256, 3, 3, 2, 2, 1, 1),   # r.l3a
+    (8, 16, 16, 128, 256, 1, 1, 2, 2, 0, 0),   # r.l3 sc
+    (16, 8, 8, 256, 512, 3, 3, 2, 2, 1, 1),    # r.l4a
+    (16, 8, 8, 256, 512, 1, 1, 2, 2, 0, 0),    # r.l4 sc
+    (3, 7, 9, 20, 36, 3, 3, 1, 1, 1, 1),       # ragged everything, non-32 channels
+    (5, 6, 6, 48, 112, 5, 5, 1, 1, 2, 2),      # GoogLeNet-style 5x5 / non-32 channels
+    (2, 13, 13, 4, 64, 11, 11, 4, 4, 5, 5),    # AlexNet conv1 11x11 s4
+    (1, 3, 3, 8, 8, 3, 3, 1, 1, 4, 4),         # pad >= FH: many outputs only see padding
+    (130, 2, 2, 32, 36, 3, 3, 1, 1, 1, 1),     # N = 130: tiles straddle positions
+]
+
+
+def _id(s):
+    return "x".join(map(str, s))
+
+
+def test_probe_tf32_rounding(env):
+    """N8: record how tcgen05 converts fp32 operands and rounds its accumulator."""
+    _, _, sm = env
+    r = sm.probe_tf32()
+    u = 2.0 ** -23
+    conv = r[0:5]
+    print("operand conversion:", [float(v) for v in conv])
+    print("accumulate across MMAs (1 + d):", [(float(v) - 1) / u for v in r[16:21]], "ulps")
+    print("sum inside one MMA (1 + d):", [(float(v) - 1) / u for v in r[32:37]], "ulps")
+    assert np.all(r[49:64] == 0)  # D[0][1..15] must be zero: descriptor / layout sanity
+    trunc = [1.0, 1.0, 1 + 2 ** -10, 1.0, -1.0]
+    rne = [1.0, 1 + 2 ** -10, 1 + 2 ** -9, 1.0, -(1 + 2 ** -10)]
+    rna = [1 + 2 ** -10, 1 + 2 ** -10, 1 + 2 ** -9, 1.0, -(1 + 2 ** -10)]
+    assert any(np.array_equal(conv, np.array(m, np.float32)) for m in (trunc, rne, rna)), conv
+
+
+def test_config1_both_modes(env):
+    s = CONFIG1
+    X, W, dY = gen(s, 1)
+    ref = oracle_all(env, s, X, W, dY)
+    for math in ("3xtf32", "tf32"):
+        got = gpu_all(env, s, X, W, dY, math)
+        for name, g, r in zip(("fwd", "dx", "dw"), got, ref):
+            e = normwise(g, r)
+            print("config1 %s %s err %.3e" % (math, name, e))
+            assert e <= TOL[math], (math, name, e)
+
+
+@pytest.mark.parametrize("s", SWEEP, ids=_id)
+def test_integer_mode_bit_exact(env, s):
+    N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw = s
+    OH = (IH + 2 * ph - FH) // sh + 1
+    OW = (IW + 2 * pw - FW) // sw + 1
+    # keep every partial sum an integer < 2^24: |x*w| <= lim^2, K terms
+    kmax = max(FH * FW * IC, FH * FW * OC, N * OH * OW)
+    lim = 2 if kmax * 4 < 2 ** 23 else 1
+    X, W, dY = gen(s, 2, integer=lim)
+    ref = oracle_all(env, s, X, W, dY)
+    for math in ("3xtf32", "tf32"):
+        got = gpu_all(env, s, X, W, dY, math)
+        for name, g, r in zip(("fwd", "dx", "dw"), got, ref):
+            assert np.array_equal(g.astype(np.float64), r), (math, name, float(np.max(np.abs(g - r))))
+
+
+@pytest.mark.parametrize("s", SWEEP, ids=_id)
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+def test_random_within_tolerance(env, s, math):
+    stem = s[3] == 4
+    X, W, dY = gen(s, 3, stem=stem)
+    if stem:  # logical IC = 3, pad lane zero
+        X[..., 3] = 0
+        W[..., 3] = 0
+    ref = oracle_all(env, s, X, W, dY)
+    got = gpu_all(env, s, X, W, dY, math)
+    for name, g, r in zip(("fwd", "dx", "dw"), got, ref):
+        e = normwise(g, r)
+        assert e <= TOL[math], (name, e)
+    if stem:  # pad lanes of dX / dW come out exactly zero
+        assert not got[1][..., 3].any() and not got[2][..., 3].any()
+
+
+def test_deterministic(env):
+    s = (8, 8, 8, 256, 256, 3, 3, 1, 1, 1, 1)
+    X, W, dY = gen(s, 4)
+    a = gpu_all(env, s, X, W, dY, "3xtf32")
+    b = gpu_all(env, s, X, W, dY, "3xtf32")
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
+
+
+def test_adjoint_identity_on_gpu_outputs(env):
+    """<conv(X,W),G> = <X,deconv(G,W)> = <W,dW(X,G)> from GPU outputs alone (pin P2)."""
+    s = (16, 8, 8, 128, 256, 3, 3, 2, 2, 1, 1)
+    X, W, dY = gen(s, 5)
+    y, dx, dw = gpu_all(env, s, X, W, dY, "3xtf32")
+    a = float(np.sum(y.astype(np.float64) * dY))
+    b = float(np.sum(X.astype(np.float64) * dx))
+    c = float(np.sum(W.astype(np.float64) * dw))
+    scale = float(np.sum(np.abs(y.astype(np.float64)) * np.abs(dY)))
+    assert abs(a - b) <= 2e-6 * scale and abs(a - c) <= 2e-6 * scale
+
+
+def test_variants_equivalent(env):
+    """SPEC.md:247,843 path equivalence: the generic and TMA variants agree with the oracle on the
+    same inputs (when TMA serves the shape)."""
+    torch, oracle, sm = env
+    for s in [(128, 2, 2, 512, 512, 3, 3, 1, 1, 1, 1), (16, 8, 8, 256, 256, 3, 3, 1, 1, 1, 1),
+              (16, 8, 8, 256, 512, 3, 3, 2, 2, 1, 1)]:
+        X, W, dY = gen(s, 6)
+        ref = oracle_all(env, s, X, W, dY)
+        for v in (sm.CONV_VARIANT_GENERIC, sm.CONV_VARIANT_TMA):
+            for op in (0, 1, 2):
+                sm.force_variant(op, v)
+            try:
+                got = gpu_all(env, s, X, W, dY, "3xtf32")
+            except sm.ConvError as e:
+                assert e.code == sm.CONV_EUNSUPPORTED
+                continue
+            finally:
+                for op in (0, 1, 2):
+                    sm.force_variant(op, sm.CONV_VARIANT_AUTO)
+            for name, g, r in zip(("fwd", "dx", "dw"), got, ref):
+                assert normwise(g, r) <= 1e-5, (v, name)
+
+
+def test_dp_shard_sum_equals_full_batch(env):
+    """Batch sharding (north_star (e)): sum over shards of dW == full-batch dW, bit-exact on
+    integer inputs (what the NCCL all-reduce SUM computes, reading L10)."""
+    torch, oracle, sm = env
+    s = (64, 8, 8, 64, 64, 3, 3, 1, 1, 1, 1)
+    X, W, dY = gen(s, 7, integer=1)
+    x, dy = torch.from_numpy(X).cuda(), torch.from_numpy(dY).cuda()
+    full = sm.conv2d_bwd_filter(x, dy, (3, 3), math="3xtf32")
+    for g in (2, 4, 8):
+        parts = [sm.conv2d_bwd_filter(x[r * 64 // g:(r + 1) * 64 // g].contiguous(),
+                                      dy[r * 64 // g:(r + 1) * 64 // g].contiguous(), (3, 3), math="3xtf32")
+                 for r in range(g)]
+        tot = parts[0].clone()
+        for p in parts[1:]:
+            tot += p
+        assert torch.equal(tot, full)
+    assert np.array_equal(full.cpu().numpy().astype(np.float64), oracle.conv2d_bwd_filter(X, dY, (3, 3)))
+
+
+def test_errors_on_gpu_call(env):
+    torch, _, sm = env
+    buf = torch.zeros(4096, device="cuda")
+    x = buf[:512].view(2, 8, 8, 4)
+    w = torch.zeros((8, 3, 3, 4), device="cuda")
+    with pytest.raises(sm.ConvError) as e:
+        sm.conv2d_fwd(x, w, (1, 1), (1, 1), out=buf[256:1280].view(2, 8, 8, 8))
+    assert e.value.code == sm.CONV_EALIAS
