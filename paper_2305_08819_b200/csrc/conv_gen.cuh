@@ -444,6 +444,7 @@ __global__ void __launch_bounds__(GenCfg<OP, BN, PLANES>::NTHREADS, 1)
 }
 
 // Deterministic split-K reduction: out[i] = sum_{s=0..S-1} ws[s*stride + i] in fixed order.
+template <int UNUSED = 0>
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ out,
                                                             long long n4, int splits, long long stride4) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {

@@ -1,0 +1,166 @@
+// conv_tma.cu — host side of the TMA variant: eligibility, tensor-map encoding, launch.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/smconv.h"
+#include <cudaTypedefs.h>
+
+#include "conv_tma.cuh"
+
+namespace smconv {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::atomic<int> g_encode_state{0};
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    if (g_encode_state.load() == 0) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess && fn) {
+            g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+            g_encode_state.store(1);
+        } else {
+            g_encode_state.store(2);
+        }
+    }
+    return g_encode;
+}
+
+// Encode an fp32 tiled map. dims/strides/box in TMA order (dim 0 innermost, stride[0] = 4 implied).
+bool encode(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+            const uint32_t* box, CUtensorMapSwizzle sw) {
+    auto fn = encoder();
+    if (!fn) return false;
+    cuuint64_t gd[5], gs[4];
+    cuuint32_t bd[5], es[5];
+    for (int i = 0; i < rank; ++i) {
+        gd[i] = dims[i];
+        bd[i] = box[i];
+        es[i] = 1;
+    }
+    for (int i = 0; i < rank - 1; ++i) gs[i] = strides_bytes[i];
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), gd, gs, bd, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int OP, int BN, int PLANES>
+int launch_t(const TmaParams& tp, const GenParams& g, dim3 grid, cudaStream_t st, char* err, size_t errlen) {
+    using C = TmaCfg<OP, BN, PLANES>;
+    static std::atomic<unsigned long long> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_done.load() & bit)) {
+        if (cudaFuncSetAttribute(conv_tma_kernel<OP, BN, PLANES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::SMEM_BYTES) != cudaSuccess) {
+            snprintf(err, errlen, "cudaFuncSetAttribute(tma smem=%d): %s", C::SMEM_BYTES,
+                     cudaGetErrorString(cudaGetLastError()));
+            return CONV_ECUDA;
+        }
+        attr_done.fetch_or(bit);
+    }
+    conv_tma_kernel<OP, BN, PLANES><<<grid, C::NTHREADS, C::SMEM_BYTES, st>>>(tp, g);
+    return CONV_OK;
+}
+
+template <int OP, int PLANES>
+int launch_bn(int BN, const TmaParams& tp, const GenParams& g, dim3 grid, cudaStream_t st, char* err, size_t n) {
+    switch (BN) {
+        case 32: return launch_t<OP, 32, PLANES>(tp, g, grid, st, err, n);
+        case 64: return launch_t<OP, 64, PLANES>(tp, g, grid, st, err, n);
+        case 128: return launch_t<OP, 128, PLANES>(tp, g, grid, st, err, n);
+        default:
+            if (PLANES == 2) return launch_t<OP, 128, PLANES>(tp, g, grid, st, err, n);  // unreachable (BN capped)
+            return launch_t<OP, (PLANES == 2 ? 128 : 256), PLANES>(tp, g, grid, st, err, n);
+    }
+}
+
+template <int OP>
+int launch_op(int BN, int planes, const TmaParams& tp, const GenParams& g, dim3 grid, cudaStream_t st, char* err,
+              size_t n) {
+    return planes == 2 ? launch_bn<OP, 2>(BN, tp, g, grid, st, err, n) : launch_bn<OP, 1>(BN, tp, g, grid, st, err, n);
+}
+
+}  // namespace
+
+bool tma_supported(int op, int N, int IC, int OC, int FH, int FW, int sh, int sw) {
+    (void)FH; (void)FW; (void)sh; (void)sw;
+    if (N % 32) return false;
+    if (op == CONV_OP_FWD) return IC % 32 == 0;
+    return IC % 32 == 0 && OC % 32 == 0;
+}
+
+int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3& grid, char* err, size_t errlen) {
+    (void)grid;
+    memset(&tp, 0, sizeof tp);
+    tp.G = (g.N % 128 == 0) ? 128 : 32;
+    tp.chunk_kb = 8;
+    if (planes == 2 && BN > 128) {
+        snprintf(err, errlen, "tma plan: BN %d > 128 in 3xTF32", BN);
+        return CONV_EUNSUPPORTED;
+    }
+    if (op == CONV_OP_FWD) {
+        tp.CB = g.IC / 32;
+    } else if (op == CONV_OP_BWD_DATA) {
+        tp.CB = g.OC / 32;
+    } else {
+        tp.NB32 = g.N / 32;
+        // one B box per (tap, contiguous channel run): gcd(BN, IC) columns never cross a tap
+        int a = BN, b = g.IC;
+        while (b) {
+            const int t = a % b;
+            a = b;
+            b = t;
+        }
+        tp.b_box_cols = a;
+        tp.b_boxes = BN / tp.b_box_cols;
+    }
+    return CONV_OK;
+}
+
+int tma_launch(int op, int BN, int planes, const GenParams& g, TmaParams& tp, dim3 grid, cudaStream_t st, char* err,
+               size_t errlen) {
+    const uint64_t N = g.N, IH = g.IH, IW = g.IW, IC = g.IC, OC = g.OC, OH = g.OH, OW = g.OW;
+    const uint64_t T = (uint64_t)g.FH * g.FW;
+    bool ok = true;
+    if (op == CONV_OP_FWD) {
+        // A = X (IC, IW, IH, N); B = W (IC, T, OC)
+        uint64_t da[4] = {IC, IW, IH, N}, sa[3] = {IC * 4, IW * IC * 4, IH * IW * IC * 4};
+        uint32_t ba[4] = {32, 1, 1, (uint32_t)tp.G};
+        ok &= encode(&tp.mapA, g.A, 4, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B);
+        uint64_t db[3] = {IC, T, OC}, sb[2] = {IC * 4, T * IC * 4};
+        uint32_t bb[3] = {32, 1, (uint32_t)BN};
+        ok &= encode(&tp.mapB, g.B, 3, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else if (op == CONV_OP_BWD_DATA) {
+        // A = dY (OC, OW, OH, N); B = W viewed (32 ic, OC, IC/32, T), MN-major
+        uint64_t da[4] = {OC, OW, OH, N}, sa[3] = {OC * 4, OW * OC * 4, OH * OW * OC * 4};
+        uint32_t ba[4] = {32, 1, 1, (uint32_t)tp.G};
+        ok &= encode(&tp.mapA, g.A, 4, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B);
+        uint64_t db[4] = {32, OC, IC / 32, T}, sb[3] = {T * IC * 4, 128, IC * 4};
+        uint32_t bb[4] = {32, 32, (uint32_t)(BN / 32), 1};
+        ok &= encode(&tp.mapB, g.B, 4, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    } else {
+        // A = dY viewed (32 oc, N, OC/32, OH*OW), MN-major; B = X viewed (32 ic, N, IC/32, IW, IH), MN-major
+        uint64_t da[4] = {32, N, OC / 32, OH * OW}, sa[3] = {OH * OW * OC * 4, 128, OC * 4};
+        uint32_t ba[4] = {32, 32, 4, 1};
+        ok &= encode(&tp.mapA, g.A, 4, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+        uint64_t db[5] = {32, N, IC / 32, IW, IH}, sb[4] = {IH * IW * IC * 4, 128, IC * 4, IW * IC * 4};
+        uint32_t bb[5] = {32, 32, (uint32_t)(tp.b_box_cols / 32), 1, 1};
+        ok &= encode(&tp.mapB, g.B, 5, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    }
+    if (!ok) {
+        snprintf(err, errlen, "cuTensorMapEncodeTiled failed (op %d)", op);
+        return CONV_ECUDA;
+    }
+    if (op == CONV_OP_FWD) return launch_op<OP_FWD>(BN, planes, tp, g, grid, st, err, errlen);
+    if (op == CONV_OP_BWD_DATA) return launch_op<OP_DX>(BN, planes, tp, g, grid, st, err, errlen);
+    return launch_op<OP_DW>(BN, planes, tp, g, grid, st, err, errlen);
+}
+
+}  // namespace smconv

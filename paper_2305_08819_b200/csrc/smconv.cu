@@ -154,6 +154,12 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
     if (pl.variant == CONV_VARIANT_TMA && !tma_ok)
         return fail(CONV_EUNSUPPORTED, "%s: TMA variant forced but unsupported for this shape", op_name(op));
 
+    // 3xTF32 on the TMA variant promotes chunks into BN/2 fp32 registers per epilogue thread: BN <= 128
+    auto bn_for = [&](int n) {
+        int b = pick_bn(n);
+        if (pl.variant == CONV_VARIANT_TMA && pl.planes == 2 && b > 128) b = 128;
+        return b;
+    };
     GenParams& g = pl.gp;
     fill_common(g, d);
     long long out_elems;
@@ -162,7 +168,7 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
         g.M = d.N * d.OH * d.OW;
         g.Ngemm = d.OC;
         m_tiles = (g.M + 127) / 128;
-        pl.BN = pick_bn(g.Ngemm);
+        pl.BN = bn_for(g.Ngemm);
         n_tiles = (g.Ngemm + pl.BN - 1) / pl.BN;
         out_elems = (long long)d.N * d.OH * d.OW * d.OC;
         nkb_est = (est_taps(d) * d.IC + 31) / 32;
@@ -183,7 +189,7 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
                 m_tiles += (IHp * IWp * d.N + 127) / 128;
             }
         g.phase_tile0[g.nphase] = m_tiles;
-        pl.BN = pick_bn(g.Ngemm);
+        pl.BN = bn_for(g.Ngemm);
         n_tiles = (g.Ngemm + pl.BN - 1) / pl.BN;
         out_elems = (long long)d.N * d.IH * d.IW * d.IC;
         const int taps_per_phase = (est_taps(d) + d.sh * d.sw - 1) / (d.sh * d.sw) * 1;
@@ -193,7 +199,7 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
         g.Ngemm = d.FH * d.FW * d.IC;
         g.P = d.N * d.OH * d.OW;
         m_tiles = (d.OC + 127) / 128;
-        pl.BN = pick_bn(g.Ngemm);
+        pl.BN = bn_for(g.Ngemm);
         n_tiles = (g.Ngemm + pl.BN - 1) / pl.BN;
         out_elems = (long long)d.OC * d.FH * d.FW * d.IC;
         nkb_est = (g.P + 31) / 32;
@@ -294,7 +300,7 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
         const long long n4 = pl.out_elems / 4;
         int blocks = (int)((n4 + 255) / 256);
         if (blocks > kSMs * 8) blocks = kSMs * 8;
-        splitk_reduce_kernel<<<blocks, 256, 0, st>>>((const float4*)ws, (float4*)out, n4, pl.splits, n4);
+        splitk_reduce_kernel<0><<<blocks, 256, 0, st>>>((const float4*)ws, (float4*)out, n4, pl.splits, n4);
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: reduce launch failed: %s", op_name(op), cudaGetErrorString(e));
     }

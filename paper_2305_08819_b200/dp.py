@@ -45,6 +45,48 @@ class LayerBuf:
     ws_bytes: List[int] = field(default_factory=lambda: [0, 0, 0])
 
 
+def shard_range(batch: int, world: int, rank: int):
+    """Images [lo, hi) of the global batch owned by `rank` (contiguous equal shards)."""
+    if batch % world:
+        raise ValueError("global batch %d not divisible by %d ranks" % (batch, world))
+    per = batch // world
+    return rank * per, (rank + 1) * per
+
+
+def flat_offsets_backward(sizes):
+    """Offset of each layer's dW in the flat buffer laid out in BACKWARD (last layer first) order."""
+    offs, o = {}, 0
+    for i in reversed(range(len(sizes))):
+        offs[i] = o
+        o += sizes[i]
+    return offs
+
+
+def plan_buckets(sizes, bucket_elems):
+    """Cut the backward-ordered flat dW buffer into buckets of >= bucket_elems elements (the last
+    may be smaller).  Returns [(i, start, end)]: bucket [start, end) is complete once layer i's dW
+    (the last layer of the bucket in backward order) has been written."""
+    buckets, start, acc = [], 0, 0
+    order = list(reversed(range(len(sizes))))
+    for k, i in enumerate(order):
+        acc += sizes[i]
+        if acc - start >= bucket_elems or k == len(order) - 1:
+            buckets.append((i, start, acc))
+            start = acc
+    return buckets
+
+
+def allreduce_buckets(flat, buckets, pg, ready_layer=None):
+    """Issue async SUM all-reduces (reading L10) of the buckets whose last layer is `ready_layer`
+    (all buckets if None).  Returns the work handles."""
+    import torch.distributed as dist
+    hs = []
+    for (i, s, e) in buckets:
+        if ready_layer is None or i == ready_layer:
+            hs.append(dist.all_reduce(flat[s:e], op=dist.ReduceOp.SUM, async_op=True, group=pg))
+    return hs
+
+
 def _chain_resnet(layers):
     """(x_src, dy_src, dy_share) per layer for the conv-only ResNet chain."""
     n = len(layers)
@@ -110,10 +152,7 @@ class ConvNetStep:
         # flat dW buffer in BACKWARD order (bucket = contiguous run of finished layers)
         sizes = [l.OC * l.FH * l.FW * l.IC for l in L]
         self.dw_flat = torch.zeros(sum(sizes), dtype=f32, device=device)
-        offs, o = {}, 0
-        for i in reversed(range(len(L))):
-            offs[i] = o
-            o += sizes[i]
+        offs = flat_offsets_backward(sizes)
         for i, l in enumerate(L):
             b = LayerBuf(l, x_src=xs[i], dy_src=ds[i], dy_share=sh[i])
             X, Wt, dY = synth.torch_layer_inputs(l, batch, device, seed=seed * 1000 + i)
@@ -139,22 +178,15 @@ class ConvNetStep:
         # external inputs of the step (what a user would upload): chain heads and loss gradients
         self.inputs = [b.X for b in self.bufs if b.x_src < 0] + \
                       [b.dY for b in self.bufs if b.dy_src < 0 and b.dy_share < 0]
-        # workspaces (split-K partials), one per layer & op, sized by the library
+        # one split-K workspace shared by every call (they are stream-ordered), sized by the library
         for b in self.bufs:
-            dims = b.layer.dims(batch)
-            b.ws_bytes = [sm.workspace_bytes(op, dims, self.math) for op in range(3)]
-            mx = max(b.ws_bytes)
-            b.ws = torch.empty(max(mx, 16), dtype=torch.uint8, device=device) if mx else None
+            b.ws_bytes = [sm.workspace_bytes(op, b.layer.dims(batch), self.math) for op in range(3)]
+        mx = max(max(b.ws_bytes) for b in self.bufs)
+        ws = torch.empty(max(mx, 16), dtype=torch.uint8, device=device) if mx else None
+        for b in self.bufs:
+            b.ws = ws
         # buckets over the backward-ordered flat buffer
-        self.buckets = []
-        lim = int(bucket_mb * (1 << 20) / 4)
-        start, acc = 0, 0
-        order = list(reversed(range(len(L))))
-        for k, i in enumerate(order):
-            acc += sizes[i]
-            if acc - start >= lim or k == len(order) - 1:
-                self.buckets.append((i, start, acc))   # flush after layer i's dW
-                start = acc
+        self.buckets = plan_buckets(sizes, int(bucket_mb * (1 << 20) / 4))
         self.kernels_per_step = sum(
             sm.plan_kernels(0, b.layer.dims(batch), self.math) + sm.plan_kernels(2, b.layer.dims(batch), self.math)
             + (sm.plan_kernels(1, b.layer.dims(batch), self.math) if k > 0 else 0)
@@ -184,19 +216,19 @@ class ConvNetStep:
             self._call(0, b, b.X, b.W, b.Y, stream)
             mark(("fwd", i, 1))
         handles = []
-        bk = {i: (s, e) for (i, s, e) in self.buckets}
         for i in reversed(range(len(self.bufs))):
             b = self.bufs[i]
+            # dW first: its bucket's all-reduce (NCCL waits on this stream's work so far) then
+            # overlaps this layer's dX and the rest of the backward pass
+            mark(("dw", i, 0))
+            self._call(2, b, b.X, b.dY, b.dW, stream)
+            mark(("dw", i, 1))
+            if pg is not None:
+                handles += allreduce_buckets(self.dw_flat, self.buckets, pg, ready_layer=i)
             if i > 0:
                 mark(("dx", i, 0))
                 self._call(1, b, b.dY, b.W, b.dX, stream)
                 mark(("dx", i, 1))
-            mark(("dw", i, 0))
-            self._call(2, b, b.X, b.dY, b.dW, stream)
-            mark(("dw", i, 1))
-            if pg is not None and i in bk:
-                s, e = bk[i]
-                handles.append(torch.distributed.all_reduce(self.dw_flat[s:e], async_op=True, group=pg))
         for h in handles:
             h.wait()
 

@@ -231,3 +231,54 @@ def test_errors_on_gpu_call(env):
     with pytest.raises(sm.ConvError) as e:
         sm.conv2d_fwd(x, w, (1, 1), (1, 1), out=buf[256:1280].view(2, 8, 8, 8))
     assert e.value.code == sm.CONV_EALIAS
+
+
+# ---------------------------------------------------------------- TMA variant (N % 32 == 0, channels % 32 == 0)
+SWEEP_TMA = [
+    (32, 8, 8, 32, 32, 3, 3, 1, 1, 1, 1),      # smallest: one 32-image group per tile position
+    (64, 32, 32, 64, 64, 3, 3, 1, 1, 1, 1),    # r.l1 / vgg2 class, tiles straddle positions (N % 128 != 0)
+    (128, 16, 16, 64, 128, 3, 3, 1, 1, 1, 1),  # vgg3, batch-folded tiles
+    (32, 16, 16, 128, 128, 3, 3, 1, 1, 1, 1),
+    (32, 8, 8, 256, 256, 3, 3, 1, 1, 1, 1),
+    (32, 4, 4, 512, 512, 3, 3, 1, 1, 1, 1),
+    (128, 2, 2, 512, 512, 3, 3, 1, 1, 1, 1),   # vgg11-13 at b128
+    (96, 2, 2, 256, 96, 3, 3, 1, 1, 1, 1),     # ragged N tiles (96 images), OC 96
+    (32, 32, 32, 64, 128, 3, 3, 2, 2, 1, 1),   # r.l2a 3x3 s2
+    (32, 32, 32, 64, 128, 1, 1, 2, 2, 0, 0),   # r.l2 sc
+    (64, 8, 8, 256, 512, 3, 3, 2, 2, 1, 1),    # r.l4a
+    (64, 8, 8, 256, 512, 1, 1, 2, 2, 0, 0),    # r.l4 sc
+    (32, 6, 6, 96, 160, 5, 5, 1, 1, 2, 2),     # 5x5 p2, non-power-of-2 channels (multiples of 32)
+    (32, 7, 5, 32, 64, 3, 3, 2, 2, 1, 1),      # odd extents, stride 2
+]
+
+
+@pytest.fixture
+def force_tma(env):
+    _, _, sm = env
+    for op in (0, 1, 2):
+        sm.force_variant(op, sm.CONV_VARIANT_TMA)
+    yield
+    for op in (0, 1, 2):
+        sm.force_variant(op, sm.CONV_VARIANT_AUTO)
+
+
+@pytest.mark.parametrize("s", SWEEP_TMA, ids=_id)
+def test_tma_integer_bit_exact(env, force_tma, s):
+    X, W, dY = gen(s, 12, integer=1)
+    ref = oracle_all(env, s, X, W, dY)
+    for math in ("3xtf32", "tf32"):
+        got = gpu_all(env, s, X, W, dY, math)
+        for name, g, r in zip(("fwd", "dx", "dw"), got, ref):
+            assert np.array_equal(g.astype(np.float64), r), (math, name, float(np.max(np.abs(g - r))))
+
+
+@pytest.mark.parametrize("s", SWEEP_TMA, ids=_id)
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+def test_tma_random_within_tolerance(env, force_tma, s, math):
+    X, W, dY = gen(s, 13)
+    ref = oracle_all(env, s, X, W, dY)
+    got = gpu_all(env, s, X, W, dY, math)
+    for name, g, r in zip(("fwd", "dx", "dw"), got, ref):
+        e = normwise(g, r)
+        print("tma %s %s %s err %.3e" % (_id(s), math, name, e))
+        assert e <= TOL[math], (name, e)
