@@ -28,7 +28,7 @@
 
 namespace smconv {
 
-enum { OP_FWD = 0, OP_DX = 1, OP_DW = 2 };
+enum { OP_FWD = 0, OP_DX = 1, OP_DW = 2, OP_DWT = 3 };  // OP_DWT: dW with (tap,IC) rows, OC cols (TMA variant, OC <= 64)
 
 constexpr int kMaxTaps = 256;
 constexpr int kMaxPhases = 16;
@@ -44,6 +44,7 @@ struct GenParams {
     int P;       // dw: N*OH*OW (reduction length)
     int splits;
     int kb_per_split;  // dw only
+    int dwt;           // dw on the TMA variant with (tap,IC) rows x OC cols (OC <= 64): M = T*IC, Ngemm = OC
     FastDiv fd_N, fd_OW, fd_IC, fd_OC, fd_FW;
     // dx stride phases (rh, rw): rows ih = rh + sh*i', i' < IHp
     int nphase;

@@ -97,8 +97,12 @@ bool tma_supported(int op, int N, int IC, int OC, int FH, int FW, int sh, int sw
 }
 
 int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3& grid, char* err, size_t errlen) {
-    (void)grid;
     memset(&tp, 0, sizeof tp);
+    // persistent: work items (m-tile, split, n-tile), one CTA per SM walks them round-robin
+    tp.m_tiles = grid.x;
+    tp.n_tiles = grid.y;
+    tp.work = grid.x * grid.y * grid.z;
+    grid = dim3(tp.work < 148 ? tp.work : 148, 1, 1);
     tp.G = (g.N % 128 == 0) ? 128 : 32;
     tp.chunk_kb = 8;
     if (planes == 2 && BN > 128) {
@@ -111,15 +115,22 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
         tp.CB = g.OC / 32;
     } else {
         tp.NB32 = g.N / 32;
-        // one B box per (tap, contiguous channel run): gcd(BN, IC) columns never cross a tap
-        int a = BN, b = g.IC;
-        while (b) {
-            const int t = a % b;
-            a = b;
-            b = t;
+        // one X box per (tap, contiguous channel run): gcd(cols, IC) GEMM columns never cross a tap
+        auto gcd = [](int a, int b) {
+            while (b) {
+                const int t = a % b;
+                a = b;
+                b = t;
+            }
+            return a;
+        };
+        if (g.dwt) {
+            tp.a_box_cols = gcd(128, g.IC);
+            tp.a_boxes = 128 / tp.a_box_cols;
+        } else {
+            tp.b_box_cols = gcd(BN, g.IC);
+            tp.b_boxes = BN / tp.b_box_cols;
         }
-        tp.b_box_cols = a;
-        tp.b_boxes = BN / tp.b_box_cols;
     }
     return CONV_OK;
 }
@@ -145,6 +156,14 @@ int tma_launch(int op, int BN, int planes, const GenParams& g, TmaParams& tp, di
         uint64_t db[4] = {32, OC, IC / 32, T}, sb[3] = {T * IC * 4, 128, IC * 4};
         uint32_t bb[4] = {32, 32, (uint32_t)(BN / 32), 1};
         ok &= encode(&tp.mapB, g.B, 4, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    } else if (g.dwt) {
+        // transposed dW: A = X viewed (32 ic, N, IC/32, IW, IH), B = dY viewed (32 oc, N, OC/32, OH*OW)
+        uint64_t da[5] = {32, N, IC / 32, IW, IH}, sa[4] = {IH * IW * IC * 4, 128, IC * 4, IW * IC * 4};
+        uint32_t ba[5] = {32, 32, (uint32_t)(tp.a_box_cols / 32), 1, 1};
+        ok &= encode(&tp.mapA, g.B, 5, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+        uint64_t db[4] = {32, N, OC / 32, OH * OW}, sb[3] = {OH * OW * OC * 4, 128, OC * 4};
+        uint32_t bb[4] = {32, 32, (uint32_t)(BN / 32), 1};
+        ok &= encode(&tp.mapB, g.A, 4, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     } else {
         // A = dY viewed (32 oc, N, OC/32, OH*OW), MN-major; B = X viewed (32 ic, N, IC/32, IW, IH), MN-major
         uint64_t da[4] = {32, N, OC / 32, OH * OW}, sa[3] = {OH * OW * OC * 4, 128, OC * 4};
@@ -160,6 +179,7 @@ int tma_launch(int op, int BN, int planes, const GenParams& g, TmaParams& tp, di
     }
     if (op == CONV_OP_FWD) return launch_op<OP_FWD>(BN, planes, tp, g, grid, st, err, errlen);
     if (op == CONV_OP_BWD_DATA) return launch_op<OP_DX>(BN, planes, tp, g, grid, st, err, errlen);
+    if (g.dwt) return launch_op<OP_DWT>(BN, planes, tp, g, grid, st, err, errlen);
     return launch_op<OP_DW>(BN, planes, tp, g, grid, st, err, errlen);
 }
 

@@ -1,5 +1,5 @@
-// conv_tma.cuh — TMA variant: TMA-staged implicit GEMM on tcgen05 (sm_100a), the fast path for
-// channel extents that are multiples of 32 and batches that are multiples of 32.
+// conv_tma.cuh — TMA variant: persistent, warp-specialised, TMA-staged implicit GEMM on tcgen05
+// (sm_100a); the fast path for channel extents and batches that are multiples of 32.
 //
 // Same GEMM mapping as conv_gen.cuh (fwd / dX / dW; position-major "batch-folded" rows), but
 // operand tiles are moved HBM/L2 -> shared memory by the Tensor Memory Accelerator
@@ -13,19 +13,23 @@
 //   dW  B : X  as (32 ic, N, IC/32, IW, IH) box (32, 32, cols/32, 1, 1) per tap   MN-major
 //
 // Zero padding, ragged tiles and taps that fall off the map are TMA out-of-bounds zero fill
-// (CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE): no predication in the data path at all.  K-major
-// boxes use SWIZZLE_128B, MN-major boxes SWIZZLE_128B_ATOM_32B (= UMMA SWIZZLE_128B_BASE32B).
+// (CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE): no predication in the data path.  K-major boxes use
+// SWIZZLE_128B, MN-major boxes SWIZZLE_128B_ATOM_32B (= UMMA SWIZZLE_128B_BASE32B).
+//
+// Persistent CTAs (one per SM) walk the work list (m-tile, split, n-tile) round-robin.  The
+// smem stage ring, the two TMEM accumulator buffers and all mbarrier phases run continuously
+// across tiles, so the TMA of tile i+1 and its MMAs overlap the epilogue of tile i.
 //
 // Warp roles: warps 0-7 epilogue (+ accumulator promotion), warp 8 TMA producer (1 lane),
 // warp 9 TMEM owner + MMA issuer (1 lane), warps 10-13 (3xTF32 only) split converters.
 //
-// 3xTF32 here exploits what the probe measured: tcgen05 kind::tf32 reads an
-// fp32 operand by TRUNCATION to TF32, so the raw TMA tile IS a_hi = trunc_tf32(a); the
-// converters only write a_lo = a - trunc_tf32(a) (exact in fp32).  Per k-step:
-// a_lo*b_hi + a_hi*b_lo + a_hi*b_hi.  The accumulator adds by truncation too, so the K loop
-// is cut into chunks of kChunkKb k-blocks accumulated in alternating TMEM buffers and
-// promoted into fp32 registers (round-to-nearest) by the epilogue warps while the next
-// chunk runs (SURVEY.md §7 hard part 1).
+// 3xTF32 exploits what the probe measured: tcgen05 kind::tf32 reads an fp32
+// operand by TRUNCATION to TF32, so the raw TMA tile IS a_hi = trunc_tf32(a); converters only
+// write a_lo = a - trunc_tf32(a) (exact in fp32).  Per k-step: a_lo*b_hi + a_hi*b_lo + a_hi*b_hi.
+// The accumulator adds by truncation too, so K is cut into chunks of chunk_kb k-blocks that
+// alternate between the two TMEM buffers and are promoted into fp32 registers (round to
+// nearest) by the epilogue warps while the next chunk runs (SURVEY.md §7 hard part 1).
+// TF32 mode: one chunk per tile; the buffers alternate per tile.
 #pragma once
 #include <cuda.h>
 
@@ -39,15 +43,19 @@ struct __align__(64) TmaParams {
     int G;           // images per A box (fwd/dx): 128 when N % 128 == 0, else 32
     int CB;          // fwd/dx: channel blocks of 32 per tap (IC/32 resp. OC/32)
     int NB32;        // dw: N / 32 (image blocks per position)
-    int b_boxes;     // dw: B boxes (taps) per tile
-    int b_box_cols;  // dw: GEMM columns per B box
+    int b_boxes;     // dw: B boxes per tile
+    int b_box_cols;  // dw: GEMM columns per B box (never crosses a tap)
+    int a_boxes;     // dwT: A boxes (X patches) per 128-row tile
+    int a_box_cols;  // dwT: GEMM rows per A box (never crosses a tap)
     int chunk_kb;    // promotion interval in k-blocks (3xTF32)
+    int m_tiles, n_tiles;  // work decomposition (dx: m_tiles over all phases)
+    int work;        // m_tiles * splits * n_tiles
 };
 
 template <int OP, int BN, int PLANES>
 struct TmaCfg {
     static constexpr int BM = 128, BK = 32;
-    static constexpr int NEPI = 8;                       // epilogue warps 0-7
+    static constexpr int NEPI = 8;  // epilogue warps 0-7
     static constexpr int TMA_W = 8, MMA_W = 9, CONV_W0 = 10;
     static constexpr int NCONV = PLANES == 2 ? 4 : 0;
     static constexpr int NTHREADS = (10 + NCONV) * 32;
@@ -55,12 +63,13 @@ struct TmaCfg {
     static constexpr int B_BYTES = BN * BK * 4;
     static constexpr int STAGE_BYTES = PLANES * (A_BYTES + B_BYTES);
     static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-    static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
-    static constexpr bool A_MN = (OP == OP_DW);
+    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+    static constexpr bool IS_DW = (OP == OP_DW || OP == OP_DWT);
+    static constexpr bool A_MN = IS_DW;
     static constexpr bool B_MN = (OP != OP_FWD);
-    static constexpr int ACC_COLS = PLANES == 2 ? 2 * BN : BN;
+    static constexpr int ACC_COLS = 2 * BN;
     static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128 : ACC_COLS <= 256 ? 256 : 512;
-    static constexpr int AUX_BYTES = 2048 + kMaxTaps * 16;
+    static constexpr int AUX_BYTES = 1024 + kMaxTaps * 16;
     static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + AUX_BYTES;
     static_assert(STAGES >= 2, "stage does not fit");
     static_assert(PLANES == 1 || BN <= 128, "3xTF32 promotion keeps BN/2 fp32 per epilogue thread");
@@ -70,9 +79,7 @@ struct TmaAux {
     uint64_t full[8], conv[8], empty[8];
     uint64_t tfull[2], tempty[2];
     uint32_t tmem_base;
-    int ntaps;
-    int4 grp[4];          // A-box groups: {h0, w0, n0, valid}
-    int4 taps[kMaxTaps];  // {dh, dw, tapfull, 0}
+    int4 ptaps[kMaxTaps];  // producer-private per-tile tap list / X-box geometry
 };
 
 SMCONV_DEV void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, int c3) {
@@ -104,6 +111,86 @@ SMCONV_DEV void prefetch_tmap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
+// Everything a role needs to know about one work item; recomputed independently by every role
+// (cheap: at most 4 A-box groups x FH*FW taps), so no smem hand-off between roles is needed.
+template <int OP>
+struct TileInfo {
+    int phase, m0, n0, split;
+    int ngrp;
+    int4 grp[4];  // {h0, w0, n_img, valid}
+    int kb_begin, kb_end;
+
+    SMCONV_DEV void init(const TmaParams& tp, const GenParams& p, int w) {
+        const int nt = w % tp.n_tiles;
+        const int rest = w / tp.n_tiles;
+        split = rest % p.splits;
+        int mt = rest / p.splits;
+        phase = 0;
+        if (OP == OP_DX) {
+            while (phase + 1 < p.nphase && mt >= p.phase_tile0[phase + 1]) ++phase;
+            mt -= p.phase_tile0[phase];
+        }
+        constexpr bool DWK = (OP == OP_DW || OP == OP_DWT);  // reduction over pixels
+        m0 = mt * 128;
+        if (!DWK && tp.G == 128) {
+            // image-block-major walk over (128-image block, position): consecutive tiles are
+            // neighbouring positions of the same images, so the 3x3 taps' source rows are reused
+            // from L2 instead of re-read from HBM (a position-major walk thrashed L2: 3x X reads)
+            const int P = OP == OP_DX ? p.phase_IHp[phase] * p.phase_IWp[phase] : p.OH * p.OW;
+            const int ib = mt / P, pos = mt - ib * P;
+            m0 = pos * p.N + ib * 128;
+        }
+        n0 = nt;  // caller multiplies by BN
+        ngrp = 0;
+        if (!DWK) {
+            const int Mrows = OP == OP_DX ? p.phase_IHp[phase] * p.phase_IWp[phase] * p.N : p.M;
+            ngrp = 128 / tp.G;
+            for (int g = 0; g < ngrp; ++g) {
+                const int m = m0 + g * tp.G;
+                grp[g] = make_int4(-(1 << 20), -(1 << 20), 0, 0);
+                if (m < Mrows) {
+                    RowInfo ri = row_info<OP>(p, phase, m);
+                    grp[g] = make_int4(ri.h0, ri.w0, ri.n, 1);
+                }
+            }
+        }
+        int nkb;
+        if (DWK) {
+            nkb = p.OH * p.OW * tp.NB32;
+            kb_begin = split * p.kb_per_split;
+            kb_end = min(nkb, kb_begin + p.kb_per_split);
+        } else {
+            int ntaps = 0;
+            for (int fh = 0; fh < p.FH; ++fh)
+                for (int fw = 0; fw < p.FW; ++fw) ntaps += tap_valid(p, fh, fw, nullptr);
+            nkb = ntaps * tp.CB;
+            const int per = (nkb + p.splits - 1) / p.splits;
+            kb_begin = split * per;
+            kb_end = min(nkb, kb_begin + per);
+        }
+        if (kb_end < kb_begin) kb_end = kb_begin;
+    }
+
+    // Is tap (fh, fw) used by this tile (some group has its source pixel in bounds)?  If so and
+    // t != nullptr, writes {dh, dw, tapfull}.
+    SMCONV_DEV bool tap_valid(const GenParams& p, int fh, int fw, int4* t) const {
+        int dh = fh, dw = fw;
+        if (OP == OP_DX) {
+            const int th = p.phase_rh[phase] + p.ph - fh, tw = p.phase_rw[phase] + p.pw - fw;
+            if (((th % p.sh) + p.sh) % p.sh != 0 || ((tw % p.sw) + p.sw) % p.sw != 0) return false;
+            dh = th / p.sh;
+            dw = tw / p.sw;
+        }
+        const int srcH = OP == OP_FWD ? p.IH : p.OH;
+        const int srcW = OP == OP_FWD ? p.IW : p.OW;
+        bool any = false;
+        for (int g = 0; g < ngrp; ++g)
+            any |= grp[g].w && (unsigned)(grp[g].x + dh) < (unsigned)srcH && (unsigned)(grp[g].y + dw) < (unsigned)srcW;
+        if (any && t) *t = make_int4(dh, dw, fh * p.FW + fw, 0);
+        return any;
+    }
+};
+
 template <int OP, int BN, int PLANES>
 __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
     conv_tma_kernel(const __grid_constant__ TmaParams tp, const __grid_constant__ GenParams p) {
@@ -115,16 +202,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
     TmaAux* aux = reinterpret_cast<TmaAux*>(tiles_ptr + C::STAGES * C::STAGE_BYTES);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-    int phase = 0, mt = blockIdx.x;
-    if (OP == OP_DX) {
-        while (phase + 1 < p.nphase && mt >= p.phase_tile0[phase + 1]) ++phase;
-        mt -= p.phase_tile0[phase];
-    }
-    const int m0 = mt * C::BM;
-    const int n0 = blockIdx.y * BN;
-    const int split = blockIdx.z;
-    const int Mrows = OP == OP_DX ? p.phase_IHp[phase] * p.phase_IWp[phase] * p.N : p.M;
+    const int CHK = PLANES == 2 ? tp.chunk_kb : (1 << 30);
 
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
@@ -138,43 +216,6 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
         }
         fence_mbar_init();
     }
-    if (OP != OP_DW && warp == 0) {
-        // A-box groups (G images each) and the union of their valid taps
-        const int ngrp = C::BM / tp.G;
-        if (lane < ngrp) {
-            const int m = m0 + lane * tp.G;
-            int4 gi = make_int4(-(1 << 20), -(1 << 20), 0, 0);
-            if (m < Mrows) {
-                RowInfo ri = row_info<OP>(p, phase, m);
-                gi = make_int4(ri.h0, ri.w0, ri.n, 1);
-            }
-            aux->grp[lane] = gi;
-        }
-        __syncwarp();
-        const int srcH = OP == OP_FWD ? p.IH : p.OH;
-        const int srcW = OP == OP_FWD ? p.IW : p.OW;
-        int nt = 0;
-        for (int fh = 0; fh < p.FH; ++fh)
-            for (int fw = 0; fw < p.FW; ++fw) {
-                int dh = fh, dw = fw;
-                if (OP == OP_DX) {
-                    const int th = p.phase_rh[phase] + p.ph - fh, tw = p.phase_rw[phase] + p.pw - fw;
-                    if (((th % p.sh) + p.sh) % p.sh != 0 || ((tw % p.sw) + p.sw) % p.sw != 0) continue;
-                    dh = th / p.sh;
-                    dw = tw / p.sw;
-                }
-                bool any = false;
-                if (lane < ngrp) {
-                    const int4 gi = aux->grp[lane];
-                    any = gi.w && (unsigned)(gi.x + dh) < (unsigned)srcH && (unsigned)(gi.y + dw) < (unsigned)srcW;
-                }
-                if (__any_sync(0xffffffffu, any)) {
-                    if (lane == 0) aux->taps[nt] = make_int4(dh, dw, fh * p.FW + fw, 0);
-                    ++nt;
-                }
-            }
-        if (lane == 0) aux->ntaps = nt;
-    }
     if (warp == C::TMA_W && lane == 0) {
         prefetch_tmap(&tp.mapA);
         prefetch_tmap(&tp.mapB);
@@ -185,61 +226,92 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
     tc_fence_after();
     const uint32_t tmem = aux->tmem_base;
 
-    int kb_begin, kb_end;
-    {
-        int nkb;
-        if (OP == OP_DW) {
-            nkb = p.OH * p.OW * tp.NB32;
-            kb_begin = split * p.kb_per_split;
-            kb_end = min(nkb, kb_begin + p.kb_per_split);
-        } else {
-            nkb = aux->ntaps * tp.CB;
-            const int per = (nkb + p.splits - 1) / p.splits;
-            kb_begin = split * per;
-            kb_end = min(nkb, kb_begin + per);
-        }
-    }
-    const int nkb_local = max(0, kb_end - kb_begin);
-    const int CHK = PLANES == 2 ? tp.chunk_kb : (1 << 30);
-    const int nchunks = nkb_local > 0 ? (nkb_local + CHK - 1) / CHK : 0;
-
     if (warp == C::TMA_W) {
         // ======================= TMA producer
+        // The single issuing thread is on the critical path when k-blocks are short (BN = 64: one
+        // k-block is 128 tensor cycles in TF32), so per-tile bookkeeping is hoisted out of the
+        // k-loop: the tap list / box geometry is built once per tile and the loop only adds.
         if (lane == 0) {
-            for (int it = 0; it < nkb_local; ++it) {
-                const int kb = kb_begin + it;
-                const int s = it % C::STAGES, r = it / C::STAGES;
-                if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
-                const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
-                const uint32_t sB = sA + PLANES * C::A_BYTES;
+            int s = 0;
+            uint32_t r = 0;  // stage index, ring round
+            int4* taps = aux->ptaps;
+            for (int w = blockIdx.x; w < tp.work; w += gridDim.x) {
+                TileInfo<OP> ti;
+                ti.init(tp, p, w);
+                const int n0 = ti.n0 * BN;
+                const int nkb = ti.kb_end - ti.kb_begin;
+                if (nkb <= 0) continue;
                 if (OP == OP_FWD || OP == OP_DX) {
-                    const int j = kb / tp.CB, cb = kb - j * tp.CB;
-                    const int4 t = aux->taps[j];
-                    mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + C::B_BYTES);
-                    const int ngrp = C::BM / tp.G;
-                    for (int g = 0; g < ngrp; ++g) {
-                        const int4 gi = aux->grp[g];
-                        tma_load_4d(sA + g * tp.G * 128, &tp.mapA, &aux->full[s], cb * 32, gi.y + t.y, gi.x + t.x, gi.z);
+                    int nt = 0;
+                    for (int fh = 0; fh < p.FH; ++fh)
+                        for (int fw = 0; fw < p.FW; ++fw)
+                            if (ti.tap_valid(p, fh, fw, &taps[nt])) ++nt;
+                    int j = ti.kb_begin / tp.CB, cb = ti.kb_begin - j * tp.CB;
+                    int4 tap = taps[j];
+                    for (int it = 0; it < nkb; ++it) {
+                        if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
+                        const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
+                        const uint32_t sB = sA + PLANES * C::A_BYTES;
+                        mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + C::B_BYTES);
+                        for (int g = 0; g < ti.ngrp; ++g)
+                            tma_load_4d(sA + g * tp.G * 128, &tp.mapA, &aux->full[s], cb * 32, ti.grp[g].y + tap.y,
+                                        ti.grp[g].x + tap.x, ti.grp[g].z);
+                        if (OP == OP_FWD) tma_load_3d(sB, &tp.mapB, &aux->full[s], cb * 32, tap.z, n0);
+                        else tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, cb * 32, n0 / 32, tap.z);
+                        if (++cb == tp.CB) {
+                            cb = 0;
+                            tap = taps[++j < nt ? j : 0];
+                        }
+                        if (++s == C::STAGES) {
+                            s = 0;
+                            ++r;
+                        }
                     }
-                    if (OP == OP_FWD) tma_load_3d(sB, &tp.mapB, &aux->full[s], cb * 32, t.z, n0);
-                    else tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, cb * 32, n0 / 32, t.z);
                 } else {
-                    const int pos = kb / tp.NB32, nb = kb - pos * tp.NB32;
-                    const int oh = pos / p.OW, ow = pos - oh * p.OW;
+                    // image-block-major reduction order (k-block = 32 images at one position)
+                    const int P = p.OH * p.OW;
+                    int nb = ti.kb_begin / P, pos = ti.kb_begin - nb * P;
+                    int oh = pos / p.OW, ow = pos - oh * p.OW;
+                    // X boxes of this tile (dw: B side; dwT: A side): tap offsets and channel block
+                    const int nboxes = OP == OP_DWT ? tp.a_boxes : tp.b_boxes;
+                    const int bcols = OP == OP_DWT ? tp.a_box_cols : tp.b_box_cols;
+                    const int base = OP == OP_DWT ? ti.m0 : n0;
+                    const int lim = OP == OP_DWT ? p.M : p.Ngemm;
                     int nbox = 0;
-                    for (int b = 0; b < tp.b_boxes; ++b) {
-                        const int col0 = n0 + b * tp.b_box_cols;
-                        if (col0 < p.Ngemm) ++nbox;
+                    for (int b = 0; b < nboxes; ++b) {
+                        const int c0 = base + b * bcols;
+                        if (c0 >= lim) break;
+                        const int tp_ = c0 / p.IC, icb = (c0 - tp_ * p.IC) / 32;
+                        const int fh_ = tp_ / p.FW, fw_ = tp_ - fh_ * p.FW;
+                        taps[b] = make_int4(fw_ - p.pw, fh_ - p.ph, icb, 0);
+                        ++nbox;
                     }
-                    mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + nbox * tp.b_box_cols * 128);
-                    tma_load_4d(sA, &tp.mapA, &aux->full[s], 0, nb * 32, m0 / 32, pos);
-                    for (int b = 0; b < tp.b_boxes; ++b) {
-                        const int col0 = n0 + b * tp.b_box_cols;
-                        if (col0 >= p.Ngemm) break;
-                        const int tap = col0 / p.IC, icb = (col0 - tap * p.IC) / 32;
-                        const int fh = tap / p.FW, fw = tap - fh * p.FW;
-                        tma_load_5d(sB + b * tp.b_box_cols * 128, &tp.mapB, &aux->full[s], 0, nb * 32, icb,
-                                    ow * p.sw - p.pw + fw, oh * p.sh - p.ph + fh);
+                    const uint32_t xbytes = nbox * bcols * 128;
+                    const uint32_t tx = OP == OP_DWT ? xbytes + C::B_BYTES : C::A_BYTES + xbytes;
+                    for (int it = 0; it < nkb; ++it) {
+                        if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
+                        const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
+                        const uint32_t sB = sA + PLANES * C::A_BYTES;
+                        mbar_arrive_expect_tx(&aux->full[s], tx);
+                        const uint32_t sX = OP == OP_DWT ? sA : sB;
+                        const int iw0 = ow * p.sw, ih0 = oh * p.sh;
+                        for (int b = 0; b < nbox; ++b)
+                            tma_load_5d(sX + b * bcols * 128, OP == OP_DWT ? &tp.mapA : &tp.mapB, &aux->full[s], 0,
+                                        nb * 32, taps[b].z, iw0 + taps[b].x, ih0 + taps[b].y);
+                        if (OP == OP_DWT) tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, nb * 32, n0 / 32, pos);
+                        else tma_load_4d(sA, &tp.mapA, &aux->full[s], 0, nb * 32, ti.m0 / 32, pos);
+                        if (++ow == p.OW) {
+                            ow = 0;
+                            if (++oh == p.OH) oh = 0;
+                        }
+                        if (++pos == P) {
+                            pos = 0;
+                            ++nb;
+                        }
+                        if (++s == C::STAGES) {
+                            s = 0;
+                            ++r;
+                        }
                     }
                 }
             }
@@ -253,142 +325,188 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
             const uint32_t asbo = C::A_MN ? 512u : 1024u, bsbo = C::B_MN ? 512u : 1024u;
             const uint32_t alay = C::A_MN ? kLayoutSW128Base32 : kLayoutSW128;
             const uint32_t blay = C::B_MN ? kLayoutSW128Base32 : kLayoutSW128;
-            for (int it = 0; it < nkb_local; ++it) {
-                const int s = it % C::STAGES, r = it / C::STAGES;
-                const int c = it / CHK, first = (it - c * CHK) == 0;
-                const int buf = c & 1;
-                if (PLANES == 2 && first && c >= 2) {
-                    mbar_wait(&aux->tempty[buf], ((c >> 1) - 1) & 1);
-                }
-                mbar_wait(PLANES == 2 ? &aux->conv[s] : &aux->full[s], r & 1);
-                tc_fence_after();
-                const uint32_t d = tmem + (PLANES == 2 ? (uint32_t)(buf * BN) : 0u);
-                const uint32_t aH = tiles_addr + s * C::STAGE_BYTES, aL = aH + C::A_BYTES;
-                const uint32_t bH = aH + PLANES * C::A_BYTES, bL = bH + C::B_BYTES;
+            // descriptors of stage 0; stage s / k-step g only add to the 14-bit start-address field
+            const uint64_t adH0 = make_sdesc(tiles_addr, albo, asbo, alay);
+            const uint64_t bdH0 = make_sdesc(tiles_addr + PLANES * C::A_BYTES, blbo, bsbo, blay);
+            constexpr uint64_t A_LO = C::A_BYTES >> 4, B_LO = C::B_BYTES >> 4;
+            constexpr uint64_t A_G = C::A_MN ? 64 : 2, B_G = C::B_MN ? 64 : 2;  // (1024 or 32 bytes) >> 4
+            int s = 0, in_chunk = 0;
+            uint32_t r = 0, c = 0;  // stage, ring round, chunk counter (all global across tiles)
+            for (int w = blockIdx.x; w < tp.work; w += gridDim.x) {
+                TileInfo<OP> ti;
+                ti.init(tp, p, w);
+                const int nkb = ti.kb_end - ti.kb_begin;
+                for (int it = 0; it < nkb; ++it) {
+                    const int buf = c & 1;
+                    if (in_chunk == 0 && c >= 2) {
+                        mbar_wait(&aux->tempty[buf], ((c >> 1) - 1) & 1);
+                        tc_fence_after();
+                    }
+                    mbar_wait(PLANES == 2 ? &aux->conv[s] : &aux->full[s], r & 1);
+                    tc_fence_after();
+                    const uint32_t d = tmem + (uint32_t)(buf * BN);
+                    const uint64_t so = (uint64_t)(s * C::STAGE_BYTES) >> 4;
 #pragma unroll
-                for (int g = 0; g < C::BK / 8; ++g) {
-                    const uint32_t aoff = C::A_MN ? g * 1024u : g * 32u;
-                    const uint32_t boff = C::B_MN ? g * 1024u : g * 32u;
-                    const uint64_t adH = make_sdesc(aH + aoff, albo, asbo, alay);
-                    const uint64_t bdH = make_sdesc(bH + boff, blbo, bsbo, blay);
-                    const uint32_t acc0 = (PLANES == 2 ? (!first || g > 0) : (it > 0 || g > 0)) ? 1u : 0u;
-                    if (PLANES == 2) {
-                        const uint64_t adL = make_sdesc(aL + aoff, albo, asbo, alay);
-                        const uint64_t bdL = make_sdesc(bL + boff, blbo, bsbo, blay);
-                        mma_tf32_ss(d, adL, bdH, IDESC, acc0);
-                        mma_tf32_ss(d, adH, bdL, IDESC, 1u);
-                        mma_tf32_ss(d, adH, bdH, IDESC, 1u);
-                    } else {
-                        mma_tf32_ss(d, adH, bdH, IDESC, acc0);
+                    for (int g = 0; g < C::BK / 8; ++g) {
+                        const uint64_t adH = adH0 + so + g * A_G, bdH = bdH0 + so + g * B_G;
+                        const uint32_t acc0 = (in_chunk > 0 || g > 0) ? 1u : 0u;
+                        if (PLANES == 2) {
+                            mma_tf32_ss(d, adH + A_LO, bdH, IDESC, acc0);
+                            mma_tf32_ss(d, adH, bdH + B_LO, IDESC, 1u);
+                            mma_tf32_ss(d, adH, bdH, IDESC, 1u);
+                        } else {
+                            mma_tf32_ss(d, adH, bdH, IDESC, acc0);
+                        }
+                    }
+                    mma_commit(&aux->empty[s]);
+                    if (++in_chunk == CHK || it == nkb - 1) {
+                        mma_commit(&aux->tfull[buf]);
+                        ++c;
+                        in_chunk = 0;
+                    }
+                    if (++s == C::STAGES) {
+                        s = 0;
+                        ++r;
                     }
                 }
-                mma_commit(&aux->empty[s]);
-                if (PLANES == 2 && (it - c * CHK == CHK - 1 || it == nkb_local - 1)) mma_commit(&aux->tfull[buf]);
             }
-            if (PLANES == 1) mma_commit(&aux->tfull[0]);
-            if (nkb_local == 0 && PLANES == 2) mma_commit(&aux->tfull[0]);
         }
         __syncwarp();
     } else if (warp >= C::CONV_W0) {
         // ======================= 3xTF32 split converters: lo = a - trunc_tf32(a)
         const int ct = tid - C::CONV_W0 * 32;
         constexpr int NCT = C::NCONV * 32;
-        for (int it = 0; it < nkb_local; ++it) {
-            const int s = it % C::STAGES, r = it / C::STAGES;
-            mbar_wait(&aux->full[s], r & 1);
-            uint8_t* st = tiles_ptr + s * C::STAGE_BYTES;
-            const float4* aH = reinterpret_cast<const float4*>(st);
-            float4* aL = reinterpret_cast<float4*>(st + C::A_BYTES);
-            const float4* bH = reinterpret_cast<const float4*>(st + PLANES * C::A_BYTES);
-            float4* bL = reinterpret_cast<float4*>(st + PLANES * C::A_BYTES + C::B_BYTES);
+        uint32_t q = 0;
+        for (int w = blockIdx.x; w < tp.work; w += gridDim.x) {
+            TileInfo<OP> ti;
+            ti.init(tp, p, w);
+            const int nkb = ti.kb_end - ti.kb_begin;
+            for (int it = 0; it < nkb; ++it, ++q) {
+                const int s = q % C::STAGES;
+                const uint32_t r = q / C::STAGES;
+                mbar_wait(&aux->full[s], r & 1);
+                uint8_t* st = tiles_ptr + s * C::STAGE_BYTES;
+                const float4* aH = reinterpret_cast<const float4*>(st);
+                float4* aL = reinterpret_cast<float4*>(st + C::A_BYTES);
+                const float4* bH = reinterpret_cast<const float4*>(st + PLANES * C::A_BYTES);
+                float4* bL = reinterpret_cast<float4*>(st + PLANES * C::A_BYTES + C::B_BYTES);
 #pragma unroll 4
-            for (int i = ct; i < C::A_BYTES / 16; i += NCT) {
-                const float4 v = aH[i];
-                float4 o;
-                o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-                o.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-                o.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-                o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-                aL[i] = o;
-            }
+                for (int i = ct; i < C::A_BYTES / 16; i += NCT) {
+                    const float4 v = aH[i];
+                    float4 o;
+                    o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                    o.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                    o.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                    o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                    aL[i] = o;
+                }
 #pragma unroll 4
-            for (int i = ct; i < C::B_BYTES / 16; i += NCT) {
-                const float4 v = bH[i];
-                float4 o;
-                o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-                o.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-                o.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-                o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-                bL[i] = o;
+                for (int i = ct; i < C::B_BYTES / 16; i += NCT) {
+                    const float4 v = bH[i];
+                    float4 o;
+                    o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                    o.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                    o.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                    o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                    bL[i] = o;
+                }
+                fence_proxy_async_smem();
+                mbar_arrive(&aux->conv[s]);
             }
-            fence_proxy_async_smem();
-            mbar_arrive(&aux->conv[s]);
         }
     } else {
         // ======================= epilogue warps 0-7 (+ promotion of TMEM chunks, 3xTF32)
-        const int q = warp & 3, half = warp >> 2;
-        const int row = q * 32 + lane;
+        const int qd = warp & 3, half = warp >> 2;
+        const int row = qd * 32 + lane;
         constexpr int HALF = BN / 2;
-        const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-        float* outp = p.out + (long long)split * p.split_stride;
-        long long obase = -1;
-        if (OP == OP_DW) {
-            const int oc = m0 + row;
-            if (oc < p.OC) obase = (long long)oc * p.Ngemm;
-        } else {
-            RowInfo ri = row_info<OP>(p, phase, m0 + row);
-            if (ri.ok) obase = (long long)ri.orow * p.Ngemm;
-        }
-        if (PLANES == 2) {
-            float acc[HALF];
-#pragma unroll
-            for (int e = 0; e < HALF; ++e) acc[e] = 0.f;
-            for (int c = 0; c < nchunks; ++c) {
-                const int buf = c & 1;
-                mbar_wait(&aux->tfull[buf], (c >> 1) & 1);
-                tc_fence_after();
-#pragma unroll
-                for (int c0 = 0; c0 < HALF; c0 += 16) {
-                    uint32_t v[16];
-                    tmem_ld_32x32b_x16(tmem + lane_addr + (uint32_t)(buf * BN + half * HALF + c0), v);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
-                }
-                tc_fence_before();
-                mbar_arrive(&aux->tempty[buf]);
+        const uint32_t lane_addr = (uint32_t)(qd * 32) << 16;
+        uint32_t c = 0;
+        for (int w = blockIdx.x; w < tp.work; w += gridDim.x) {
+            TileInfo<OP> ti;
+            ti.init(tp, p, w);
+            const int n0 = ti.n0 * BN;
+            const int nkb = ti.kb_end - ti.kb_begin;
+            const int nch = nkb > 0 ? (nkb + CHK - 1) / CHK : 0;
+            float* outp = p.out + (long long)ti.split * p.split_stride;
+            long long obase = -1;
+            if (OP == OP_DW) {
+                const int oc = ti.m0 + row;
+                if (oc < p.OC) obase = (long long)oc * p.Ngemm;
+            } else if (OP == OP_DWT) {
+                const int m = ti.m0 + row;  // (tap, ic) index; dW[oc][m] at oc * M + m
+                if (m < p.M) obase = m;
+            } else {
+                RowInfo ri = row_info<OP>(p, ti.phase, ti.m0 + row);
+                if (ri.ok) obase = (long long)ri.orow * p.Ngemm;
             }
-            if (obase >= 0) {
-#pragma unroll
-                for (int e = 0; e < HALF; e += 4) {
-                    const int col = n0 + half * HALF + e;
-                    if (col < p.Ngemm)
-                        *reinterpret_cast<float4*>(outp + obase + col) =
-                            make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
-                }
-            }
-        } else {
-            mbar_wait(&aux->tfull[0], 0);
-            tc_fence_after();
-#pragma unroll 1
-            for (int c0 = 0; c0 < HALF; c0 += 16) {
-                uint32_t v[16];
-                if (nkb_local > 0) {
-                    tmem_ld_32x32b_x16(tmem + lane_addr + (uint32_t)(half * HALF + c0), v);
-                    tmem_ld_wait();
+            // 4 consecutive GEMM columns of this thread's row -> output
+            auto st4 = [&](int col, float x, float y, float z, float w4) {
+                if (OP == OP_DWT) {  // column = oc: a warp's 32 rows are 128 contiguous bytes per column
+                    float* o = outp + obase + (long long)col * p.M;
+                    o[0] = x;
+                    o[p.M] = y;
+                    o[2 * (long long)p.M] = z;
+                    o[3 * (long long)p.M] = w4;
                 } else {
+                    *reinterpret_cast<float4*>(outp + obase + col) = make_float4(x, y, z, w4);
+                }
+            };
+            if (PLANES == 2) {
+                float acc[HALF];
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) v[e] = 0u;
+                for (int e = 0; e < HALF; ++e) acc[e] = 0.f;
+                for (int k = 0; k < nch; ++k, ++c) {
+                    const int buf = c & 1;
+                    mbar_wait(&aux->tfull[buf], (c >> 1) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int c0 = 0; c0 < HALF; c0 += 16) {
+                        uint32_t v[16];
+                        tmem_ld_32x32b_x16(tmem + lane_addr + (uint32_t)(buf * BN + half * HALF + c0), v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
+                    }
+                    tc_fence_before();
+                    mbar_arrive(&aux->tempty[buf]);
                 }
                 if (obase >= 0) {
 #pragma unroll
-                    for (int e = 0; e < 16; e += 4) {
-                        const int col = n0 + half * HALF + c0 + e;
-                        if (col < p.Ngemm)
-                            *reinterpret_cast<float4*>(outp + obase + col) =
-                                make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
-                                            __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+                    for (int e = 0; e < HALF; e += 4) {
+                        const int col = n0 + half * HALF + e;
+                        if (col < p.Ngemm) st4(col, acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
                     }
+                }
+            } else {
+                const int buf = c & 1;
+                if (nch > 0) {
+                    mbar_wait(&aux->tfull[buf], (c >> 1) & 1);
+                    tc_fence_after();
+                }
+#pragma unroll 1
+                for (int c0 = 0; c0 < HALF; c0 += 16) {
+                    uint32_t v[16];
+                    if (nch > 0) {
+                        tmem_ld_32x32b_x16(tmem + lane_addr + (uint32_t)(buf * BN + half * HALF + c0), v);
+                        tmem_ld_wait();
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = 0u;
+                    }
+                    if (obase >= 0) {
+#pragma unroll
+                        for (int e = 0; e < 16; e += 4) {
+                            const int col = n0 + half * HALF + c0 + e;
+                            if (col < p.Ngemm)
+                                st4(col, __uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
+                                    __uint_as_float(v[e + 3]));
+                        }
+                    }
+                }
+                if (nch > 0) {
+                    tc_fence_before();
+                    mbar_arrive(&aux->tempty[buf]);
+                    ++c;
                 }
             }
         }

@@ -194,6 +194,18 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
         out_elems = (long long)d.N * d.IH * d.IW * d.IC;
         const int taps_per_phase = (est_taps(d) + d.sh * d.sw - 1) / (d.sh * d.sw) * 1;
         nkb_est = ((taps_per_phase < 1 ? 1 : taps_per_phase) * d.OC + 31) / 32;
+    } else if (pl.variant == CONV_VARIANT_TMA && d.OC <= 64 && d.FH * d.FW * d.IC >= 128) {
+        // OC <= 64 would leave half of every 128-row MMA empty: transpose the dW GEMM to
+        // (tap, IC) rows x OC columns (TMA variant only)
+        g.dwt = 1;
+        g.M = d.FH * d.FW * d.IC;
+        g.Ngemm = d.OC;
+        g.P = d.N * d.OH * d.OW;
+        m_tiles = (g.M + 127) / 128;
+        pl.BN = bn_for(g.Ngemm);
+        n_tiles = (g.Ngemm + pl.BN - 1) / pl.BN;
+        out_elems = (long long)d.OC * d.FH * d.FW * d.IC;
+        nkb_est = (g.P + 31) / 32;
     } else {
         g.M = d.OC;
         g.Ngemm = d.FH * d.FW * d.IC;
