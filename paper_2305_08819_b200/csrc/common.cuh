@@ -69,6 +69,20 @@ SMCONV_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// One lane of the (converged) warp gets true.  Issue loops for tcgen05.mma / TMA run on the
+// whole warp with warp-uniform values and issue under elect_one(): if only `lane == 0` ran the
+// loop, ptxas cannot prove the operands uniform and wraps every UTCHMMA / UTMALDG in an
+// ELECT + R2UR.BROADCAST + BRA.U.ANY waterfall (measured: ~140 issue instructions per k-block).
+SMCONV_DEV bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .b32 r;\n\t.reg .pred p;\n\t"
+        "elect.sync r|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // Make this thread's generic-proxy shared-memory writes visible to the async proxy
 // (tensor-core operand reads, TMA).  Must precede the release (mbarrier arrive).
 SMCONV_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }

@@ -396,34 +396,29 @@ __global__ void __launch_bounds__(GenCfg<OP, BN, PLANES>::NTHREADS, 1)
             }
         }
     } else if (warp == C::NLW) {
-        // ======================= MMA issuer (one lane)
-        if (lane == 0) {
-            constexpr uint32_t IDESC = idesc_tf32(128, BN, C::A_MN, C::B_MN);
-            for (int it = 0; it < nkb_local; ++it) {
-                const int s = it % C::STAGES;
-                const int round = it / C::STAGES;
-                mbar_wait(&aux->full[s], round & 1);
-                tc_fence_after();
-                const uint32_t st = tiles_addr + s * C::STAGE_BYTES;
-                const uint32_t aH = st, aL = st + C::A_BYTES;
-                const uint32_t bH = st + PLANES * C::A_BYTES, bL = bH + C::B_BYTES;
+        // ======================= MMA issuer (whole warp runs the loop, one elected lane issues)
+        constexpr uint32_t IDESC = idesc_tf32(128, BN, C::A_MN, C::B_MN);
+        // K-major: SWIZZLE_128B, SBO 1024;  MN-major: SWIZZLE_128B_BASE32B, LBO 4096, SBO 512
+        const uint64_t adH0 = make_sdesc(tiles_addr, C::A_MN ? 4096u : 16u, C::A_MN ? 512u : 1024u,
+                                         C::A_MN ? kLayoutSW128Base32 : kLayoutSW128);
+        const uint64_t bdH0 = make_sdesc(tiles_addr + PLANES * C::A_BYTES, C::B_MN ? 4096u : 16u,
+                                         C::B_MN ? 512u : 1024u, C::B_MN ? kLayoutSW128Base32 : kLayoutSW128);
+        constexpr uint64_t A_LO = C::A_BYTES >> 4, B_LO = C::B_BYTES >> 4;
+        constexpr uint64_t A_G = C::A_MN ? 64 : 2, B_G = C::B_MN ? 64 : 2;
+        for (int it = 0; it < nkb_local; ++it) {
+            const int s = it % C::STAGES;
+            const int round = it / C::STAGES;
+            mbar_wait(&aux->full[s], round & 1);
+            tc_fence_after();
+            const uint64_t so = (uint64_t)(s * C::STAGE_BYTES) >> 4;
+            if (elect_one()) {
 #pragma unroll
                 for (int g = 0; g < C::BK / 8; ++g) {
-                    const uint32_t aoff = C::A_MN ? g * 1024u : g * 32u;
-                    const uint32_t boff = C::B_MN ? g * 1024u : g * 32u;
-                    // K-major: SWIZZLE_128B, SBO 1024;  MN-major: SWIZZLE_128B_BASE32B, LBO 4096, SBO 512
-                    const uint32_t albo = C::A_MN ? 4096u : 16u, blbo = C::B_MN ? 4096u : 16u;
-                    const uint32_t asbo = C::A_MN ? 512u : 1024u, bsbo = C::B_MN ? 512u : 1024u;
-                    const uint32_t alay = C::A_MN ? kLayoutSW128Base32 : kLayoutSW128;
-                    const uint32_t blay = C::B_MN ? kLayoutSW128Base32 : kLayoutSW128;
-                    const uint64_t adH = make_sdesc(aH + aoff, albo, asbo, alay);
-                    const uint64_t bdH = make_sdesc(bH + boff, blbo, bsbo, blay);
+                    const uint64_t adH = adH0 + so + g * A_G, bdH = bdH0 + so + g * B_G;
                     const uint32_t acc0 = (it > 0 || g > 0) ? 1u : 0u;
                     if (PLANES == 2) {
-                        const uint64_t adL = make_sdesc(aL + aoff, albo, asbo, alay);
-                        const uint64_t bdL = make_sdesc(bL + boff, blbo, bsbo, blay);
-                        mma_tf32_ss(tmem, adL, bdH, IDESC, acc0);
-                        mma_tf32_ss(tmem, adH, bdL, IDESC, 1u);
+                        mma_tf32_ss(tmem, adH + A_LO, bdH, IDESC, acc0);
+                        mma_tf32_ss(tmem, adH, bdH + B_LO, IDESC, 1u);
                         mma_tf32_ss(tmem, adH, bdH, IDESC, 1u);
                     } else {
                         mma_tf32_ss(tmem, adH, bdH, IDESC, acc0);
@@ -431,8 +426,9 @@ __global__ void __launch_bounds__(GenCfg<OP, BN, PLANES>::NTHREADS, 1)
                 }
                 mma_commit(&aux->empty[s]);
             }
-            mma_commit(&aux->done);
+            __syncwarp();
         }
+        if (elect_one()) mma_commit(&aux->done);
         __syncwarp();
     }
 

@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
         // The single issuing thread is on the critical path when k-blocks are short (BN = 64: one
         // k-block is 128 tensor cycles in TF32), so per-tile bookkeeping is hoisted out of the
         // k-loop: the tap list / box geometry is built once per tile and the loop only adds.
-        if (lane == 0) {
+        {
             int s = 0;
             uint32_t r = 0;  // stage index, ring round
             int4* taps = aux->ptaps;
@@ -245,19 +245,23 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                     int nt = 0;
                     for (int fh = 0; fh < p.FH; ++fh)
                         for (int fw = 0; fw < p.FW; ++fw)
-                            if (ti.tap_valid(p, fh, fw, &taps[nt])) ++nt;
+                            if (ti.tap_valid(p, fh, fw, &taps[nt])) ++nt;  // same value from every lane
+                    __syncwarp();
                     int j = ti.kb_begin / tp.CB, cb = ti.kb_begin - j * tp.CB;
                     int4 tap = taps[j];
                     for (int it = 0; it < nkb; ++it) {
                         if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
                         const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
                         const uint32_t sB = sA + PLANES * C::A_BYTES;
-                        mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + C::B_BYTES);
-                        for (int g = 0; g < ti.ngrp; ++g)
-                            tma_load_4d(sA + g * tp.G * 128, &tp.mapA, &aux->full[s], cb * 32, ti.grp[g].y + tap.y,
-                                        ti.grp[g].x + tap.x, ti.grp[g].z);
-                        if (OP == OP_FWD) tma_load_3d(sB, &tp.mapB, &aux->full[s], cb * 32, tap.z, n0);
-                        else tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, cb * 32, n0 / 32, tap.z);
+                        if (elect_one()) {
+                            mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + C::B_BYTES);
+                            for (int g = 0; g < ti.ngrp; ++g)
+                                tma_load_4d(sA + g * tp.G * 128, &tp.mapA, &aux->full[s], cb * 32,
+                                            ti.grp[g].y + tap.y, ti.grp[g].x + tap.x, ti.grp[g].z);
+                            if (OP == OP_FWD) tma_load_3d(sB, &tp.mapB, &aux->full[s], cb * 32, tap.z, n0);
+                            else tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, cb * 32, n0 / 32, tap.z);
+                        }
+                        __syncwarp();
                         if (++cb == tp.CB) {
                             cb = 0;
                             tap = taps[++j < nt ? j : 0];
@@ -283,23 +287,27 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                         if (c0 >= lim) break;
                         const int tp_ = c0 / p.IC, icb = (c0 - tp_ * p.IC) / 32;
                         const int fh_ = tp_ / p.FW, fw_ = tp_ - fh_ * p.FW;
-                        taps[b] = make_int4(fw_ - p.pw, fh_ - p.ph, icb, 0);
+                        taps[b] = make_int4(fw_ - p.pw, fh_ - p.ph, icb, 0);  // same value from every lane
                         ++nbox;
                     }
+                    __syncwarp();
                     const uint32_t xbytes = nbox * bcols * 128;
                     const uint32_t tx = OP == OP_DWT ? xbytes + C::B_BYTES : C::A_BYTES + xbytes;
                     for (int it = 0; it < nkb; ++it) {
                         if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
                         const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
                         const uint32_t sB = sA + PLANES * C::A_BYTES;
-                        mbar_arrive_expect_tx(&aux->full[s], tx);
                         const uint32_t sX = OP == OP_DWT ? sA : sB;
                         const int iw0 = ow * p.sw, ih0 = oh * p.sh;
-                        for (int b = 0; b < nbox; ++b)
-                            tma_load_5d(sX + b * bcols * 128, OP == OP_DWT ? &tp.mapA : &tp.mapB, &aux->full[s], 0,
-                                        nb * 32, taps[b].z, iw0 + taps[b].x, ih0 + taps[b].y);
-                        if (OP == OP_DWT) tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, nb * 32, n0 / 32, pos);
-                        else tma_load_4d(sA, &tp.mapA, &aux->full[s], 0, nb * 32, ti.m0 / 32, pos);
+                        if (elect_one()) {
+                            mbar_arrive_expect_tx(&aux->full[s], tx);
+                            for (int b = 0; b < nbox; ++b)
+                                tma_load_5d(sX + b * bcols * 128, OP == OP_DWT ? &tp.mapA : &tp.mapB, &aux->full[s],
+                                            0, nb * 32, taps[b].z, iw0 + taps[b].x, ih0 + taps[b].y);
+                            if (OP == OP_DWT) tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, nb * 32, n0 / 32, pos);
+                            else tma_load_4d(sA, &tp.mapA, &aux->full[s], 0, nb * 32, ti.m0 / 32, pos);
+                        }
+                        __syncwarp();
                         if (++ow == p.OW) {
                             ow = 0;
                             if (++oh == p.OH) oh = 0;
@@ -318,8 +326,8 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
         }
         __syncwarp();
     } else if (warp == C::MMA_W) {
-        // ======================= MMA issuer
-        if (lane == 0) {
+        // ======================= MMA issuer (whole warp runs the loop, one elected lane issues)
+        {
             constexpr uint32_t IDESC = idesc_tf32(128, BN, C::A_MN, C::B_MN);
             const uint32_t albo = C::A_MN ? 4096u : 16u, blbo = C::B_MN ? 4096u : 16u;
             const uint32_t asbo = C::A_MN ? 512u : 1024u, bsbo = C::B_MN ? 512u : 1024u;
@@ -346,23 +354,29 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                     tc_fence_after();
                     const uint32_t d = tmem + (uint32_t)(buf * BN);
                     const uint64_t so = (uint64_t)(s * C::STAGE_BYTES) >> 4;
+                    const bool last = (in_chunk + 1 == CHK || it == nkb - 1);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int g = 0; g < C::BK / 8; ++g) {
-                        const uint64_t adH = adH0 + so + g * A_G, bdH = bdH0 + so + g * B_G;
-                        const uint32_t acc0 = (in_chunk > 0 || g > 0) ? 1u : 0u;
-                        if (PLANES == 2) {
-                            mma_tf32_ss(d, adH + A_LO, bdH, IDESC, acc0);
-                            mma_tf32_ss(d, adH, bdH + B_LO, IDESC, 1u);
-                            mma_tf32_ss(d, adH, bdH, IDESC, 1u);
-                        } else {
-                            mma_tf32_ss(d, adH, bdH, IDESC, acc0);
+                        for (int g = 0; g < C::BK / 8; ++g) {
+                            const uint64_t adH = adH0 + so + g * A_G, bdH = bdH0 + so + g * B_G;
+                            const uint32_t acc0 = (in_chunk > 0 || g > 0) ? 1u : 0u;
+                            if (PLANES == 2) {
+                                mma_tf32_ss(d, adH + A_LO, bdH, IDESC, acc0);
+                                mma_tf32_ss(d, adH, bdH + B_LO, IDESC, 1u);
+                                mma_tf32_ss(d, adH, bdH, IDESC, 1u);
+                            } else {
+                                mma_tf32_ss(d, adH, bdH, IDESC, acc0);
+                            }
                         }
+                        mma_commit(&aux->empty[s]);
+                        if (last) mma_commit(&aux->tfull[buf]);
                     }
-                    mma_commit(&aux->empty[s]);
-                    if (++in_chunk == CHK || it == nkb - 1) {
-                        mma_commit(&aux->tfull[buf]);
+                    __syncwarp();
+                    if (last) {
                         ++c;
                         in_chunk = 0;
+                    } else {
+                        ++in_chunk;
                     }
                     if (++s == C::STAGES) {
                         s = 0;
