@@ -1,5 +1,6 @@
 // conv_tma.cu — host side of the TMA variant: eligibility, tensor-map encoding, launch.
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 
@@ -11,6 +12,16 @@
 namespace smconv {
 
 namespace {
+
+// Tuning knobs (read once; for experiments only): SMCONV_TMA_G (32|128 images per A box),
+// SMCONV_TMA_L2PROMO (0..3 = NONE/64B/128B/256B), SMCONV_TMA_CHUNK (promotion interval, k-blocks).
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+const int g_knob_G = env_int("SMCONV_TMA_G", 0);
+const int g_knob_promo = env_int("SMCONV_TMA_L2PROMO", 3);
+const int g_knob_chunk = env_int("SMCONV_TMA_CHUNK", 8);
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::atomic<int> g_encode_state{0};
@@ -44,7 +55,7 @@ bool encode(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, co
     }
     for (int i = 0; i < rank - 1; ++i) gs[i] = strides_bytes[i];
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), gd, gs, bd, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, (CUtensorMapL2promotion)g_knob_promo,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -104,7 +115,8 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
     tp.work = grid.x * grid.y * grid.z;
     grid = dim3(tp.work < 148 ? tp.work : 148, 1, 1);
     tp.G = (g.N % 128 == 0) ? 128 : 32;
-    tp.chunk_kb = 8;
+    if (g_knob_G == 32) tp.G = 32;
+    tp.chunk_kb = g_knob_chunk > 0 ? g_knob_chunk : 8;
     if (planes == 2 && BN > 128) {
         snprintf(err, errlen, "tma plan: BN %d > 128 in 3xTF32", BN);
         return CONV_EUNSUPPORTED;

@@ -57,7 +57,7 @@ struct TmaCfg {
     static constexpr int BM = 128, BK = 32;
     static constexpr int NEPI = 8;  // epilogue warps 0-7
     static constexpr int TMA_W = 8, MMA_W = 9, CONV_W0 = 10;
-    static constexpr int NCONV = PLANES == 2 ? 4 : 0;
+    static constexpr int NCONV = PLANES == 2 ? 8 : 0;  // converters: 8 warps keep up with N=64 MMAs
     static constexpr int NTHREADS = (10 + NCONV) * 32;
     static constexpr int A_BYTES = BM * BK * 4;
     static constexpr int B_BYTES = BN * BK * 4;
@@ -145,7 +145,9 @@ struct TileInfo {
         if (!DWK) {
             const int Mrows = OP == OP_DX ? p.phase_IHp[phase] * p.phase_IWp[phase] * p.N : p.M;
             ngrp = 128 / tp.G;
-            for (int g = 0; g < ngrp; ++g) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {  // static indexing keeps grp[] in registers
+                if (g >= ngrp) break;
                 const int m = m0 + g * tp.G;
                 grp[g] = make_int4(-(1 << 20), -(1 << 20), 0, 0);
                 if (m < Mrows) {
@@ -184,8 +186,9 @@ struct TileInfo {
         const int srcH = OP == OP_FWD ? p.IH : p.OH;
         const int srcW = OP == OP_FWD ? p.IW : p.OW;
         bool any = false;
-        for (int g = 0; g < ngrp; ++g)
-            any |= grp[g].w && (unsigned)(grp[g].x + dh) < (unsigned)srcH && (unsigned)(grp[g].y + dw) < (unsigned)srcW;
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+            if (g < ngrp) any |= grp[g].w && (unsigned)(grp[g].x + dh) < (unsigned)srcH && (unsigned)(grp[g].y + dw) < (unsigned)srcW;
         if (any && t) *t = make_int4(dh, dw, fh * p.FW + fw, 0);
         return any;
     }
@@ -255,8 +258,9 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                         const uint32_t sB = sA + PLANES * C::A_BYTES;
                         if (elect_one()) {
                             mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + C::B_BYTES);
-                            for (int g = 0; g < ti.ngrp; ++g)
-                                tma_load_4d(sA + g * tp.G * 128, &tp.mapA, &aux->full[s], cb * 32,
+#pragma unroll
+                            for (int g = 0; g < 4; ++g)
+                                if (g < ti.ngrp) tma_load_4d(sA + g * tp.G * 128, &tp.mapA, &aux->full[s], cb * 32,
                                             ti.grp[g].y + tap.y, ti.grp[g].x + tap.x, ti.grp[g].z);
                             if (OP == OP_FWD) tma_load_3d(sB, &tp.mapB, &aux->full[s], cb * 32, tap.z, n0);
                             else tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, cb * 32, n0 / 32, tap.z);
@@ -389,7 +393,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
     } else if (warp >= C::CONV_W0) {
         // ======================= 3xTF32 split converters: lo = a - trunc_tf32(a)
         const int ct = tid - C::CONV_W0 * 32;
-        constexpr int NCT = C::NCONV * 32;
+        constexpr int NCT = C::NCONV > 0 ? C::NCONV * 32 : 32;  // (dead code when PLANES == 1)
         uint32_t q = 0;
         for (int w = blockIdx.x; w < tp.work; w += gridDim.x) {
             TileInfo<OP> ti;
@@ -404,26 +408,25 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                 float4* aL = reinterpret_cast<float4*>(st + C::A_BYTES);
                 const float4* bH = reinterpret_cast<const float4*>(st + PLANES * C::A_BYTES);
                 float4* bL = reinterpret_cast<float4*>(st + PLANES * C::A_BYTES + C::B_BYTES);
-#pragma unroll 4
-                for (int i = ct; i < C::A_BYTES / 16; i += NCT) {
-                    const float4 v = aH[i];
+                constexpr int NA = C::A_BYTES / 16 / NCT, NB = C::B_BYTES / 16 / NCT;
+                static_assert(NA * NCT * 16 == C::A_BYTES && NB * NCT * 16 == C::B_BYTES, "converter split");
+                float4 va[NA], vb[NB];  // all loads first (ILP), then split + store
+#pragma unroll
+                for (int i = 0; i < NA; ++i) va[i] = aH[ct + i * NCT];
+#pragma unroll
+                for (int i = 0; i < NB; ++i) vb[i] = bH[ct + i * NCT];
+                auto lo4 = [](float4 v) {
                     float4 o;
                     o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
                     o.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
                     o.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
                     o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-                    aL[i] = o;
-                }
-#pragma unroll 4
-                for (int i = ct; i < C::B_BYTES / 16; i += NCT) {
-                    const float4 v = bH[i];
-                    float4 o;
-                    o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-                    o.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-                    o.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-                    o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-                    bL[i] = o;
-                }
+                    return o;
+                };
+#pragma unroll
+                for (int i = 0; i < NA; ++i) aL[ct + i * NCT] = lo4(va[i]);
+#pragma unroll
+                for (int i = 0; i < NB; ++i) bL[ct + i * NCT] = lo4(vb[i]);
                 fence_proxy_async_smem();
                 mbar_arrive(&aux->conv[s]);
             }
