@@ -1,0 +1,111 @@
+// conv_strip.cu — host side of the STRIP variant (conv_strip.cuh): eligibility, maps, launch.
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include <cudaTypedefs.h>
+
+#include "../../include/smconv.h"
+#include "conv_strip.cuh"
+
+namespace smconv {
+
+bool tma_encode_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                    const uint32_t* box, CUtensorMapSwizzle sw);  // conv_tma.cu
+
+namespace {
+
+const int g_knob_chunk_s = getenv("SMCONV_TMA_CHUNK") ? atoi(getenv("SMCONV_TMA_CHUNK")) : 8;
+
+template <int OP, int BN, int PLANES, int R>
+int launch_t(const StripParams& sp, const GenParams& g, cudaStream_t st, char* err, size_t errlen) {
+    using C = StripCfg<OP, BN, PLANES, R>;
+    static std::atomic<unsigned long long> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_done.load() & bit)) {
+        if (cudaFuncSetAttribute(conv_strip_kernel<OP, BN, PLANES, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::SMEM_BYTES) != cudaSuccess) {
+            snprintf(err, errlen, "cudaFuncSetAttribute(strip smem=%d): %s", C::SMEM_BYTES,
+                     cudaGetErrorString(cudaGetLastError()));
+            return CONV_ECUDA;
+        }
+        attr_done.fetch_or(bit);
+    }
+    const int grid = sp.work < 148 ? sp.work : 148;
+    conv_strip_kernel<OP, BN, PLANES, R><<<grid, C::NTHREADS, C::SMEM_BYTES, st>>>(sp, g);
+    return CONV_OK;
+}
+
+template <int OP>
+int launch_op(int BN, int planes, const StripParams& sp, const GenParams& g, cudaStream_t st, char* err, size_t n) {
+    if (planes == 2) {
+        if (BN == 32) return launch_t<OP, 32, 2, 1>(sp, g, st, err, n);
+        return launch_t<OP, 64, 2, 1>(sp, g, st, err, n);
+    }
+    if (BN == 32) return launch_t<OP, 32, 1, 4>(sp, g, st, err, n);
+    if (BN == 64) return launch_t<OP, 64, 1, 2>(sp, g, st, err, n);
+    return launch_t<OP, 128, 1, 1>(sp, g, st, err, n);
+}
+
+}  // namespace
+
+int strip_R(int BN, int planes) {
+    if (planes == 2) return 1;
+    return BN == 32 ? 4 : BN == 64 ? 2 : 1;
+}
+
+bool strip_supported(int op, int N, int IC, int OC, int FW, int sh, int sw, int OWo, int BN, int planes) {
+    if (op != CONV_OP_FWD && op != CONV_OP_BWD_DATA) return false;
+    if (sh != 1 || sw != 1 || FW != kStripFW) return false;
+    if (N % 32 || IC % 32 || OC % 32) return false;
+    if (OWo < 4) return false;
+    if (planes == 2) return BN <= 64;
+    return BN <= 128;
+}
+
+int strip_launch(int op, int BN, int planes, const GenParams& g, cudaStream_t st, char* err, size_t errlen) {
+    StripParams sp;
+    memset(&sp, 0, sizeof sp);
+    const int R = strip_R(BN, planes);
+    const bool fwd = op == CONV_OP_FWD;
+    const uint64_t N = g.N, T = (uint64_t)g.FH * g.FW;
+    const uint64_t C = fwd ? g.IC : g.OC;                 // channels of the activation operand
+    const uint64_t H = fwd ? g.IH : g.OH, W = fwd ? g.IW : g.OW;
+    sp.CB = (int)(C / 32);
+    sp.NG = g.N / 32;
+    sp.OHo = fwd ? g.OH : g.IH;
+    sp.OWo = fwd ? g.OW : g.IW;
+    sp.SH = (int)H;
+    sp.SW = (int)W;
+    sp.strips = (sp.OWo + 4 * R - 1) / (4 * R);
+    sp.n_tiles = (g.Ngemm + BN - 1) / BN;
+    sp.work = sp.NG * sp.OHo * sp.strips * sp.n_tiles;
+    sp.chunk_kb = g_knob_chunk_s > 0 ? g_knob_chunk_s : 8;
+    sp.row_off = fwd ? -g.ph : g.ph;
+    sp.col_off = fwd ? -g.pw : g.pw - (kStripFW - 1);
+    const uint32_t slabs = 4 * R + kStripFW - 1;
+    // A: activations viewed (32 ch, N, W, H, C/32) -> smem [slab][32 images][32 ch]
+    uint64_t da[5] = {32, N, W, H, C / 32}, sa[4] = {H * W * C * 4, C * 4, W * C * 4, 128};
+    uint32_t ba[5] = {32, 32, slabs, 1, 1};
+    bool ok = tma_encode_f32(&sp.mapA, g.A, 5, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (fwd) {
+        uint64_t db[3] = {(uint64_t)g.IC, (uint64_t)g.OC, T}, sb[2] = {T * g.IC * 4, (uint64_t)g.IC * 4};
+        uint32_t bb[3] = {32, (uint32_t)BN, (uint32_t)kStripFW};
+        ok &= tma_encode_f32(&sp.mapB, g.B, 3, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else {
+        uint64_t db[4] = {32, (uint64_t)g.OC, (uint64_t)g.IC / 32, T}, sb[3] = {T * g.IC * 4, 128, (uint64_t)g.IC * 4};
+        uint32_t bb[4] = {32, 32, (uint32_t)(BN / 32), (uint32_t)kStripFW};
+        ok &= tma_encode_f32(&sp.mapB, g.B, 4, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    }
+    if (!ok) {
+        snprintf(err, errlen, "strip: cuTensorMapEncodeTiled failed (op %d)", op);
+        return CONV_ECUDA;
+    }
+    return fwd ? launch_op<OP_FWD>(BN, planes, sp, g, st, err, errlen)
+               : launch_op<OP_DX>(BN, planes, sp, g, st, err, errlen);
+}
+
+}  // namespace smconv

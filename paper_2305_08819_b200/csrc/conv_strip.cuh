@@ -1,0 +1,367 @@
+// conv_strip.cuh — STRIP variant: stride-1 fwd / dX (3-wide filters) with input-slab reuse
+// across the filter columns; the fast path for the 64/128-channel 32x32 and 16x16 layers.
+//
+// With a 128 x BN output tile of the plain implicit GEMM, every A (activation) byte brought in by
+// TMA feeds only BN output channels, and for BN = 64 (ResNet l1 / VGG conv2: 64 channels) the
+// kernel is bound by TMA traffic, not by the tensor core.  Here a tile is a strip of 4R output
+// positions of one output row x 32 images x BN channels.  Per (filter row fh, 32-channel block)
+// one TMA box brings the (4R + FW - 1) input "slabs" [32 images x 32 channels] of the source row
+// into shared memory, contiguously; the 128-row A operand of accumulator j and filter column fw
+// is then the 4-slab window starting at slab 4j + fw (fwd) / 4j + FW-1-fw (dX) -- a plain
+// descriptor offset, no copy.  Each slab is loaded once and used FW times (3x fewer A bytes),
+// and one stage feeds R * FW * 4 MMAs (6-12x fewer TMA instructions per MMA).
+//
+// Row of an accumulator: position p = row / 32 of its 4-group, image = row % 32, so epilogue
+// warp quadrant q handles position 4j + q.  Zero padding / ragged strips = TMA OOB zero fill.
+// Roles, 3xTF32 handling and TMEM double buffering are those of conv_tma.cuh.
+#pragma once
+#include "conv_tma.cuh"
+
+namespace smconv {
+
+constexpr int kStripFW = 3;
+
+struct __align__(64) StripParams {
+    CUtensorMap mapA;  // activations viewed (32 ch, N, W, H, C/32)
+    CUtensorMap mapB;  // fwd: W viewed (IC, OC, T); dX: W viewed (32 ic, OC, IC/32, T)
+    int CB;            // 32-channel blocks of the reduction (fwd: IC/32, dX: OC/32)
+    int NG;            // 32-image groups
+    int OHo, OWo;      // output extent (fwd: OH x OW, dX: IH x IW)
+    int SH, SW;        // source extent (fwd: IH x IW, dX: OH x OW)
+    int strips;        // strips per output row
+    int n_tiles, work, chunk_kb;
+    int row_off;       // source row = out row + row_off + (fwd: fh | dX: -fh)   (fwd: -ph, dX: +ph)
+    int col_off;       // first slab column = strip origin + col_off (fwd: -pw, dX: pw - (FW-1))
+};
+
+template <int OP, int BN, int PLANES, int R>
+struct StripCfg {
+    static constexpr int FW = kStripFW;
+    static constexpr int SLABS = 4 * R + FW - 1;
+    static constexpr int A_BYTES = SLABS * 4096;
+    static constexpr int B_BYTES = FW * BN * 128;
+    static constexpr int STAGE_BYTES = PLANES * (A_BYTES + B_BYTES);
+    static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
+    static constexpr int NEPI = 8, TMA_W = 8, MMA_W = 9, CONV_W0 = 10;
+    static constexpr int NCONV = PLANES == 2 ? 8 : 0;
+    static constexpr int NTHREADS = (10 + NCONV) * 32;
+    static constexpr bool B_MN = (OP == OP_DX);
+    static constexpr int ACC_COLS = 2 * R * BN;
+    static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128 : ACC_COLS <= 256 ? 256 : 512;
+    static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 1024;
+    static_assert(STAGES >= 2, "strip stage does not fit");
+    static_assert(ACC_COLS <= 512, "TMEM");
+    static_assert(PLANES == 1 || R * BN <= 128, "3xTF32 promotion keeps R*BN/2 fp32 per epilogue thread");
+};
+
+struct StripTile {
+    int g, orow, s, nt;
+    SMCONV_DEV void init(const StripParams& sp, int w) {
+        nt = w % sp.n_tiles;
+        int r = w / sp.n_tiles;
+        s = r % sp.strips;
+        r /= sp.strips;
+        orow = r % sp.OHo;
+        g = r / sp.OHo;
+    }
+};
+
+template <int OP>
+SMCONV_DEV int strip_src_row(const StripParams& sp, int orow, int fh) {
+    return OP == OP_FWD ? orow + sp.row_off + fh : orow + sp.row_off - fh;
+}
+
+// number of filter rows whose source row is inside the map (others are all-zero stages: skipped)
+template <int OP>
+SMCONV_DEV int strip_rows(const StripParams& sp, const GenParams& p, int orow) {
+    int n = 0;
+    for (int fh = 0; fh < p.FH; ++fh) n += (unsigned)strip_src_row<OP>(sp, orow, fh) < (unsigned)sp.SH;
+    return n;
+}
+
+template <int OP, int BN, int PLANES, int R>
+__global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
+    conv_strip_kernel(const __grid_constant__ StripParams sp, const __grid_constant__ GenParams p) {
+    using C = StripCfg<OP, BN, PLANES, R>;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    const uint32_t tiles_addr = (raw_addr + 1023u) & ~1023u;
+    uint8_t* tiles_ptr = smem_raw + (tiles_addr - raw_addr);
+    TmaAux* aux = reinterpret_cast<TmaAux*>(tiles_ptr + C::STAGES * C::STAGE_BYTES);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int CHK = PLANES == 2 ? sp.chunk_kb : (1 << 30);
+
+    if (tid == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&aux->full[s], 1);
+            mbar_init(&aux->conv[s], C::NCONV * 32);
+            mbar_init(&aux->empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&aux->tfull[b], 1);
+            mbar_init(&aux->tempty[b], C::NEPI * 32);
+        }
+        fence_mbar_init();
+    }
+    if (warp == C::TMA_W && lane == 0) {
+        prefetch_tmap(&sp.mapA);
+        prefetch_tmap(&sp.mapB);
+    }
+    if (warp == C::MMA_W) tmem_alloc(&aux->tmem_base, C::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = aux->tmem_base;
+
+    if (warp == C::TMA_W) {
+        // ======================= TMA producer: 2 boxes per stage (slab row, FW filter taps)
+        int s = 0;
+        uint32_t r = 0;
+        for (int w = blockIdx.x; w < sp.work; w += gridDim.x) {
+            StripTile t;
+            t.init(sp, w);
+            const int col0 = t.s * 4 * R + sp.col_off;
+            for (int fh = 0; fh < p.FH; ++fh) {
+                const int srow = strip_src_row<OP>(sp, t.orow, fh);
+                if ((unsigned)srow >= (unsigned)sp.SH) continue;
+                for (int cb = 0; cb < sp.CB; ++cb) {
+                    if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
+                    const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
+                    const uint32_t sB = sA + PLANES * C::A_BYTES;
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + C::B_BYTES);
+                        tma_load_5d(sA, &sp.mapA, &aux->full[s], 0, t.g * 32, col0, srow, cb);
+                        if (OP == OP_FWD) tma_load_3d(sB, &sp.mapB, &aux->full[s], cb * 32, t.nt * BN, fh * C::FW);
+                        else tma_load_4d(sB, &sp.mapB, &aux->full[s], 0, cb * 32, t.nt * BN / 32, fh * C::FW);
+                    }
+                    __syncwarp();
+                    if (++s == C::STAGES) {
+                        s = 0;
+                        ++r;
+                    }
+                }
+            }
+        }
+    } else if (warp == C::MMA_W) {
+        // ======================= MMA issuer: R accumulators x FW taps x 4 k-steps per stage
+        constexpr uint32_t IDESC = idesc_tf32(128, BN, false, C::B_MN);
+        const uint64_t adH0 = make_sdesc(tiles_addr, 16u, 1024u, kLayoutSW128);
+        const uint64_t bdH0 = make_sdesc(tiles_addr + PLANES * C::A_BYTES, C::B_MN ? 4096u : 16u,
+                                         C::B_MN ? 512u : 1024u, C::B_MN ? kLayoutSW128Base32 : kLayoutSW128);
+        constexpr uint64_t A_LO = C::A_BYTES >> 4, B_LO = C::B_BYTES >> 4;
+        constexpr uint64_t B_G = C::B_MN ? 64 : 2, B_TAP = (BN * 128) >> 4;
+        int s = 0, in_chunk = 0;
+        uint32_t r = 0, c = 0;
+        for (int w = blockIdx.x; w < sp.work; w += gridDim.x) {
+            StripTile t;
+            t.init(sp, w);
+            const int nkb = strip_rows<OP>(sp, p, t.orow) * sp.CB;
+            for (int it = 0; it < nkb; ++it) {
+                const int buf = c & 1;
+                if (in_chunk == 0 && c >= 2) {
+                    mbar_wait(&aux->tempty[buf], ((c >> 1) - 1) & 1);
+                    tc_fence_after();
+                }
+                mbar_wait(PLANES == 2 ? &aux->conv[s] : &aux->full[s], r & 1);
+                tc_fence_after();
+                const uint64_t so = (uint64_t)(s * C::STAGE_BYTES) >> 4;
+                const bool last = (in_chunk + 1 == CHK || it == nkb - 1);
+                if (elect_one()) {
+#pragma unroll
+                    for (int j = 0; j < R; ++j) {
+                        const uint32_t d = tmem + (uint32_t)((buf * R + j) * BN);
+#pragma unroll
+                        for (int fw = 0; fw < C::FW; ++fw) {
+                            const int woff = OP == OP_FWD ? fw : C::FW - 1 - fw;
+                            const uint64_t a0 = adH0 + so + (uint64_t)((4 * j + woff) * 4096 >> 4);
+                            const uint64_t b0 = bdH0 + so + fw * B_TAP;
+#pragma unroll
+                            for (int g = 0; g < 4; ++g) {
+                                const uint64_t adH = a0 + g * 2, bdH = b0 + g * B_G;
+                                const uint32_t acc0 = (in_chunk > 0 || fw > 0 || g > 0) ? 1u : 0u;
+                                if (PLANES == 2) {
+                                    mma_tf32_ss(d, adH + A_LO, bdH, IDESC, acc0);
+                                    mma_tf32_ss(d, adH, bdH + B_LO, IDESC, 1u);
+                                    mma_tf32_ss(d, adH, bdH, IDESC, 1u);
+                                } else {
+                                    mma_tf32_ss(d, adH, bdH, IDESC, acc0);
+                                }
+                            }
+                        }
+                    }
+                    mma_commit(&aux->empty[s]);
+                    if (last) mma_commit(&aux->tfull[buf]);
+                }
+                __syncwarp();
+                if (last) {
+                    ++c;
+                    in_chunk = 0;
+                } else {
+                    ++in_chunk;
+                }
+                if (++s == C::STAGES) {
+                    s = 0;
+                    ++r;
+                }
+            }
+        }
+    } else if (warp >= C::CONV_W0) {
+        // ======================= 3xTF32 split converters (elementwise over the stage)
+        const int ct = tid - C::CONV_W0 * 32;
+        constexpr int NCT = C::NCONV > 0 ? C::NCONV * 32 : 32;
+        int s = 0;
+        uint32_t r = 0;
+        for (int w = blockIdx.x; w < sp.work; w += gridDim.x) {
+            StripTile t;
+            t.init(sp, w);
+            const int nkb = strip_rows<OP>(sp, p, t.orow) * sp.CB;
+            for (int it = 0; it < nkb; ++it) {
+                mbar_wait(&aux->full[s], r & 1);
+                uint8_t* st = tiles_ptr + s * C::STAGE_BYTES;
+                auto lo4 = [](float4 v) {
+                    float4 o;
+                    o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                    o.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                    o.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                    o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                    return o;
+                };
+                {
+                    const float4* aH = reinterpret_cast<const float4*>(st);
+                    float4* aL = reinterpret_cast<float4*>(st + C::A_BYTES);
+                    constexpr int NA = (C::A_BYTES / 16 + NCT - 1) / NCT;
+                    float4 v[NA];
+#pragma unroll
+                    for (int i = 0; i < NA; ++i)
+                        if (ct + i * NCT < C::A_BYTES / 16) v[i] = aH[ct + i * NCT];
+#pragma unroll
+                    for (int i = 0; i < NA; ++i)
+                        if (ct + i * NCT < C::A_BYTES / 16) aL[ct + i * NCT] = lo4(v[i]);
+                }
+                {
+                    const float4* bH = reinterpret_cast<const float4*>(st + PLANES * C::A_BYTES);
+                    float4* bL = reinterpret_cast<float4*>(st + PLANES * C::A_BYTES + C::B_BYTES);
+                    constexpr int NB = (C::B_BYTES / 16 + NCT - 1) / NCT;
+                    float4 v[NB];
+#pragma unroll
+                    for (int i = 0; i < NB; ++i)
+                        if (ct + i * NCT < C::B_BYTES / 16) v[i] = bH[ct + i * NCT];
+#pragma unroll
+                    for (int i = 0; i < NB; ++i)
+                        if (ct + i * NCT < C::B_BYTES / 16) bL[ct + i * NCT] = lo4(v[i]);
+                }
+                fence_proxy_async_smem();
+                mbar_arrive(&aux->conv[s]);
+                if (++s == C::STAGES) {
+                    s = 0;
+                    ++r;
+                }
+            }
+        }
+    } else {
+        // ======================= epilogue warps 0-7: quadrant q = position 4j+q, lane = image
+        const int qd = warp & 3, half = warp >> 2;
+        constexpr int HALF = BN / 2;
+        const uint32_t lane_addr = (uint32_t)(qd * 32) << 16;
+        uint32_t c = 0;
+        for (int w = blockIdx.x; w < sp.work; w += gridDim.x) {
+            StripTile t;
+            t.init(sp, w);
+            const int nkb = strip_rows<OP>(sp, p, t.orow) * sp.CB;
+            const int nch = nkb > 0 ? (nkb + CHK - 1) / CHK : 0;
+            const int n0 = t.nt * BN;
+            const int img = t.g * 32 + lane;
+            long long obase[R];
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                const int ocol = t.s * 4 * R + 4 * j + qd;
+                obase[j] = (ocol < sp.OWo && img < p.N)
+                               ? ((long long)(img * sp.OHo + t.orow) * sp.OWo + ocol) * p.Ngemm
+                               : -1;
+            }
+            float* outp = p.out;
+            if (PLANES == 2) {
+                float acc[R][HALF];
+#pragma unroll
+                for (int j = 0; j < R; ++j)
+#pragma unroll
+                    for (int e = 0; e < HALF; ++e) acc[j][e] = 0.f;
+                for (int k = 0; k < nch; ++k, ++c) {
+                    const int buf = c & 1;
+                    mbar_wait(&aux->tfull[buf], (c >> 1) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int j = 0; j < R; ++j)
+#pragma unroll
+                        for (int c0 = 0; c0 < HALF; c0 += 16) {
+                            uint32_t v[16];
+                            tmem_ld_32x32b_x16(tmem + lane_addr + (uint32_t)((buf * R + j) * BN + half * HALF + c0), v);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) acc[j][c0 + e] += __uint_as_float(v[e]);
+                        }
+                    tc_fence_before();
+                    mbar_arrive(&aux->tempty[buf]);
+                }
+#pragma unroll
+                for (int j = 0; j < R; ++j)
+                    if (obase[j] >= 0)
+#pragma unroll
+                        for (int e = 0; e < HALF; e += 4) {
+                            const int col = n0 + half * HALF + e;
+                            if (col < p.Ngemm)
+                                *reinterpret_cast<float4*>(outp + obase[j] + col) =
+                                    make_float4(acc[j][e], acc[j][e + 1], acc[j][e + 2], acc[j][e + 3]);
+                        }
+            } else {
+                const int buf = c & 1;
+                if (nch > 0) {
+                    mbar_wait(&aux->tfull[buf], (c >> 1) & 1);
+                    tc_fence_after();
+                }
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+#pragma unroll 1
+                    for (int c0 = 0; c0 < HALF; c0 += 16) {
+                        uint32_t v[16];
+                        if (nch > 0) {
+                            tmem_ld_32x32b_x16(tmem + lane_addr + (uint32_t)((buf * R + j) * BN + half * HALF + c0), v);
+                            tmem_ld_wait();
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) v[e] = 0u;
+                        }
+                        if (obase[j] >= 0)
+#pragma unroll
+                            for (int e = 0; e < 16; e += 4) {
+                                const int col = n0 + half * HALF + c0 + e;
+                                if (col < p.Ngemm)
+                                    *reinterpret_cast<float4*>(outp + obase[j] + col) =
+                                        make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
+                                                    __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+                            }
+                    }
+                }
+                if (nch > 0) {
+                    tc_fence_before();
+                    mbar_arrive(&aux->tempty[buf]);
+                    ++c;
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == C::MMA_W) {
+        tc_fence_after();
+        tmem_dealloc(tmem, C::TMEM_COLS);
+    }
+}
+
+bool strip_supported(int op, int N, int IC, int OC, int FW, int sh, int sw, int OWo, int BN, int planes);
+int strip_launch(int op, int BN, int planes, const GenParams& g, cudaStream_t st, char* err, size_t errlen);
+int strip_R(int BN, int planes);
+
+}  // namespace smconv

@@ -100,6 +100,11 @@ int launch_op(int BN, int planes, const TmaParams& tp, const GenParams& g, dim3 
 
 }  // namespace
 
+bool tma_encode_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                    const uint32_t* box, CUtensorMapSwizzle sw) {
+    return encode(m, base, rank, dims, strides, box, sw);
+}
+
 bool tma_supported(int op, int N, int IC, int OC, int FH, int FW, int sh, int sw) {
     (void)FH; (void)FW; (void)sh; (void)sw;
     if (N % 32) return false;

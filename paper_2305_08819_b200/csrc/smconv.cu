@@ -15,7 +15,7 @@
 #include "../../include/smconv.h"
 #include "../../include/smconv_ext.h"
 #include "conv_gen.cuh"
-#include "conv_tma.cuh"
+#include "conv_strip.cuh"
 
 using namespace smconv;
 
@@ -45,7 +45,7 @@ void read_env_once() {
             if (j == std::string::npos) j = s.size();
             std::string item = s.substr(i, j - i);
             int op = -1, var = -1;
-            if (sscanf(item.c_str(), "%d:%d", &op, &var) == 2 && op >= 0 && op < 3 && var >= 0 && var <= 2)
+            if (sscanf(item.c_str(), "%d:%d", &op, &var) == 2 && op >= 0 && op < 3 && var >= 0 && var <= 3)
                 g_force[op].store(var);
             i = j + 1;
         }
@@ -153,6 +153,14 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
     pl.variant = forced == CONV_VARIANT_AUTO ? (tma_ok ? CONV_VARIANT_TMA : CONV_VARIANT_GENERIC) : forced;
     if (pl.variant == CONV_VARIANT_TMA && !tma_ok)
         return fail(CONV_EUNSUPPORTED, "%s: TMA variant forced but unsupported for this shape", op_name(op));
+    if (op != CONV_OP_BWD_FILTER && (forced == CONV_VARIANT_AUTO || forced == CONV_VARIANT_STRIP)) {
+        const int bns = pick_bn(op == CONV_OP_FWD ? d.OC : d.IC);
+        const bool strip_ok = strip_supported(op, d.N, d.IC, d.OC, d.FW, d.sh, d.sw, op == CONV_OP_FWD ? d.OW : d.IW,
+                                              bns, pl.planes);
+        if (strip_ok) pl.variant = CONV_VARIANT_STRIP;
+        else if (forced == CONV_VARIANT_STRIP)
+            return fail(CONV_EUNSUPPORTED, "%s: STRIP variant forced but unsupported for this shape", op_name(op));
+    }
 
     // 3xTF32 on the TMA variant promotes chunks into BN/2 fp32 registers per epilogue thread: BN <= 128
     auto bn_for = [&](int n) {
@@ -218,7 +226,9 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
     }
     const int tiles = m_tiles * n_tiles;
     int splits = 1;
-    if (op == CONV_OP_BWD_FILTER) {
+    if (pl.variant == CONV_VARIANT_STRIP) {
+        // strip tiles (32 images x 4R positions) are plentiful: no split-K
+    } else if (op == CONV_OP_BWD_FILTER) {
         const int need_prec = (nkb_est + kMaxKbPerChain - 1) / kMaxKbPerChain;
         int fill = kSMs / tiles;
         if (fill < 1) fill = 1;
@@ -295,7 +305,9 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
     g.B = B;
     g.out = pl.splits > 1 ? (float*)ws : out;
     cudaGetLastError();  // clear sticky-free earlier errors of the caller
-    if (pl.variant == CONV_VARIANT_TMA) {
+    if (pl.variant == CONV_VARIANT_STRIP) {
+        rc = strip_launch(op, pl.BN, pl.planes, g, st, g_detail, sizeof g_detail);
+    } else if (pl.variant == CONV_VARIANT_TMA) {
         TmaParams tp = pl.tp;
         rc = tma_launch(op, pl.BN, pl.planes, g, tp, pl.grid, st, g_detail, sizeof g_detail);
     } else if (op == CONV_OP_FWD) {
@@ -405,7 +417,7 @@ const char* conv2d_strerror(int code) {
 const char* conv2d_last_error_detail(void) { return g_detail; }
 
 int conv2d_force_variant(int op, int variant) {
-    if (op < 0 || op > 2 || variant < 0 || variant > 2) return fail(CONV_EARG, "conv2d_force_variant: bad op/variant");
+    if (op < 0 || op > 2 || variant < 0 || variant > 3) return fail(CONV_EARG, "conv2d_force_variant: bad op/variant");
     read_env_once();
     g_force[op].store(variant);
     return CONV_OK;
@@ -421,7 +433,7 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
     if (rc) return rc;
     if (buf && len)
         snprintf(buf, len, "variant=%s BN=%d planes=%d splits=%d grid=%ux%ux%u ws=%zu kernels=%d",
-                 pl.variant == CONV_VARIANT_TMA ? "tma" : "generic", pl.BN, pl.planes, pl.splits, pl.grid.x,
+                 pl.variant == CONV_VARIANT_STRIP ? "strip" : pl.variant == CONV_VARIANT_TMA ? "tma" : "generic", pl.BN, pl.planes, pl.splits, pl.grid.x,
                  pl.grid.y, pl.grid.z, pl.ws_bytes, pl.splits > 1 ? 2 : 1);
     return CONV_OK;
 }

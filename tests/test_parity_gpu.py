@@ -282,3 +282,62 @@ def test_tma_random_within_tolerance(env, force_tma, s, math):
         e = normwise(g, r)
         print("tma %s %s %s err %.3e" % (_id(s), math, name, e))
         assert e <= TOL[math], (name, e)
+
+
+# ---------------------------------------------------------------- STRIP variant (stride 1, 3-wide filters)
+SWEEP_STRIP = [
+    (32, 32, 32, 64, 64, 3, 3, 1, 1, 1, 1),     # ResNet l1 / VGG conv2 class (BN 64)
+    (64, 16, 16, 128, 128, 3, 3, 1, 1, 1, 1),   # l2 class (BN 128, TF32 only; 3xTF32 falls back)
+    (32, 8, 8, 64, 32, 3, 3, 1, 1, 1, 1),       # BN 32
+    (32, 7, 10, 32, 64, 3, 3, 1, 1, 1, 1),      # ragged strip (OW 10 not a multiple of 4R)
+    (32, 6, 6, 64, 64, 3, 3, 1, 1, 0, 0),       # no padding
+    (32, 5, 9, 32, 64, 5, 3, 1, 1, 2, 1),       # FH 5 rows, pad 2 / 1
+    (96, 4, 4, 64, 64, 3, 3, 1, 1, 1, 1),       # 3 image groups, 4x4 map
+]
+
+
+@pytest.fixture
+def force_strip(env):
+    _, _, sm = env
+    for op in (0, 1):
+        sm.force_variant(op, sm.CONV_VARIANT_STRIP)
+    yield
+    for op in (0, 1):
+        sm.force_variant(op, sm.CONV_VARIANT_AUTO)
+
+
+def _strip_ok(sm, s, math, op):
+    try:
+        return "strip" in sm.plan_describe(op, s, sm.MATH[math])
+    except sm.ConvError as e:
+        assert e.code == sm.CONV_EUNSUPPORTED
+        return False
+
+
+@pytest.mark.parametrize("s", SWEEP_STRIP, ids=_id)
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+def test_strip_parity(env, force_strip, s, math):
+    torch, oracle, sm = env
+    N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw = s
+    for integer in (1, 0):
+        X, W, dY = gen(s, 20 + integer, integer=integer)
+        x, w, dy = (torch.from_numpy(a).cuda() for a in (X, W, dY))
+        ran = 0
+        if _strip_ok(sm, s, math, 0):
+            y = sm.conv2d_fwd(x, w, (sh, sw), (ph, pw), math=math).cpu().numpy()
+            ref = oracle.conv2d_fwd(X, W, (sh, sw), (ph, pw))
+            ran += 1
+            if integer:
+                assert np.array_equal(y.astype(np.float64), ref)
+            else:
+                assert normwise(y, ref) <= TOL[math]
+        if _strip_ok(sm, s, math, 1):
+            dx = sm.conv2d_bwd_data(dy, w, (IH, IW), (sh, sw), (ph, pw), math=math).cpu().numpy()
+            ref = oracle.conv2d_bwd_data(dY, W, (IH, IW), (sh, sw), (ph, pw))
+            ran += 1
+            if integer:
+                assert np.array_equal(dx.astype(np.float64), ref)
+            else:
+                assert normwise(dx, ref) <= TOL[math]
+        if math == "tf32" or s[4] <= 64:
+            assert ran == 2, "strip variant should serve this shape"
