@@ -61,13 +61,21 @@ struct TmaCfg {
     static constexpr int NTHREADS = (10 + NCONV) * 32;
     static constexpr int A_BYTES = BM * BK * 4;
     static constexpr int B_BYTES = BN * BK * 4;
-    static constexpr int STAGE_BYTES = PLANES * (A_BYTES + B_BYTES);
+    // 3xTF32 with a K-major A (fwd, dX): the converters write a_hi and a_lo straight into TMEM
+    // (tcgen05.st) and the MMAs read A from TMEM, so A is read from shared memory once per k-block
+    // instead of three times and no a_lo plane is stored there (the kernel is smem-bandwidth bound).
+    static constexpr bool A_TMEM = (PLANES == 2) && (OP == OP_FWD || OP == OP_DX);
+    static constexpr int B_OFF = A_TMEM ? A_BYTES : PLANES * A_BYTES;  // B (hi) offset in a stage
+    static constexpr int STAGE_BYTES = A_TMEM ? A_BYTES + 2 * B_BYTES : PLANES * (A_BYTES + B_BYTES);
     static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+    static constexpr int STAGES_TM = A_TMEM ? (512 - 2 * BN) / 64 : 8;  // TMEM slots for A (64 cols each)
+    static constexpr int STAGES_C = STAGES_RAW < STAGES_TM ? STAGES_RAW : STAGES_TM;
+    static constexpr int STAGES = STAGES_C > 8 ? 8 : STAGES_C;
     static constexpr bool IS_DW = (OP == OP_DW || OP == OP_DWT);
     static constexpr bool A_MN = IS_DW;
     static constexpr bool B_MN = (OP != OP_FWD);
-    static constexpr int ACC_COLS = 2 * BN;
+    static constexpr int A_TCOL0 = 2 * BN;  // TMEM column of A slot 0 (A_TMEM)
+    static constexpr int ACC_COLS = 2 * BN + (A_TMEM ? STAGES * 64 : 0);
     static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128 : ACC_COLS <= 256 ? 256 : 512;
     static constexpr int AUX_BYTES = 1024 + kMaxTaps * 16;
     static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + AUX_BYTES;
@@ -255,7 +263,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                     for (int it = 0; it < nkb; ++it) {
                         if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
                         const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
-                        const uint32_t sB = sA + PLANES * C::A_BYTES;
+                        const uint32_t sB = sA + C::B_OFF;
                         if (elect_one()) {
                             mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + C::B_BYTES);
 #pragma unroll
@@ -300,7 +308,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                     for (int it = 0; it < nkb; ++it) {
                         if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
                         const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
-                        const uint32_t sB = sA + PLANES * C::A_BYTES;
+                        const uint32_t sB = sA + C::B_OFF;
                         const uint32_t sX = OP == OP_DWT ? sA : sB;
                         const int iw0 = ow * p.sw, ih0 = oh * p.sh;
                         if (elect_one()) {
@@ -339,7 +347,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
             const uint32_t blay = C::B_MN ? kLayoutSW128Base32 : kLayoutSW128;
             // descriptors of stage 0; stage s / k-step g only add to the 14-bit start-address field
             const uint64_t adH0 = make_sdesc(tiles_addr, albo, asbo, alay);
-            const uint64_t bdH0 = make_sdesc(tiles_addr + PLANES * C::A_BYTES, blbo, bsbo, blay);
+            const uint64_t bdH0 = make_sdesc(tiles_addr + C::B_OFF, blbo, bsbo, blay);
             constexpr uint64_t A_LO = C::A_BYTES >> 4, B_LO = C::B_BYTES >> 4;
             constexpr uint64_t A_G = C::A_MN ? 64 : 2, B_G = C::B_MN ? 64 : 2;  // (1024 or 32 bytes) >> 4
             int s = 0, in_chunk = 0;
@@ -364,7 +372,12 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                         for (int g = 0; g < C::BK / 8; ++g) {
                             const uint64_t adH = adH0 + so + g * A_G, bdH = bdH0 + so + g * B_G;
                             const uint32_t acc0 = (in_chunk > 0 || g > 0) ? 1u : 0u;
-                            if (PLANES == 2) {
+                            if (C::A_TMEM) {
+                                const uint32_t ahi = tmem + (uint32_t)(C::A_TCOL0 + s * 64 + g * 8);
+                                mma_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);
+                                mma_tf32_ts(d, ahi, bdH + B_LO, IDESC, 1u);
+                                mma_tf32_ts(d, ahi, bdH, IDESC, 1u);
+                            } else if (PLANES == 2) {
                                 mma_tf32_ss(d, adH + A_LO, bdH, IDESC, acc0);
                                 mma_tf32_ss(d, adH, bdH + B_LO, IDESC, 1u);
                                 mma_tf32_ss(d, adH, bdH, IDESC, 1u);
@@ -404,17 +417,10 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                 const uint32_t r = q / C::STAGES;
                 mbar_wait(&aux->full[s], r & 1);
                 uint8_t* st = tiles_ptr + s * C::STAGE_BYTES;
-                const float4* aH = reinterpret_cast<const float4*>(st);
-                float4* aL = reinterpret_cast<float4*>(st + C::A_BYTES);
-                const float4* bH = reinterpret_cast<const float4*>(st + PLANES * C::A_BYTES);
-                float4* bL = reinterpret_cast<float4*>(st + PLANES * C::A_BYTES + C::B_BYTES);
-                constexpr int NA = C::A_BYTES / 16 / NCT, NB = C::B_BYTES / 16 / NCT;
-                static_assert(NA * NCT * 16 == C::A_BYTES && NB * NCT * 16 == C::B_BYTES, "converter split");
-                float4 va[NA], vb[NB];  // all loads first (ILP), then split + store
-#pragma unroll
-                for (int i = 0; i < NA; ++i) va[i] = aH[ct + i * NCT];
-#pragma unroll
-                for (int i = 0; i < NB; ++i) vb[i] = bH[ct + i * NCT];
+                const float4* bH = reinterpret_cast<const float4*>(st + C::B_OFF);
+                float4* bL = reinterpret_cast<float4*>(st + C::B_OFF + C::B_BYTES);
+                constexpr int NB = C::B_BYTES / 16 / NCT;
+                static_assert(NB * NCT * 16 == C::B_BYTES, "converter split");
                 auto lo4 = [](float4 v) {
                     float4 o;
                     o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
@@ -423,11 +429,47 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                     o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
                     return o;
                 };
+                float4 vb[NB];
 #pragma unroll
-                for (int i = 0; i < NA; ++i) aL[ct + i * NCT] = lo4(va[i]);
+                for (int i = 0; i < NB; ++i) vb[i] = bH[ct + i * NCT];
+                if (C::A_TMEM) {
+                    // this thread: A row 32*(warp%4)+lane, K half h: hi/lo -> TMEM slot s (tcgen05.st)
+                    const int qd = warp & 3, h = (warp - C::CONV_W0) >> 2;
+                    const int row = qd * 32 + lane;
+                    float4 v[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        v[c] = *reinterpret_cast<const float4*>(st + kmaj_off((uint32_t)row, (uint32_t)(4 * h + c)));
+                    uint32_t hi[16], lo[16];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const float e[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint32_t hb = __float_as_uint(e[k]) & 0xFFFFE000u;
+                            hi[c * 4 + k] = hb;
+                            lo[c * 4 + k] = __float_as_uint(e[k] - __uint_as_float(hb));
+                        }
+                    }
+                    const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(C::A_TCOL0 + s * 64 + h * 16);
+                    tmem_st_32x32b_x16(ta, hi);
+                    tmem_st_32x32b_x16(ta + 32, lo);
+                } else {
+                    const float4* aH = reinterpret_cast<const float4*>(st);
+                    float4* aL = reinterpret_cast<float4*>(st + C::A_BYTES);
+                    constexpr int NA = C::A_BYTES / 16 / NCT;
+                    static_assert(NA * NCT * 16 == C::A_BYTES, "converter split");
+                    float4 va[NA];
+#pragma unroll
+                    for (int i = 0; i < NA; ++i) va[i] = aH[ct + i * NCT];
+#pragma unroll
+                    for (int i = 0; i < NA; ++i) aL[ct + i * NCT] = lo4(va[i]);
+                }
 #pragma unroll
                 for (int i = 0; i < NB; ++i) bL[ct + i * NCT] = lo4(vb[i]);
+                if (C::A_TMEM) tmem_st_wait();
                 fence_proxy_async_smem();
+                tc_fence_before();
                 mbar_arrive(&aux->conv[s]);
             }
         }
