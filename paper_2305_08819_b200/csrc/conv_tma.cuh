@@ -64,7 +64,7 @@ struct TmaCfg {
     // 3xTF32 with a K-major A (fwd, dX): the converters write a_hi and a_lo straight into TMEM
     // (tcgen05.st) and the MMAs read A from TMEM, so A is read from shared memory once per k-block
     // instead of three times and no a_lo plane is stored there (the kernel is smem-bandwidth bound).
-    static constexpr bool A_TMEM = (PLANES == 2) && (OP == OP_FWD || OP == OP_DX);
+    static constexpr bool A_TMEM = (PLANES == 2);
     static constexpr int B_OFF = A_TMEM ? A_BYTES : PLANES * A_BYTES;  // B (hi) offset in a stage
     static constexpr int STAGE_BYTES = A_TMEM ? A_BYTES + 2 * B_BYTES : PLANES * (A_BYTES + B_BYTES);
     static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
     } else if (warp == C::MMA_W) {
         // ======================= MMA issuer (whole warp runs the loop, one elected lane issues)
         {
-            constexpr uint32_t IDESC = idesc_tf32(128, BN, C::A_MN, C::B_MN);
+            constexpr uint32_t IDESC = idesc_tf32(128, BN, C::A_TMEM ? false : C::A_MN, C::B_MN);  // TMEM A: K along columns
             const uint32_t albo = C::A_MN ? 4096u : 16u, blbo = C::B_MN ? 4096u : 16u;
             const uint32_t asbo = C::A_MN ? 512u : 1024u, bsbo = C::B_MN ? 512u : 1024u;
             const uint32_t alay = C::A_MN ? kLayoutSW128Base32 : kLayoutSW128;
@@ -436,20 +436,29 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                     // this thread: A row 32*(warp%4)+lane, K half h: hi/lo -> TMEM slot s (tcgen05.st)
                     const int qd = warp & 3, h = (warp - C::CONV_W0) >> 2;
                     const int row = qd * 32 + lane;
-                    float4 v[4];
+                    float e[16];
+                    if (C::A_MN) {  // MN-major A tile [32 k][128 m]: one 4-byte element per k
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        v[c] = *reinterpret_cast<const float4*>(st + kmaj_off((uint32_t)row, (uint32_t)(4 * h + c)));
+                        for (int k = 0; k < 16; ++k)
+                            e[k] = *reinterpret_cast<const float*>(st + mnmaj_off((uint32_t)(16 * h + k), (uint32_t)(row & ~3)) +
+                                                                   (row & 3) * 4);
+                    } else {  // K-major A tile [128 m][32 k]: four 16-B chunks of this row
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const float4 v =
+                                *reinterpret_cast<const float4*>(st + kmaj_off((uint32_t)row, (uint32_t)(4 * h + c)));
+                            e[4 * c] = v.x;
+                            e[4 * c + 1] = v.y;
+                            e[4 * c + 2] = v.z;
+                            e[4 * c + 3] = v.w;
+                        }
+                    }
                     uint32_t hi[16], lo[16];
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const float e[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const uint32_t hb = __float_as_uint(e[k]) & 0xFFFFE000u;
-                            hi[c * 4 + k] = hb;
-                            lo[c * 4 + k] = __float_as_uint(e[k] - __uint_as_float(hb));
-                        }
+                    for (int k = 0; k < 16; ++k) {
+                        const uint32_t hb = __float_as_uint(e[k]) & 0xFFFFE000u;
+                        hi[k] = hb;
+                        lo[k] = __float_as_uint(e[k] - __uint_as_float(hb));
                     }
                     const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(C::A_TCOL0 + s * 64 + h * 16);
                     tmem_st_32x32b_x16(ta, hi);
