@@ -40,14 +40,22 @@ struct StripCfg {
     static constexpr int SLABS = 4 * R + FW - 1;
     static constexpr int A_BYTES = SLABS * 4096;
     static constexpr int B_BYTES = FW * BN * 128;
-    static constexpr int STAGE_BYTES = PLANES * (A_BYTES + B_BYTES);
+    // 3xTF32: the converters write the R*FW A windows (hi and lo) into TMEM, so the 3 MMAs per
+    // k-step read A from TMEM and only b_lo is stored in shared memory (smem-bandwidth bound path)
+    static constexpr bool A_TMEM = (PLANES == 2);
+    static constexpr int B_OFF = A_TMEM ? A_BYTES : PLANES * A_BYTES;
+    static constexpr int STAGE_BYTES = A_TMEM ? A_BYTES + 2 * B_BYTES : PLANES * (A_BYTES + B_BYTES);
+    static constexpr int A_SLOT_COLS = R * FW * 64;  // TMEM columns per stage: (j, fw) windows x (hi 32 + lo 32)
     static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-    static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
+    static constexpr int STAGES_TM = A_TMEM ? (512 - 2 * R * BN) / A_SLOT_COLS : 6;
+    static constexpr int STAGES_C = STAGES_RAW < STAGES_TM ? STAGES_RAW : STAGES_TM;
+    static constexpr int STAGES = STAGES_C > 6 ? 6 : STAGES_C;
     static constexpr int NEPI = 8, TMA_W = 8, MMA_W = 9, CONV_W0 = 10;
     static constexpr int NCONV = PLANES == 2 ? 8 : 0;
     static constexpr int NTHREADS = (10 + NCONV) * 32;
     static constexpr bool B_MN = (OP == OP_DX);
-    static constexpr int ACC_COLS = 2 * R * BN;
+    static constexpr int A_TCOL0 = 2 * R * BN;
+    static constexpr int ACC_COLS = 2 * R * BN + (A_TMEM ? STAGES * A_SLOT_COLS : 0);
     static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128 : ACC_COLS <= 256 ? 256 : 512;
     static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 1024;
     static_assert(STAGES >= 2, "strip stage does not fit");
@@ -128,7 +136,7 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                 for (int cb = 0; cb < sp.CB; ++cb) {
                     if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
                     const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
-                    const uint32_t sB = sA + PLANES * C::A_BYTES;
+                    const uint32_t sB = sA + C::B_OFF;
                     if (elect_one()) {
                         mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + C::B_BYTES);
                         tma_load_5d(sA, &sp.mapA, &aux->full[s], 0, t.g * 32, col0, srow, cb);
@@ -147,7 +155,7 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
         // ======================= MMA issuer: R accumulators x FW taps x 4 k-steps per stage
         constexpr uint32_t IDESC = idesc_tf32(128, BN, false, C::B_MN);
         const uint64_t adH0 = make_sdesc(tiles_addr, 16u, 1024u, kLayoutSW128);
-        const uint64_t bdH0 = make_sdesc(tiles_addr + PLANES * C::A_BYTES, C::B_MN ? 4096u : 16u,
+        const uint64_t bdH0 = make_sdesc(tiles_addr + C::B_OFF, C::B_MN ? 4096u : 16u,
                                          C::B_MN ? 512u : 1024u, C::B_MN ? kLayoutSW128Base32 : kLayoutSW128);
         constexpr uint64_t A_LO = C::A_BYTES >> 4, B_LO = C::B_BYTES >> 4;
         constexpr uint64_t B_G = C::B_MN ? 64 : 2, B_TAP = (BN * 128) >> 4;
@@ -180,7 +188,13 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                             for (int g = 0; g < 4; ++g) {
                                 const uint64_t adH = a0 + g * 2, bdH = b0 + g * B_G;
                                 const uint32_t acc0 = (in_chunk > 0 || fw > 0 || g > 0) ? 1u : 0u;
-                                if (PLANES == 2) {
+                                if (C::A_TMEM) {
+                                    const uint32_t ahi =
+                                        tmem + (uint32_t)(C::A_TCOL0 + s * C::A_SLOT_COLS + (j * C::FW + fw) * 64 + g * 8);
+                                    mma_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);
+                                    mma_tf32_ts(d, ahi, bdH + B_LO, IDESC, 1u);
+                                    mma_tf32_ts(d, ahi, bdH, IDESC, 1u);
+                                } else if (PLANES == 2) {
                                     mma_tf32_ss(d, adH + A_LO, bdH, IDESC, acc0);
                                     mma_tf32_ss(d, adH, bdH + B_LO, IDESC, 1u);
                                     mma_tf32_ss(d, adH, bdH, IDESC, 1u);
@@ -227,7 +241,34 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                     o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
                     return o;
                 };
-                {
+                if (C::A_TMEM) {
+                    // window (j, fw) row 32*qd+lane = slab 4j+woff(fw)+qd, image lane; K half h
+                    const int qd = warp & 3, h = (warp - C::CONV_W0) >> 2;
+#pragma unroll
+                    for (int j = 0; j < R; ++j)
+#pragma unroll
+                        for (int fw = 0; fw < C::FW; ++fw) {
+                            const int woff = OP == OP_FWD ? fw : C::FW - 1 - fw;
+                            const uint8_t* slab = st + (4 * j + woff + qd) * 4096;
+                            uint32_t hi[16], lo[16];
+#pragma unroll
+                            for (int cq = 0; cq < 4; ++cq) {
+                                const float4 v = *reinterpret_cast<const float4*>(
+                                    slab + kmaj_off((uint32_t)lane, (uint32_t)(4 * h + cq)));
+                                const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) {
+                                    const uint32_t hb = __float_as_uint(e[k]) & 0xFFFFE000u;
+                                    hi[4 * cq + k] = hb;
+                                    lo[4 * cq + k] = __float_as_uint(e[k] - __uint_as_float(hb));
+                                }
+                            }
+                            const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) +
+                                                (uint32_t)(C::A_TCOL0 + s * C::A_SLOT_COLS + (j * C::FW + fw) * 64 + h * 16);
+                            tmem_st_32x32b_x16(ta, hi);
+                            tmem_st_32x32b_x16(ta + 32, lo);
+                        }
+                } else {
                     const float4* aH = reinterpret_cast<const float4*>(st);
                     float4* aL = reinterpret_cast<float4*>(st + C::A_BYTES);
                     constexpr int NA = (C::A_BYTES / 16 + NCT - 1) / NCT;
@@ -240,8 +281,8 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                         if (ct + i * NCT < C::A_BYTES / 16) aL[ct + i * NCT] = lo4(v[i]);
                 }
                 {
-                    const float4* bH = reinterpret_cast<const float4*>(st + PLANES * C::A_BYTES);
-                    float4* bL = reinterpret_cast<float4*>(st + PLANES * C::A_BYTES + C::B_BYTES);
+                    const float4* bH = reinterpret_cast<const float4*>(st + C::B_OFF);
+                    float4* bL = reinterpret_cast<float4*>(st + C::B_OFF + C::B_BYTES);
                     constexpr int NB = (C::B_BYTES / 16 + NCT - 1) / NCT;
                     float4 v[NB];
 #pragma unroll
@@ -251,7 +292,9 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                     for (int i = 0; i < NB; ++i)
                         if (ct + i * NCT < C::B_BYTES / 16) bL[ct + i * NCT] = lo4(v[i]);
                 }
+                if (C::A_TMEM) tmem_st_wait();
                 fence_proxy_async_smem();
+                tc_fence_before();
                 mbar_arrive(&aux->conv[s]);
                 if (++s == C::STAGES) {
                     s = 0;
