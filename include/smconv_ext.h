@@ -22,8 +22,9 @@ enum {
     CONV_VARIANT_AUTO = 0,
     CONV_VARIANT_GENERIC = 1,   /* register-staged implicit GEMM: any IC%4 / OC%4, any geometry */
     CONV_VARIANT_TMA = 2,       /* TMA-staged implicit GEMM: channel extents multiple of 32 */
-    CONV_VARIANT_STRIP = 3      /* TMA strips with input-slab reuse across filter columns:
+    CONV_VARIANT_STRIP = 3,     /* TMA strips with input-slab reuse across filter columns:
                                    stride-1 3-wide fwd / dX, BN <= 128 (TF32) / 64 (3xTF32) */
+    CONV_VARIANT_DIRECT = 4     /* CUDA-core fp32 direct conv for few-channel (IC <= 8) stems, fwd / dW */
 };
 
 /* Force a variant for all subsequent calls of `op` in this process (thread-safe);

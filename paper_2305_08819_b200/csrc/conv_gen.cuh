@@ -440,6 +440,19 @@ __global__ void __launch_bounds__(GenCfg<OP, BN, PLANES>::NTHREADS, 1)
     }
 }
 
+// dX positions of stride phases that no filter tap reaches (reading L5: written as 0), e.g. three
+// of the four phases of a 1x1 stride-2 shortcut: a streaming zero fill instead of MMA tiles.
+template <int UNUSED = 0>
+__global__ void __launch_bounds__(256) zero_phases_kernel(float4* __restrict__ dx, long long n4, int IC4, int IH, int IW,
+                                                          int sh, int sw, uint32_t empty_mask) {
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n4; e += (long long)gridDim.x * blockDim.x) {
+        const long long px = e / IC4;
+        const int iw = (int)(px % IW), ih = (int)((px / IW) % IH);
+        if ((empty_mask >> ((ih % sh) * sw + iw % sw)) & 1u) dx[e] = z;
+    }
+}
+
 // Deterministic split-K reduction: out[i] = sum_{s=0..S-1} ws[s*stride + i] in fixed order.
 template <int UNUSED = 0>
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ out,

@@ -17,6 +17,12 @@
 #include "conv_gen.cuh"
 #include "conv_strip.cuh"
 
+namespace smconv {  // conv_direct.cu
+bool direct_supported(int op, int IC, int OC, int FH, int FW, int OW, int sw);
+int direct_dw_blocks(int N, int OH);
+int direct_launch(int op, const GenParams& g, int blocks, cudaStream_t st, char* err, size_t errlen);
+}  // namespace smconv
+
 using namespace smconv;
 
 namespace {
@@ -45,7 +51,7 @@ void read_env_once() {
             if (j == std::string::npos) j = s.size();
             std::string item = s.substr(i, j - i);
             int op = -1, var = -1;
-            if (sscanf(item.c_str(), "%d:%d", &op, &var) == 2 && op >= 0 && op < 3 && var >= 0 && var <= 3)
+            if (sscanf(item.c_str(), "%d:%d", &op, &var) == 2 && op >= 0 && op < 3 && var >= 0 && var <= 4)
                 g_force[op].store(var);
             i = j + 1;
         }
@@ -100,6 +106,7 @@ struct Plan {
     int BN;
     int planes;
     int splits;
+    uint32_t zero_mask;  // dX stride phases with no tap (zero_phases_kernel)
     dim3 grid;
     size_t ws_bytes;
     long long out_elems;
@@ -161,6 +168,13 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
         else if (forced == CONV_VARIANT_STRIP)
             return fail(CONV_EUNSUPPORTED, "%s: STRIP variant forced but unsupported for this shape", op_name(op));
     }
+    if (forced == CONV_VARIANT_AUTO || forced == CONV_VARIANT_DIRECT) {
+        // few-channel stems: HBM-bound, K = FH*FW*IC tiny -> CUDA-core fp32 direct kernels
+        const bool direct_ok = direct_supported(op, d.IC, d.OC, d.FH, d.FW, d.OW, d.sw);
+        if (direct_ok) pl.variant = CONV_VARIANT_DIRECT;
+        else if (forced == CONV_VARIANT_DIRECT)
+            return fail(CONV_EUNSUPPORTED, "%s: DIRECT variant forced but unsupported for this shape", op_name(op));
+    }
 
     // 3xTF32 on the TMA variant promotes chunks into BN/2 fp32 registers per epilogue thread: BN <= 128
     auto bn_for = [&](int n) {
@@ -194,7 +208,13 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
                 g.phase_IWp[ph_i] = IWp;
                 g.phase_fd_IWp[ph_i] = make_fastdiv(IWp > 0 ? IWp : 1);
                 g.phase_tile0[ph_i] = m_tiles;
-                m_tiles += (IHp * IWp * d.N + 127) / 128;
+                // a phase with no filter tap at all (fh = rh+ph mod sh, fw likewise) is all zeros:
+                // no tiles; zero_phases_kernel writes it
+                bool th = false, tw = false;
+                for (int f = 0; f < d.FH; ++f) th |= ((rh + d.ph - f) % d.sh + d.sh) % d.sh == 0;
+                for (int f = 0; f < d.FW; ++f) tw |= ((rw + d.pw - f) % d.sw + d.sw) % d.sw == 0;
+                if (th && tw) m_tiles += (IHp * IWp * d.N + 127) / 128;
+                else if (pl.variant != CONV_VARIANT_STRIP) pl.zero_mask |= 1u << ph_i;
             }
         g.phase_tile0[g.nphase] = m_tiles;
         pl.BN = bn_for(g.Ngemm);
@@ -228,6 +248,9 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
     int splits = 1;
     if (pl.variant == CONV_VARIANT_STRIP) {
         // strip tiles (32 images x 4R positions) are plentiful: no split-K
+    } else if (pl.variant == CONV_VARIANT_DIRECT) {
+        // fwd: one block per output row; dW: per-block partials over (n, oh) rows, fixed-order sum
+        if (op == CONV_OP_BWD_FILTER) splits = direct_dw_blocks(d.N, d.OH);
     } else if (op == CONV_OP_BWD_FILTER) {
         const int need_prec = (nkb_est + kMaxKbPerChain - 1) / kMaxKbPerChain;
         int fill = kSMs / tiles;
@@ -305,7 +328,9 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
     g.B = B;
     g.out = pl.splits > 1 ? (float*)ws : out;
     cudaGetLastError();  // clear sticky-free earlier errors of the caller
-    if (pl.variant == CONV_VARIANT_STRIP) {
+    if (pl.variant == CONV_VARIANT_DIRECT) {
+        rc = direct_launch(op, g, pl.splits, st, g_detail, sizeof g_detail);
+    } else if (pl.variant == CONV_VARIANT_STRIP) {
         rc = strip_launch(op, pl.BN, pl.planes, g, st, g_detail, sizeof g_detail);
     } else if (pl.variant == CONV_VARIANT_TMA) {
         TmaParams tp = pl.tp;
@@ -327,6 +352,14 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
         splitk_reduce_kernel<0><<<blocks, 256, 0, st>>>((const float4*)ws, (float4*)out, n4, pl.splits, n4);
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: reduce launch failed: %s", op_name(op), cudaGetErrorString(e));
+    }
+    if (pl.zero_mask) {  // after the reduce: its workspace never held the empty phases
+        const long long n4 = pl.out_elems / 4;
+        int blocks = (int)((n4 + 255) / 256);
+        if (blocks > kSMs * 8) blocks = kSMs * 8;
+        zero_phases_kernel<0><<<blocks, 256, 0, st>>>((float4*)out, n4, d.IC / 4, d.IH, d.IW, d.sh, d.sw, pl.zero_mask);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: zero-fill launch failed: %s", op_name(op), cudaGetErrorString(e));
     }
     g_detail[0] = 0;
     return CONV_OK;
@@ -417,7 +450,7 @@ const char* conv2d_strerror(int code) {
 const char* conv2d_last_error_detail(void) { return g_detail; }
 
 int conv2d_force_variant(int op, int variant) {
-    if (op < 0 || op > 2 || variant < 0 || variant > 3) return fail(CONV_EARG, "conv2d_force_variant: bad op/variant");
+    if (op < 0 || op > 2 || variant < 0 || variant > 4) return fail(CONV_EARG, "conv2d_force_variant: bad op/variant");
     read_env_once();
     g_force[op].store(variant);
     return CONV_OK;
@@ -433,8 +466,12 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
     if (rc) return rc;
     if (buf && len)
         snprintf(buf, len, "variant=%s BN=%d planes=%d splits=%d grid=%ux%ux%u ws=%zu kernels=%d",
-                 pl.variant == CONV_VARIANT_STRIP ? "strip" : pl.variant == CONV_VARIANT_TMA ? "tma" : "generic", pl.BN, pl.planes, pl.splits, pl.grid.x,
-                 pl.grid.y, pl.grid.z, pl.ws_bytes, pl.splits > 1 ? 2 : 1);
+                 pl.variant == CONV_VARIANT_DIRECT ? "direct"
+                 : pl.variant == CONV_VARIANT_STRIP ? "strip"
+                 : pl.variant == CONV_VARIANT_TMA   ? "tma"
+                                                    : "generic",
+                 pl.BN, pl.planes, pl.splits, pl.grid.x,
+                 pl.grid.y, pl.grid.z, pl.ws_bytes, 1 + (pl.splits > 1) + (pl.zero_mask != 0));
     return CONV_OK;
 }
 
@@ -444,7 +481,7 @@ int conv2d_plan_kernels(int op, int N, int IH, int IW, int IC, int OC, int FH, i
     if (check_dims(op, d, math)) return -1;
     Plan pl;
     if (make_plan(op, d, math, pl)) return -1;
-    return pl.splits > 1 ? 2 : 1;
+    return 1 + (pl.splits > 1) + (pl.zero_mask != 0);
 }
 
 int smconv_selftest_host(void) {

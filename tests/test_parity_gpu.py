@@ -341,3 +341,32 @@ def test_strip_parity(env, force_strip, s, math):
                 assert normwise(dx, ref) <= TOL[math]
         if math == "tf32" or s[4] <= 64:
             assert ran == 2, "strip variant should serve this shape"
+
+
+# ---------------------------------------------------------------- DIRECT variant (few-channel stems)
+SWEEP_DIRECT = [
+    (4, 32, 32, 4, 64, 3, 3, 1, 1, 1, 1),     # the CIFAR stem (IC 3 -> 4)
+    (3, 9, 13, 4, 20, 3, 3, 2, 2, 1, 1),      # stride 2, ragged
+    (2, 12, 12, 4, 96, 5, 5, 1, 1, 2, 2),     # 5x5, OC not a multiple of 64
+    (2, 10, 10, 8, 64, 3, 3, 1, 1, 1, 1),     # IC 8
+    (5, 7, 7, 4, 192, 3, 3, 1, 1, 0, 0),      # GoogLeNet-stem OC, no padding
+]
+
+
+@pytest.mark.parametrize("s", SWEEP_DIRECT, ids=_id)
+def test_direct_parity(env, s):
+    torch, oracle, sm = env
+    N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw = s
+    assert "direct" in sm.plan_describe(0, s) and "direct" in sm.plan_describe(2, s)
+    for integer in (2, 0):
+        X, W, dY = gen(s, 30 + integer, integer=integer, stem=not integer)
+        x, w, dy = (torch.from_numpy(a).cuda() for a in (X, W, dY))
+        for math in ("3xtf32", "tf32"):  # DIRECT is exact fp32 FMA in both modes
+            y = sm.conv2d_fwd(x, w, (sh, sw), (ph, pw), math=math).cpu().numpy()
+            dw = sm.conv2d_bwd_filter(x, dy, (FH, FW), (sh, sw), (ph, pw), math=math).cpu().numpy()
+            ry = oracle.conv2d_fwd(X, W, (sh, sw), (ph, pw))
+            rw = oracle.conv2d_bwd_filter(X, dY, (FH, FW), (sh, sw), (ph, pw))
+            if integer:
+                assert np.array_equal(y.astype(np.float64), ry) and np.array_equal(dw.astype(np.float64), rw)
+            else:
+                assert normwise(y, ry) <= 1e-6 and normwise(dw, rw) <= 1e-6, (normwise(y, ry), normwise(dw, rw))
