@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kDirThreads) conv_direct_fwd_kernel(const __gr
 // block's (n, oh) rows, partitions summed in fixed order at the end -> per-block partial.
 // Rows stream through a 4-deep cp.async ring in smem (3 rows in flight per block): the kernel is
 // HBM-streaming (dY is 1 GB at batch 4096) and a one-row-at-a-time loop was latency bound.
-constexpr int kDirNB = 8;
+constexpr int kDirNB = 4;
 
 SMCONV_DEV void cp_async16(uint32_t dst, const void* src, bool valid) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
