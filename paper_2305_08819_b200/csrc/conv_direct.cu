@@ -30,6 +30,29 @@ struct DirectParams {
     int rows_per_block;
 };
 
+constexpr int kDirNB = 4;  // dW: cp.async row ring depth (3 rows in flight per block)
+
+SMCONV_DEV void cp_async16(uint32_t dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+SMCONV_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+SMCONV_DEV void cp_async_wait_nb2() { asm volatile("cp.async.wait_group %0;" ::"n"(kDirNB - 2) : "memory"); }
+SMCONV_DEV void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// cp.async the FH input rows of output row (n, oh) into Xs[fh][WIN][IC] (padding -> zero fill)
+SMCONV_DEV void direct_issue_rows(const DirectParams& p, float* Xs, int n, int oh, int t, int nthreads) {
+    const int IC4 = p.IC >> 2;
+    const uint32_t base = smem_u32(Xs);
+    for (int i = t; i < p.FH * p.WIN * IC4; i += nthreads) {
+        const int c4 = i % IC4, r = i / IC4;
+        const int col = r % p.WIN, fh = r / p.WIN;
+        const int ih = oh * p.sh - p.ph + fh, iw = col - p.pw;
+        const bool ok = (unsigned)ih < (unsigned)p.IH && (unsigned)iw < (unsigned)p.IW;
+        cp_async16(base + i * 16u, ok ? p.X + (((size_t)n * p.IH + ih) * p.IW + iw) * p.IC + 4 * c4 : p.X, ok);
+    }
+}
+
 // stage the FH input rows of output row (n, oh) into Xs[fh][WIN][IC] (padding -> zeros)
 SMCONV_DEV void direct_load_rows(const DirectParams& p, float* Xs, int n, int oh, int t, int nthreads) {
     const int IC4 = p.IC >> 2;
@@ -68,17 +91,26 @@ __global__ void __launch_bounds__(kDirThreads) conv_direct_fwd_kernel(const __gr
     const int slot = t / trow, tl = t - slot * trow;
     const int q = tl % OC4, ob = tl / OC4;
     const int rows = p.N * p.OH;
-    for (int r0 = blockIdx.x * rp; r0 < rows; r0 += gridDim.x * rp) {
-        __syncthreads();
+    // double-buffered row groups: group g+1 is cp.async'ed while group g is computed
+    auto issue_group = [&](int r0, int b) {
         for (int s = 0; s < rp; ++s)
             if (r0 + s < rows) {
                 const int rr = r0 + s, n = rr / p.OH, oh = rr - n * p.OH;
-                direct_load_rows(p, Xs0 + s * xs_stride, n, oh, t, kDirThreads);
+                direct_issue_rows(p, Xs0 + (b * rp + s) * xs_stride, n, oh, t, kDirThreads);
             }
+        cp_async_commit();
+    };
+    int buf = 0;
+    if (blockIdx.x * rp < rows) issue_group(blockIdx.x * rp, 0);
+    for (int r0 = blockIdx.x * rp; r0 < rows; r0 += gridDim.x * rp) {
+        const int nx = r0 + gridDim.x * rp;
+        if (nx < rows) issue_group(nx, buf ^ 1);
+        else cp_async_commit();
+        cp_async_wait_1();
         __syncthreads();
         const int row = r0 + slot;
         if (slot < rp && row < rows && tl < trow) {
-            const float* Xs = Xs0 + slot * xs_stride;
+            const float* Xs = Xs0 + (buf * rp + slot) * xs_stride;
             float acc[kDirOWB][4];
 #pragma unroll
             for (int j = 0; j < kDirOWB; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
@@ -108,7 +140,11 @@ __global__ void __launch_bounds__(kDirThreads) conv_direct_fwd_kernel(const __gr
                     *reinterpret_cast<float4*>(y + (size_t)(ow0 + j) * p.OC) =
                         make_float4(acc[j][0], acc[j][1], acc[j][2], acc[j][3]);
         }
+        __syncthreads();  // everyone is done with `buf` before the next group is issued into it
+        buf ^= 1;
     }
+    cp_async_commit();
+    asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // ---------------------------------------------------------------- weight gradient
@@ -116,15 +152,6 @@ __global__ void __launch_bounds__(kDirThreads) conv_direct_fwd_kernel(const __gr
 // block's (n, oh) rows, partitions summed in fixed order at the end -> per-block partial.
 // Rows stream through a 4-deep cp.async ring in smem (3 rows in flight per block): the kernel is
 // HBM-streaming (dY is 1 GB at batch 4096) and a one-row-at-a-time loop was latency bound.
-constexpr int kDirNB = 4;
-
-SMCONV_DEV void cp_async16(uint32_t dst, const void* src, bool valid) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
-                 : "memory");
-}
-SMCONV_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-SMCONV_DEV void cp_async_wait_nb2() { asm volatile("cp.async.wait_group %0;" ::"n"(kDirNB - 2) : "memory"); }
-
 template <int ACC4>  // accumulator float4 columns per thread = ceil(FW*IC / 4)
 __global__ void __launch_bounds__(kDirThreads) conv_direct_dw_kernel(const __grid_constant__ DirectParams p) {
     extern __shared__ float4 sm4[];
@@ -257,7 +284,7 @@ int direct_launch(int op, const GenParams& g, int blocks, cudaStream_t st, char*
         p.W = g.B;
         const int trow = (p.OC / 4) * ((p.OW + kDirOWB - 1) / kDirOWB);
         const int rp = trow >= kDirThreads ? 1 : kDirThreads / trow;
-        smem = (size_t)(p.K * p.OC + rp * xs) * sizeof(float);
+        smem = (size_t)(p.K * p.OC + 2 * rp * xs) * sizeof(float);  // W^T + 2 row-group buffers
         if (trow > kDirThreads || smem > 200 * 1024) {
             snprintf(err, errlen, "direct fwd: OC*OW too large (threads %d, smem %zu)", trow, smem);
             return CONV_EUNSUPPORTED;

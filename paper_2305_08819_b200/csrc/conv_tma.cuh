@@ -131,8 +131,17 @@ struct TileInfo {
     SMCONV_DEV void init(const TmaParams& tp, const GenParams& p, int w) {
         const int nt = w % tp.n_tiles;
         const int rest = w / tp.n_tiles;
-        split = rest % p.splits;
-        int mt = rest / p.splits;
+        int mt;
+        if (OP == OP_DW || OP == OP_DWT) {
+            // split (pixel range) outermost: all (m, n) tiles of one pixel range run together, so
+            // that range's dY and X are read from HBM once and re-used from L2 by every tile
+            // (m-tile-major order re-read them once per m-tile: 11.3 GB vs 2.1 GB compulsory, l1)
+            mt = rest % tp.m_tiles;
+            split = rest / tp.m_tiles;
+        } else {
+            split = rest % p.splits;
+            mt = rest / p.splits;
+        }
         phase = 0;
         if (OP == OP_DX) {
             while (phase + 1 < p.nphase && mt >= p.phase_tile0[phase + 1]) ++phase;
