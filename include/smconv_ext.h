@@ -24,7 +24,9 @@ enum {
     CONV_VARIANT_TMA = 2,       /* TMA-staged implicit GEMM: channel extents multiple of 32 */
     CONV_VARIANT_STRIP = 3,     /* TMA strips with input-slab reuse across filter columns:
                                    stride-1 3-wide fwd / dX, BN <= 128 (TF32) / 64 (3xTF32) */
-    CONV_VARIANT_DIRECT = 4     /* CUDA-core fp32 direct conv for few-channel (IC <= 8) stems, fwd / dW */
+    CONV_VARIANT_DIRECT = 4,    /* CUDA-core fp32 direct conv for few-channel (IC <= 8) stems, fwd / dW */
+    CONV_VARIANT_DWS = 5        /* dW of 3x3 s1 64->64 convs on 8/16/32-wide maps: one activation slab
+                                   per k-block shared by 4 taps (shift applied by the TF32 split stage) */
 };
 
 /* Force a variant for all subsequent calls of `op` in this process (thread-safe);

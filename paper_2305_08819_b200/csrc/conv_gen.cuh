@@ -458,9 +458,24 @@ template <int UNUSED = 0>
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ out,
                                                             long long n4, int splits, long long stride4) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+        // fixed summation order s = 0, 1, ..., splits-1 (deterministic); loads are batched 8 deep so
+        // a thread keeps 8 independent requests in flight (one at a time: 137 us for l1 dW's 512 splits)
         float4 a = ws[i];
-        for (int s = 1; s < splits; ++s) {
-            const float4 b = ws[s * stride4 + i];
+        int s = 1;
+        for (; s + 8 <= splits; s += 8) {
+            float4 b[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) b[u] = ws[(long long)(s + u) * stride4 + i];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                a.x += b[u].x;
+                a.y += b[u].y;
+                a.z += b[u].z;
+                a.w += b[u].w;
+            }
+        }
+        for (; s < splits; ++s) {
+            const float4 b = ws[(long long)s * stride4 + i];
             a.x += b.x;
             a.y += b.y;
             a.z += b.z;

@@ -48,6 +48,7 @@ struct __align__(64) TmaParams {
     int a_boxes;     // dwT: A boxes (X patches) per 128-row tile
     int a_box_cols;  // dwT: GEMM rows per A box (never crosses a tap)
     int chunk_kb;    // promotion interval in k-blocks (3xTF32)
+    int pf;          // dw: L2 prefetch distance in k-blocks (0 = off)
     int m_tiles, n_tiles;  // work decomposition (dx: m_tiles over all phases)
     int work;        // m_tiles * splits * n_tiles
 };
@@ -113,6 +114,20 @@ SMCONV_DEV void tma_load_5d(uint32_t dst, const CUtensorMap* map, uint64_t* bar,
             dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
         : "memory");
+}
+
+SMCONV_DEV void tma_prefetch_5d(const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4) {
+    asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+                 : "memory");
+}
+
+SMCONV_DEV void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
 }
 
 SMCONV_DEV void prefetch_tmap(const CUtensorMap* map) {
@@ -314,7 +329,34 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                     __syncwarp();
                     const uint32_t xbytes = nbox * bcols * 128;
                     const uint32_t tx = OP == OP_DWT ? xbytes + C::B_BYTES : C::A_BYTES + xbytes;
+                    // L2 prefetch cursor tp.pf k-blocks ahead: the stage ring alone covers only
+                    // STAGES k-blocks of TMA latency (l1 dW: the consumers waited on data half the time)
+                    int pnb = nb, ppos = pos, poh = oh, pow_ = ow;
+                    auto padv = [&]() {
+                        if (++pow_ == p.OW) {
+                            pow_ = 0;
+                            if (++poh == p.OH) poh = 0;
+                        }
+                        if (++ppos == P) {
+                            ppos = 0;
+                            ++pnb;
+                        }
+                    };
+                    const int pfd = min(tp.pf, nkb);
+                    for (int i = 0; i < pfd; ++i) padv();
                     for (int it = 0; it < nkb; ++it) {
+                        if (it + pfd < nkb && pfd > 0) {
+                            if (elect_one()) {
+                                const int piw = pow_ * p.sw, pih = poh * p.sh;
+                                for (int b = 0; b < nbox; ++b)
+                                    tma_prefetch_5d(OP == OP_DWT ? &tp.mapA : &tp.mapB, 0, pnb * 32, taps[b].z,
+                                                    piw + taps[b].x, pih + taps[b].y);
+                                if (OP == OP_DWT) tma_prefetch_4d(&tp.mapB, 0, pnb * 32, n0 / 32, ppos);
+                                else tma_prefetch_4d(&tp.mapA, 0, pnb * 32, ti.m0 / 32, ppos);
+                            }
+                            __syncwarp();
+                            padv();
+                        }
                         if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
                         const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
                         const uint32_t sB = sA + C::B_OFF;

@@ -21,6 +21,10 @@ namespace smconv {  // conv_direct.cu
 bool direct_supported(int op, int IC, int OC, int FH, int FW, int OW, int sw);
 int direct_dw_blocks(int N, int OH);
 int direct_launch(int op, const GenParams& g, int blocks, cudaStream_t st, char* err, size_t errlen);
+bool dws_supported(int op, int IC, int OC, int FH, int FW, int sh, int sw, int OH, int OW);
+int dws_splits(int N, int OH, int OW, int* kb_per_split);
+int dws_launch(int planes, const GenParams& g, int splits, int kb_per_split, cudaStream_t st, char* err,
+               size_t errlen);
 }  // namespace smconv
 
 using namespace smconv;
@@ -51,7 +55,7 @@ void read_env_once() {
             if (j == std::string::npos) j = s.size();
             std::string item = s.substr(i, j - i);
             int op = -1, var = -1;
-            if (sscanf(item.c_str(), "%d:%d", &op, &var) == 2 && op >= 0 && op < 3 && var >= 0 && var <= 4)
+            if (sscanf(item.c_str(), "%d:%d", &op, &var) == 2 && op >= 0 && op < 3 && var >= 0 && var <= 5)
                 g_force[op].store(var);
             i = j + 1;
         }
@@ -175,6 +179,12 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
         else if (forced == CONV_VARIANT_DIRECT)
             return fail(CONV_EUNSUPPORTED, "%s: DIRECT variant forced but unsupported for this shape", op_name(op));
     }
+    if (forced == CONV_VARIANT_AUTO || forced == CONV_VARIANT_DWS) {
+        const bool dws_ok = dws_supported(op, d.IC, d.OC, d.FH, d.FW, d.sh, d.sw, d.OH, d.OW);
+        if (dws_ok) pl.variant = CONV_VARIANT_DWS;
+        else if (forced == CONV_VARIANT_DWS)
+            return fail(CONV_EUNSUPPORTED, "%s: DWS variant forced but unsupported for this shape", op_name(op));
+    }
 
     // 3xTF32 on the TMA variant promotes chunks into BN/2 fp32 registers per epilogue thread: BN <= 128
     auto bn_for = [&](int n) {
@@ -251,6 +261,8 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
     } else if (pl.variant == CONV_VARIANT_DIRECT) {
         // fwd: one block per output row; dW: per-block partials over (n, oh) rows, fixed-order sum
         if (op == CONV_OP_BWD_FILTER) splits = direct_dw_blocks(d.N, d.OH);
+    } else if (pl.variant == CONV_VARIANT_DWS) {
+        splits = dws_splits(d.N, d.OH, d.OW, &g.kb_per_split);
     } else if (op == CONV_OP_BWD_FILTER) {
         const int need_prec = (nkb_est + kMaxKbPerChain - 1) / kMaxKbPerChain;
         int fill = kSMs / tiles;
@@ -332,6 +344,8 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
         rc = direct_launch(op, g, pl.splits, st, g_detail, sizeof g_detail);
     } else if (pl.variant == CONV_VARIANT_STRIP) {
         rc = strip_launch(op, pl.BN, pl.planes, g, st, g_detail, sizeof g_detail);
+    } else if (pl.variant == CONV_VARIANT_DWS) {
+        rc = dws_launch(pl.planes, g, pl.splits, g.kb_per_split, st, g_detail, sizeof g_detail);
     } else if (pl.variant == CONV_VARIANT_TMA) {
         TmaParams tp = pl.tp;
         rc = tma_launch(op, pl.BN, pl.planes, g, tp, pl.grid, st, g_detail, sizeof g_detail);
@@ -450,7 +464,7 @@ const char* conv2d_strerror(int code) {
 const char* conv2d_last_error_detail(void) { return g_detail; }
 
 int conv2d_force_variant(int op, int variant) {
-    if (op < 0 || op > 2 || variant < 0 || variant > 4) return fail(CONV_EARG, "conv2d_force_variant: bad op/variant");
+    if (op < 0 || op > 2 || variant < 0 || variant > 5) return fail(CONV_EARG, "conv2d_force_variant: bad op/variant");
     read_env_once();
     g_force[op].store(variant);
     return CONV_OK;
@@ -466,7 +480,8 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
     if (rc) return rc;
     if (buf && len)
         snprintf(buf, len, "variant=%s BN=%d planes=%d splits=%d grid=%ux%ux%u ws=%zu kernels=%d",
-                 pl.variant == CONV_VARIANT_DIRECT ? "direct"
+                 pl.variant == CONV_VARIANT_DWS      ? "dws"
+                 : pl.variant == CONV_VARIANT_DIRECT ? "direct"
                  : pl.variant == CONV_VARIANT_STRIP ? "strip"
                  : pl.variant == CONV_VARIANT_TMA   ? "tma"
                                                     : "generic",

@@ -18,6 +18,7 @@ CONV_OK, CONV_EARG, CONV_EALIGN, CONV_EALIAS, CONV_EWORKSPACE, CONV_EUNSUPPORTED
 CONV_MATH_FP32_3XTF32, CONV_MATH_TF32 = 0, 1
 CONV_OP_FWD, CONV_OP_BWD_DATA, CONV_OP_BWD_FILTER = 0, 1, 2
 CONV_VARIANT_AUTO, CONV_VARIANT_GENERIC, CONV_VARIANT_TMA, CONV_VARIANT_STRIP, CONV_VARIANT_DIRECT = 0, 1, 2, 3, 4
+CONV_VARIANT_DWS = 5
 MATH = {"3xtf32": CONV_MATH_FP32_3XTF32, "fp32": CONV_MATH_FP32_3XTF32, "tf32": CONV_MATH_TF32}
 
 EXPORTS = ("conv2d_out_hw", "conv2d_workspace_bytes", "conv2d_fwd", "conv2d_bwd_data", "conv2d_bwd_filter",
@@ -43,10 +44,12 @@ def lib():
     if _lib is None:
         with _lock:
             if _lib is None:
-                if not os.path.exists(LIB_PATH):
+                # SMCONV_LIB: an alternative in-tree build of the same library (A/B timing experiments)
+                path = os.environ.get("SMCONV_LIB") or LIB_PATH
+                if not os.path.exists(path):
                     raise ImportError("libsmconv.so not built (%s); run `python -c \"import __graft_entry__ as g; "
-                                      "g.build()\"`" % LIB_PATH)
-                L = ctypes.CDLL(LIB_PATH)
+                                      "g.build()\"`" % path)
+                L = ctypes.CDLL(path)
                 I, P, Z = ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t
                 L.conv2d_out_hw.argtypes = [I] * 8 + [ctypes.POINTER(I)] * 2
                 L.conv2d_out_hw.restype = I

@@ -370,3 +370,31 @@ def test_direct_parity(env, s):
                 assert np.array_equal(y.astype(np.float64), ry) and np.array_equal(dw.astype(np.float64), rw)
             else:
                 assert normwise(y, ry) <= 1e-6 and normwise(dw, rw) <= 1e-6, (normwise(y, ry), normwise(dw, rw))
+
+
+# ---------------------------------------------------------------- DWS variant (dW, 3x3 s1 64->64)
+SWEEP_DWS = [
+    (2, 32, 32, 64, 64, 3, 3, 1, 1, 1, 1),    # r.l1 / vgg2 geometry: one output row per k-block
+    (3, 16, 16, 64, 64, 3, 3, 1, 1, 1, 1),    # two rows per k-block
+    (5, 8, 8, 64, 64, 3, 3, 1, 1, 1, 1),      # four rows per k-block
+    (2, 34, 34, 64, 64, 3, 3, 1, 1, 0, 0),    # no padding (slab never out of bounds at the left)
+    (1, 30, 14, 64, 64, 3, 3, 1, 1, 2, 2),    # pad 2: OH 32 x OW 16, whole out-of-range slab rows
+    (40, 32, 32, 64, 64, 3, 3, 1, 1, 1, 1),   # chains of 13 k-blocks: 2 promotion chunks per item
+]
+
+
+@pytest.mark.parametrize("s", SWEEP_DWS, ids=_id)
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+def test_dws_parity(env, s, math):
+    torch, oracle, sm = env
+    N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw = s
+    assert "dws" in sm.plan_describe(2, s, sm.MATH[math])
+    for integer in (2, 0):
+        X, W, dY = gen(s, 40 + integer, integer=integer)
+        x, dy = torch.from_numpy(X).cuda(), torch.from_numpy(dY).cuda()
+        dw = sm.conv2d_bwd_filter(x, dy, (FH, FW), (sh, sw), (ph, pw), math=math).cpu().numpy()
+        ref = oracle.conv2d_bwd_filter(X, dY, (FH, FW), (sh, sw), (ph, pw))
+        if integer:
+            assert np.array_equal(dw.astype(np.float64), ref)
+        else:
+            assert normwise(dw, ref) <= TOL[math], normwise(dw, ref)
