@@ -53,6 +53,9 @@ def _load():
             f = getattr(lib, name)
             f.argtypes = [a, b, dp] + ints
             f.restype = ctypes.c_int
+        lib.oracle_conv2d_bwd_filter_at.argtypes = [fp, fp, ctypes.POINTER(ctypes.c_longlong), ctypes.c_int,
+                                                    dp] + ints
+        lib.oracle_conv2d_bwd_filter_at.restype = ctypes.c_int
         lib.oracle_out_hw.argtypes = [ctypes.c_int] * 8 + [ctypes.POINTER(ctypes.c_int)] * 2
         lib.oracle_out_hw.restype = ctypes.c_int
         lib.oracle_num_threads.restype = ctypes.c_int
@@ -127,6 +130,28 @@ def conv2d_bwd_filter(X, dY, kernel_hw, stride=(1, 1), padding=(1, 1)):
     if rc:
         raise ValueError("oracle_conv2d_bwd_filter: bad arguments")
     return dW
+
+
+def conv2d_bwd_filter_at(X, dY, kernel_hw, flat_idx, stride=(1, 1), padding=(1, 1)):
+    """O3 at selected flat indices of dW[OC,FH,FW,IC] (float64), full reduction over the batch —
+    for full-size parity on sampled outputs; equals conv2d_bwd_filter(...).ravel()[flat_idx]."""
+    X, xp = _f32(X)
+    dY, dyp = _f32(dY)
+    N, IH, IW, IC = X.shape
+    N2, OH, OW, OC = dY.shape
+    assert N == N2
+    FH, FW = kernel_hw
+    if out_hw(IH, IW, FH, FW, stride[0], stride[1], padding[0], padding[1]) != (OH, OW):
+        raise ValueError("dY extent does not match the forward output")
+    idx = np.ascontiguousarray(flat_idx, dtype=np.int64)
+    out = np.empty(idx.shape[0], np.float64)
+    rc = _load().oracle_conv2d_bwd_filter_at(xp, dyp, idx.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)),
+                                             int(idx.shape[0]), out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                             N, IH, IW, IC, OC, FH, FW, stride[0], stride[1],
+                                             padding[0], padding[1])
+    if rc:
+        raise ValueError("oracle_conv2d_bwd_filter_at: bad arguments")
+    return out
 
 
 def num_threads() -> int:

@@ -169,6 +169,45 @@ int oracle_conv2d_bwd_filter(const float* X, const float* dY, double* dW,
     return ORACLE_OK;
 }
 
+/*
+ * O3 at selected entries only (full-size parity on sampled outputs: "dW parity
+ * always uses the full batch"): out[i] = dW[idx[i]] for flat indices into [OC][FH][FW][IC], each
+ * computed exactly as oracle_conv2d_bwd_filter computes it (same terms, same n, oh, ow order), so
+ * it equals that function's entry bit for bit (pinned in tests/test_oracle_pins.py).
+ */
+int oracle_conv2d_bwd_filter_at(const float* X, const float* dY, const long long* idx, int nidx, double* out,
+                                int N, int IH, int IW, int IC, int OC, int FH, int FW,
+                                int sh, int sw, int ph, int pw) {
+    int OH, OW;
+    if (N < 1 || IC < 1 || OC < 1 || nidx < 0) return ORACLE_EARG;
+    if (oracle_out_hw(IH, IW, FH, FW, sh, sw, ph, pw, &OH, &OW)) return ORACLE_EARG;
+    const long long total = (long long)OC * FH * FW * IC;
+    for (int i = 0; i < nidx; ++i)
+        if (idx[i] < 0 || idx[i] >= total) return ORACLE_EARG;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int i = 0; i < nidx; ++i) {
+        long long r = idx[i];
+        const int ic = (int)(r % IC); r /= IC;
+        const int fw = (int)(r % FW); r /= FW;
+        const int fh = (int)(r % FH); r /= FH;
+        const int oc = (int)r;
+        double acc = 0.0;
+        for (int n = 0; n < N; ++n)
+            for (int oh = 0; oh < OH; ++oh) {
+                const int ih = oh * sh - ph + fh;
+                if (ih < 0 || ih >= IH) continue;
+                for (int ow = 0; ow < OW; ++ow) {
+                    const int iw = ow * sw - pw + fw;
+                    if (iw < 0 || iw >= IW) continue;
+                    acc += (double)dY[(((size_t)n * OH + oh) * OW + ow) * OC + oc] *
+                           (double)X[(((size_t)n * IH + ih) * IW + iw) * IC + ic];
+                }
+            }
+        out[i] = acc;
+    }
+    return ORACLE_OK;
+}
+
 /* Number of OpenMP threads the oracle will use (for the cpu_baseline "cores"). */
 int oracle_num_threads(void) {
 #ifdef _OPENMP

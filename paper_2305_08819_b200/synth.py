@@ -68,7 +68,8 @@ def layer_inputs(layer, N, config=0, layer_index=0, integer=0):
 
 def torch_layer_inputs(layer, N, device, seed, dtype=None):
     """Device-side seeded draws with the same distributions (bench workloads too large for
-    host generation).  Uses a torch.Generator on ``device``; never fed to the oracle."""
+    host generation).  Uses a torch.Generator on ``device``; the oracle sees these inputs only as
+    host copies in tests/test_fullsize_gpu.py (sampled outputs at the full bench size)."""
     import torch
     gen = torch.Generator(device=device)
     gen.manual_seed(int(seed))

@@ -324,3 +324,26 @@ def test_thread_count_independent(oracle_mod):
     b = oracle_mod.conv2d_bwd_filter(X, G, (3, 3))
     oracle_mod.set_num_threads(n0)
     np.testing.assert_array_equal(a, b)
+
+
+# ---------------------------------------------------------------- sampled O3 (full-size GPU parity helper)
+@pytest.mark.parametrize("s", SHAPES)
+def test_bwd_filter_at_matches_full_and_torch(oracle_mod, s):
+    """conv2d_bwd_filter_at (O3 at chosen entries, used for full-batch sampled parity) equals the
+    pinned full O3 bit for bit, and torch's float64 weight gradient (independent routine)."""
+    import torch
+    N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw = s
+    X, W, G, OH, OW = _inputs(s, 10)
+    full = oracle_mod.conv2d_bwd_filter(X, G, (FH, FW), (sh, sw), (ph, pw)).ravel()
+    g = np.random.default_rng(11)
+    idx = np.concatenate([[0, full.size - 1], g.choice(full.size, min(20, full.size), replace=False)])
+    got = oracle_mod.conv2d_bwd_filter_at(X, G, (FH, FW), idx, (sh, sw), (ph, pw))
+    np.testing.assert_array_equal(got, full[idx])
+    xt = torch.from_numpy(X).double().permute(0, 3, 1, 2)
+    wt = torch.from_numpy(W).double().permute(0, 3, 1, 2).contiguous().requires_grad_(True)
+    yt = torch.nn.functional.conv2d(xt, wt, stride=(sh, sw), padding=(ph, pw))
+    yt.backward(torch.from_numpy(G).double().permute(0, 3, 1, 2))
+    ref = wt.grad.permute(0, 2, 3, 1).numpy().ravel()[idx]
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+    with pytest.raises(ValueError):
+        oracle_mod.conv2d_bwd_filter_at(X, G, (FH, FW), [full.size], (sh, sw), (ph, pw))
