@@ -119,7 +119,10 @@ def test_plans_cover_network_shapes(sm):
                 for math in (0, 1):
                     d = sm.plan_describe(op, l.dims(128), math)
                     assert "variant=" in d
-                    assert sm.plan_kernels(op, l.dims(128), math) in (1, 2)
+                    # main kernel [+ split-K reduce] [+ zero fill of tap-less dX stride phases]
+                    k = sm.plan_kernels(op, l.dims(128), math)
+                    assert k == 1 + ("splits=1 " not in d) + (op == 1 and l.sh * l.sw > 1 and
+                                                               "variant=tma" in d and l.FH == 1), (l.name, op, d)
 
 
 def test_force_variant(sm):
