@@ -400,17 +400,20 @@ bool dws_supported(int op, int IC, int OC, int FH, int FW, int sh, int sw, int O
     return OH % (32 / OW) == 0;
 }
 
-// Split choice: chains of <= 256 k-blocks (the precision bound shared with the TMA variant) and
-// enough work items (3 groups per split) to fill the persistent grid.
+// Split choice: chains of <= 256 k-blocks (the precision bound shared with the TMA variant), and a
+// number of work items (3 groups per split) that fills whole rounds of the 148-CTA persistent grid,
+// at least 4 rounds: with 300 items (2.03 rounds) two thirds of the CTAs idled through the last one.
 int dws_splits(int N, int OH, int OW, int* kb_per_split) {
     const int RB = 32 / OW;
     const long long kb_total = (long long)N * (OH / RB);
-    const int need = (int)((kb_total + 255) / 256);
-    int splits = need > 100 ? need : 100;
-    if (splits > kb_total) splits = (int)kb_total;
-    if (splits < 1) splits = 1;
-    const int kps = (int)((kb_total + splits - 1) / splits);
-    *kb_per_split = kps;
+    const long long need = (kb_total + 255) / 256;
+    long long rounds = (3 * need + 147) / 148;
+    if (rounds < 4) rounds = 4;
+    long long smax = rounds * 148 / 3;
+    if (smax > kb_total) smax = kb_total;
+    if (smax < 1) smax = 1;
+    const long long kps = (kb_total + smax - 1) / smax;
+    *kb_per_split = (int)kps;
     return (int)((kb_total + kps - 1) / kps);
 }
 

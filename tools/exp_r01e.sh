@@ -1,3 +1,5 @@
-timeout 400 python -m pytest tests/test_parity_gpu.py -q --tb=short -x 2>&1 | tail -3
-for m in 3xtf32 tf32; do for v in 5 2; do python tools/layer_bench.py --layer l1.1b --op dw --reps 20 --math $m --variant $v; done; done
-python bench.py 2>&1 | tail -1
+timeout 400 python -m pytest tests/test_parity_gpu.py -q --tb=short -x -k "dws or direct or dp or random" 2>&1 | tail -2
+python bench.py --net vgg16 --global-batch 128 --steps 50 --warmup 5 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1
+python bench.py --net vgg16 --global-batch 128 --steps 50 --warmup 5 --math tf32 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1
+python bench.py --global-batch 512 --steps 30 --warmup 5 --no-cpu-baseline --no-e2e 2>/dev/null| tail -1
+python bench.py --no-cpu-baseline --no-e2e 2>/dev/null| tail -1
