@@ -31,6 +31,7 @@ namespace smconv {
 enum { OP_FWD = 0, OP_DX = 1, OP_DW = 2, OP_DWT = 3 };  // OP_DWT: dW with (tap,IC) rows, OC cols (TMA variant, OC <= 64)
 
 constexpr int kMaxTaps = 256;
+constexpr int kMaxTF = 16;  // TMA variant: filter rows / columns covered by the per-phase tap tables
 constexpr int kMaxPhases = 16;
 
 struct GenParams {
@@ -51,6 +52,14 @@ struct GenParams {
     int phase_tile0[kMaxPhases + 1];
     int phase_rh[kMaxPhases], phase_rw[kMaxPhases], phase_IHp[kMaxPhases], phase_IWp[kMaxPhases];
     FastDiv phase_fd_IWp[kMaxPhases];
+    // TMA variant (fwd: phase 0; dx: per stride phase): the filter rows (d = 0) / columns (d = 1)
+    // that can reach the phase, in increasing order, and their source offsets (source row =
+    // tile row origin + tf_off).  Host-built, so a tile's tap list and k-block count need no
+    // modulo / division per tap (that per-tile bookkeeping, run by every warp role, cost more
+    // issue slots than the 3xTF32 split itself on the short-K stride-2 dX tiles).
+    int8_t tf_n[kMaxPhases][2];
+    int8_t tf_f[kMaxPhases][2][kMaxTF];
+    int16_t tf_off[kMaxPhases][2][kMaxTF];
 };
 
 template <int OP, int BN, int PLANES>

@@ -108,8 +108,9 @@ bool tma_encode_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* 
 }
 
 bool tma_supported(int op, int N, int IC, int OC, int FH, int FW, int sh, int sw) {
-    (void)FH; (void)FW; (void)sh; (void)sw;
+    (void)sh; (void)sw;
     if (N % 32) return false;
+    if (FH > kMaxTF || FW > kMaxTF) return false;  // per-phase tap tables (GenParams::tf_*)
     if (op == CONV_OP_FWD) return IC % 32 == 0;
     return IC % 32 == 0 && OC % 32 == 0;
 }

@@ -194,10 +194,7 @@ struct TileInfo {
             kb_begin = split * p.kb_per_split;
             kb_end = min(nkb, kb_begin + p.kb_per_split);
         } else {
-            int ntaps = 0;
-            for (int fh = 0; fh < p.FH; ++fh)
-                for (int fw = 0; fw < p.FW; ++fw) ntaps += tap_valid(p, fh, fw, nullptr);
-            nkb = ntaps * tp.CB;
+            nkb = ntaps(p) * tp.CB;
             const int per = (nkb + p.splits - 1) / p.splits;
             kb_begin = split * per;
             kb_end = min(nkb, kb_begin + per);
@@ -205,24 +202,39 @@ struct TileInfo {
         if (kb_end < kb_begin) kb_end = kb_begin;
     }
 
-    // Is tap (fh, fw) used by this tile (some group has its source pixel in bounds)?  If so and
-    // t != nullptr, writes {dh, dw, tapfull}.
-    SMCONV_DEV bool tap_valid(const GenParams& p, int fh, int fw, int4* t) const {
-        int dh = fh, dw = fw;
-        if (OP == OP_DX) {
-            const int th = p.phase_rh[phase] + p.ph - fh, tw = p.phase_rw[phase] + p.pw - fw;
-            if (((th % p.sh) + p.sh) % p.sh != 0 || ((tw % p.sw) + p.sw) % p.sw != 0) return false;
-            dh = th / p.sh;
-            dw = tw / p.sw;
-        }
+    // Is candidate (kh, kw) of the tile's phase tap table used by this tile (some group has its
+    // source pixel in bounds)?  If so and t != nullptr, writes {dh, dw, fh * FW + fw}.
+    SMCONV_DEV bool tap_valid(const GenParams& p, int kh, int kw, int4* t) const {
+        const int ph_ = OP == OP_DX ? phase : 0;
+        const int dh = p.tf_off[ph_][0][kh], dw = p.tf_off[ph_][1][kw];
         const int srcH = OP == OP_FWD ? p.IH : p.OH;
         const int srcW = OP == OP_FWD ? p.IW : p.OW;
         bool any = false;
 #pragma unroll
         for (int g = 0; g < 4; ++g)
             if (g < ngrp) any |= grp[g].w && (unsigned)(grp[g].x + dh) < (unsigned)srcH && (unsigned)(grp[g].y + dw) < (unsigned)srcW;
-        if (any && t) *t = make_int4(dh, dw, fh * p.FW + fw, 0);
+        if (any && t) *t = make_int4(dh, dw, p.tf_f[ph_][0][kh] * p.FW + p.tf_f[ph_][1][kw], 0);
         return any;
+    }
+
+    // Number of taps used by this tile: one position per tile (G = 128) -> rows x columns in range
+    // (validity is separable); several positions -> the union over the groups, candidate by candidate.
+    SMCONV_DEV int ntaps(const GenParams& p) const {
+        const int ph_ = OP == OP_DX ? phase : 0;
+        const int nh = p.tf_n[ph_][0], nw = p.tf_n[ph_][1];
+        if (ngrp == 1) {
+            if (!grp[0].w) return 0;
+            const int srcH = OP == OP_FWD ? p.IH : p.OH;
+            const int srcW = OP == OP_FWD ? p.IW : p.OW;
+            int ch = 0, cw = 0;
+            for (int k = 0; k < nh; ++k) ch += (unsigned)(grp[0].x + p.tf_off[ph_][0][k]) < (unsigned)srcH;
+            for (int k = 0; k < nw; ++k) cw += (unsigned)(grp[0].y + p.tf_off[ph_][1][k]) < (unsigned)srcW;
+            return ch * cw;
+        }
+        int n = 0;
+        for (int kh = 0; kh < nh; ++kh)
+            for (int kw = 0; kw < nw; ++kw) n += tap_valid(p, kh, kw, nullptr);
+        return n;
     }
 };
 
@@ -278,9 +290,10 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                 if (nkb <= 0) continue;
                 if (OP == OP_FWD || OP == OP_DX) {
                     int nt = 0;
-                    for (int fh = 0; fh < p.FH; ++fh)
-                        for (int fw = 0; fw < p.FW; ++fw)
-                            if (ti.tap_valid(p, fh, fw, &taps[nt])) ++nt;  // same value from every lane
+                    const int ph_ = OP == OP_DX ? ti.phase : 0;
+                    for (int kh = 0; kh < p.tf_n[ph_][0]; ++kh)
+                        for (int kw = 0; kw < p.tf_n[ph_][1]; ++kw)
+                            if (ti.tap_valid(p, kh, kw, &taps[nt])) ++nt;  // same value from every lane
                     __syncwarp();
                     int j = ti.kb_begin / tp.CB, cb = ti.kb_begin - j * tp.CB;
                     int4 tap = taps[j];

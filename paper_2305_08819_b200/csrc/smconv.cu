@@ -254,6 +254,30 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
         out_elems = (long long)d.OC * d.FH * d.FW * d.IC;
         nkb_est = (g.P + 31) / 32;
     }
+    if (pl.variant == CONV_VARIANT_TMA && op != CONV_OP_BWD_FILTER) {
+        // per-phase tap tables (GenParams::tf_*): fwd -> all rows/columns, offset = filter index;
+        // dx phase (rh, rw) -> filter rows fh with (rh + ph - fh) % sh == 0, offset (rh + ph - fh) / sh
+        const int nph = op == CONV_OP_FWD ? 1 : g.nphase;
+        for (int k = 0; k < nph; ++k) {
+            for (int dim = 0; dim < 2; ++dim) {
+                const int F = dim == 0 ? d.FH : d.FW, S = dim == 0 ? d.sh : d.sw, P = dim == 0 ? d.ph : d.pw;
+                const int r = op == CONV_OP_FWD ? 0 : (dim == 0 ? g.phase_rh[k] : g.phase_rw[k]);
+                int n = 0;
+                for (int f = 0; f < F; ++f) {
+                    int off = f;
+                    if (op == CONV_OP_BWD_DATA) {
+                        const int t = r + P - f;
+                        if (((t % S) + S) % S != 0) continue;
+                        off = t / S;
+                    }
+                    g.tf_f[k][dim][n] = (int8_t)f;
+                    g.tf_off[k][dim][n] = (int16_t)off;
+                    ++n;
+                }
+                g.tf_n[k][dim] = (int8_t)n;
+            }
+        }
+    }
     const int tiles = m_tiles * n_tiles;
     int splits = 1;
     if (pl.variant == CONV_VARIANT_STRIP) {
