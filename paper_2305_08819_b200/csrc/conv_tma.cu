@@ -14,8 +14,7 @@ namespace smconv {
 namespace {
 
 // Tuning knobs (read once; for experiments only): SMCONV_TMA_G (32|128 images per A box),
-// SMCONV_TMA_L2PROMO (0..3 = NONE/64B/128B/256B), SMCONV_TMA_CHUNK (promotion interval, k-blocks),
-// SMCONV_TMA_PF (dW L2 prefetch distance, k-blocks).
+// SMCONV_TMA_L2PROMO (0..3 = NONE/64B/128B/256B), SMCONV_TMA_CHUNK (promotion interval, k-blocks).
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
     return e ? atoi(e) : dflt;
@@ -23,7 +22,6 @@ int env_int(const char* name, int dflt) {
 const int g_knob_G = env_int("SMCONV_TMA_G", 0);
 const int g_knob_promo = env_int("SMCONV_TMA_L2PROMO", 3);
 const int g_knob_chunk = env_int("SMCONV_TMA_CHUNK", 8);
-const int g_knob_pf = env_int("SMCONV_TMA_PF", 0);
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::atomic<int> g_encode_state{0};
@@ -125,7 +123,6 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
     tp.G = (g.N % 128 == 0) ? 128 : 32;
     if (g_knob_G == 32) tp.G = 32;
     tp.chunk_kb = g_knob_chunk > 0 ? g_knob_chunk : 8;
-    tp.pf = g_knob_pf;
     if (planes == 2 && BN > 128) {
         snprintf(err, errlen, "tma plan: BN %d > 128 in 3xTF32", BN);
         return CONV_EUNSUPPORTED;
@@ -151,6 +148,7 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
         } else {
             tp.b_box_cols = gcd(BN, g.IC);
             tp.b_boxes = BN / tp.b_box_cols;
+            if (g.IC % BN == 0) tp.dw_tap_tiles = g.IC / BN;  // n-tiles never straddle a tap
         }
     }
     return CONV_OK;

@@ -48,7 +48,8 @@ struct __align__(64) TmaParams {
     int a_boxes;     // dwT: A boxes (X patches) per 128-row tile
     int a_box_cols;  // dwT: GEMM rows per A box (never crosses a tap)
     int chunk_kb;    // promotion interval in k-blocks (3xTF32)
-    int pf;          // dw: L2 prefetch distance in k-blocks (0 = off)
+    int dw_tap_tiles;  // dw: IC / BN when every n-tile lies inside one filter tap (else 0): the tile's
+                       // k-blocks whose source pixels are all padding are skipped
     int m_tiles, n_tiles;  // work decomposition (dx: m_tiles over all phases)
     int work;        // m_tiles * splits * n_tiles
 };
@@ -116,20 +117,6 @@ SMCONV_DEV void tma_load_5d(uint32_t dst, const CUtensorMap* map, uint64_t* bar,
         : "memory");
 }
 
-SMCONV_DEV void tma_prefetch_5d(const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4) {
-    asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-                 : "memory");
-}
-
-SMCONV_DEV void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
-    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-                 : "memory");
-}
-
 SMCONV_DEV void prefetch_tmap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -142,6 +129,8 @@ struct TileInfo {
     int ngrp;
     int4 grp[4];  // {h0, w0, n_img, valid}
     int kb_begin, kb_end;
+    int nkb_eff;             // k-blocks that are issued (dw: positions where the tile's tap is in range)
+    int vr_lo, vr_hi, vc_lo, vc_hi;  // dw single-tap tiles: output rows / cols whose source is in range
 
     SMCONV_DEV void init(const TmaParams& tp, const GenParams& p, int w) {
         const int nt = w % tp.n_tiles;
@@ -200,6 +189,28 @@ struct TileInfo {
             kb_end = min(nkb, kb_begin + per);
         }
         if (kb_end < kb_begin) kb_end = kb_begin;
+        nkb_eff = kb_end - kb_begin;
+        vr_lo = 0, vr_hi = p.OH, vc_lo = 0, vc_hi = p.OW;
+        if (OP == OP_DW && tp.dw_tap_tiles > 0 && nkb_eff > 0) {
+            // a single-tap tile gets only zeros from the positions whose source pixel is padding
+            // (4x4 maps: 7 of 16 positions for a corner tap): those k-blocks are not issued at all
+            const int tap = n0 / tp.dw_tap_tiles, fh = tap / p.FW, fw = tap - fh * p.FW;
+            auto fdiv = [](int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
+            vr_lo = max(0, -fdiv(fh - p.ph, p.sh));  // ceil((ph - fh) / sh)
+            vr_hi = min(p.OH, fdiv(p.IH - 1 + p.ph - fh, p.sh) + 1);
+            vc_lo = max(0, -fdiv(fw - p.pw, p.sw));
+            vc_hi = min(p.OW, fdiv(p.IW - 1 + p.pw - fw, p.sw) + 1);
+            if (vr_hi < vr_lo) vr_hi = vr_lo;
+            if (vc_hi < vc_lo) vc_hi = vc_lo;
+            const int P = p.OH * p.OW, nvw = vc_hi - vc_lo, V = (vr_hi - vr_lo) * nvw;
+            auto cnt = [&](int k) {  // valid k-blocks below k (k-block = image block x position)
+                const int nb = k / P, pp = k - nb * P, r = pp / p.OW, c = pp - r * p.OW;
+                const int rb = min(max(r, vr_lo), vr_hi) - vr_lo;
+                const int cb = (r >= vr_lo && r < vr_hi) ? min(max(c, vc_lo), vc_hi) - vc_lo : 0;
+                return nb * V + rb * nvw + cb;
+            };
+            nkb_eff = cnt(kb_end) - cnt(kb_begin);
+        }
     }
 
     // Is candidate (kh, kw) of the tile's phase tap table used by this tile (some group has its
@@ -287,7 +298,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                 ti.init(tp, p, w);
                 const int n0 = ti.n0 * BN;
                 const int nkb = ti.kb_end - ti.kb_begin;
-                if (nkb <= 0) continue;
+                if (ti.nkb_eff <= 0) continue;
                 if (OP == OP_FWD || OP == OP_DX) {
                     int nt = 0;
                     const int ph_ = OP == OP_DX ? ti.phase : 0;
@@ -342,33 +353,19 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                     __syncwarp();
                     const uint32_t xbytes = nbox * bcols * 128;
                     const uint32_t tx = OP == OP_DWT ? xbytes + C::B_BYTES : C::A_BYTES + xbytes;
-                    // L2 prefetch cursor tp.pf k-blocks ahead: the stage ring alone covers only
-                    // STAGES k-blocks of TMA latency (l1 dW: the consumers waited on data half the time)
-                    int pnb = nb, ppos = pos, poh = oh, pow_ = ow;
-                    auto padv = [&]() {
-                        if (++pow_ == p.OW) {
-                            pow_ = 0;
-                            if (++poh == p.OH) poh = 0;
-                        }
-                        if (++ppos == P) {
-                            ppos = 0;
-                            ++pnb;
-                        }
-                    };
-                    const int pfd = min(tp.pf, nkb);
-                    for (int i = 0; i < pfd; ++i) padv();
                     for (int it = 0; it < nkb; ++it) {
-                        if (it + pfd < nkb && pfd > 0) {
-                            if (elect_one()) {
-                                const int piw = pow_ * p.sw, pih = poh * p.sh;
-                                for (int b = 0; b < nbox; ++b)
-                                    tma_prefetch_5d(OP == OP_DWT ? &tp.mapA : &tp.mapB, 0, pnb * 32, taps[b].z,
-                                                    piw + taps[b].x, pih + taps[b].y);
-                                if (OP == OP_DWT) tma_prefetch_4d(&tp.mapB, 0, pnb * 32, n0 / 32, ppos);
-                                else tma_prefetch_4d(&tp.mapA, 0, pnb * 32, ti.m0 / 32, ppos);
+                        if ((unsigned)(oh - ti.vr_lo) >= (unsigned)(ti.vr_hi - ti.vr_lo) ||
+                            (unsigned)(ow - ti.vc_lo) >= (unsigned)(ti.vc_hi - ti.vc_lo)) {
+                            // skipped k-block (all-padding source for this tile's tap): no stage
+                            if (++ow == p.OW) {
+                                ow = 0;
+                                if (++oh == p.OH) oh = 0;
                             }
-                            __syncwarp();
-                            padv();
+                            if (++pos == P) {
+                                pos = 0;
+                                ++nb;
+                            }
+                            continue;
                         }
                         if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
                         const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
@@ -419,7 +416,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
             for (int w = blockIdx.x; w < tp.work; w += gridDim.x) {
                 TileInfo<OP> ti;
                 ti.init(tp, p, w);
-                const int nkb = ti.kb_end - ti.kb_begin;
+                const int nkb = ti.nkb_eff;
                 for (int it = 0; it < nkb; ++it) {
                     const int buf = c & 1;
                     if (in_chunk == 0 && c >= 2) {
@@ -475,7 +472,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
         for (int w = blockIdx.x; w < tp.work; w += gridDim.x) {
             TileInfo<OP> ti;
             ti.init(tp, p, w);
-            const int nkb = ti.kb_end - ti.kb_begin;
+            const int nkb = ti.nkb_eff;
             for (int it = 0; it < nkb; ++it, ++q) {
                 const int s = q % C::STAGES;
                 const uint32_t r = q / C::STAGES;
@@ -557,7 +554,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
             TileInfo<OP> ti;
             ti.init(tp, p, w);
             const int n0 = ti.n0 * BN;
-            const int nkb = ti.kb_end - ti.kb_begin;
+            const int nkb = ti.nkb_eff;
             const int nch = nkb > 0 ? (nkb + CHK - 1) / CHK : 0;
             float* outp = p.out + (long long)ti.split * p.split_stride;
             long long obase = -1;

@@ -249,6 +249,9 @@ SWEEP_TMA = [
     (64, 8, 8, 256, 512, 1, 1, 2, 2, 0, 0),    # r.l4 sc
     (32, 6, 6, 96, 160, 5, 5, 1, 1, 2, 2),     # 5x5 p2, non-power-of-2 channels (multiples of 32)
     (32, 7, 5, 32, 64, 3, 3, 2, 2, 1, 1),      # odd extents, stride 2
+    # dW single-tap tiles skip the k-blocks whose source pixel is padding (IC % BN == 0):
+    (32, 7, 5, 128, 64, 3, 3, 2, 2, 2, 1),     # stride 2, asymmetric pad: partial row / column ranges
+    (64, 3, 3, 128, 32, 3, 3, 1, 1, 2, 2),     # pad 2: some taps in range at few positions only
 ]
 
 
