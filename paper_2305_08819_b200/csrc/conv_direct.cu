@@ -69,10 +69,15 @@ SMCONV_DEV void direct_load_rows(const DirectParams& p, float* Xs, int n, int oh
 
 // ---------------------------------------------------------------- forward
 // thread tile: 8 output columns x 4 output channels; W^T [K][OC] resident in smem per block.
+// TFH/TFW/TIC4/TSW: compile-time filter rows/cols, channel quads, column stride (0 = runtime):
+// the RGB stem instance <3,3,1,1> is fully unrolled (the runtime-bound loops issued ~2.5 non-FMA
+// instructions per FMA: FMA pipe 41 % busy); RAG = ragged last column block (OW % 8 != 0).
+template <int TFH, int TFW, int TIC4, int TSW, bool RAG>
 __global__ void __launch_bounds__(kDirThreads) conv_direct_fwd_kernel(const __grid_constant__ DirectParams p) {
     extern __shared__ float4 sm4[];
     float* Ws = reinterpret_cast<float*>(sm4);  // [K][OC]
-    const int OC4 = p.OC >> 2, IC4 = p.IC >> 2;
+    const int FH = TFH ? TFH : p.FH, FW = TFW ? TFW : p.FW, SW = TSW ? TSW : p.sw;
+    const int OC4 = p.OC >> 2, IC4 = TIC4 ? TIC4 : p.IC >> 2;
     const int owblocks = (p.OW + kDirOWB - 1) / kDirOWB;
     const int trow = OC4 * owblocks;                           // threads per output row
     const int rp = trow >= kDirThreads ? 1 : kDirThreads / trow;  // rows in flight per block
@@ -115,17 +120,20 @@ __global__ void __launch_bounds__(kDirThreads) conv_direct_fwd_kernel(const __gr
 #pragma unroll
             for (int j = 0; j < kDirOWB; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
             const int ow0 = ob * kDirOWB;
-            for (int fh = 0; fh < p.FH; ++fh)
-                for (int fw = 0; fw < p.FW; ++fw)
+#pragma unroll
+            for (int fh = 0; fh < FH; ++fh)
+#pragma unroll
+                for (int fw = 0; fw < FW; ++fw)
+#pragma unroll
                     for (int c4 = 0; c4 < IC4; ++c4) {
-                        const int k0 = ((fh * p.FW + fw) * IC4 + c4) * 4;
+                        const int k0 = ((fh * FW + fw) * IC4 + c4) * 4;
                         const float4* wv = reinterpret_cast<const float4*>(Ws) + (size_t)k0 * OC4 + q;
                         const float4 w0 = wv[0], w1 = wv[OC4], w2 = wv[2 * OC4], w3 = wv[3 * OC4];
                         const float4* xv = reinterpret_cast<const float4*>(Xs) + (fh * p.WIN + fw) * IC4 + c4;
 #pragma unroll
                         for (int j = 0; j < kDirOWB; ++j) {
-                            if (ow0 + j >= p.OW) break;  // ragged last column block
-                            const float4 x = xv[(ow0 + j) * p.sw * IC4];
+                            if (RAG && ow0 + j >= p.OW) break;  // ragged last column block
+                            const float4 x = xv[(ow0 + j) * SW * IC4];
                             acc[j][0] = fmaf(x.x, w0.x, fmaf(x.y, w1.x, fmaf(x.z, w2.x, fmaf(x.w, w3.x, acc[j][0]))));
                             acc[j][1] = fmaf(x.x, w0.y, fmaf(x.y, w1.y, fmaf(x.z, w2.y, fmaf(x.w, w3.y, acc[j][1]))));
                             acc[j][2] = fmaf(x.x, w0.z, fmaf(x.y, w1.z, fmaf(x.z, w2.z, fmaf(x.w, w3.z, acc[j][2]))));
@@ -291,10 +299,13 @@ int direct_launch(int op, const GenParams& g, int blocks, cudaStream_t st, char*
             snprintf(err, errlen, "direct fwd: OC*OW too large (threads %d, smem %zu)", trow, smem);
             return CONV_EUNSUPPORTED;
         }
-        if (smem > 48 * 1024) cudaFuncSetAttribute(conv_direct_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int grid = (p.N * p.OH + rp - 1) / rp;
         if (grid > 148 * 8) grid = 148 * 8;
-        conv_direct_fwd_kernel<<<grid, kDirThreads, smem, st>>>(p);
+        auto kern = conv_direct_fwd_kernel<0, 0, 0, 0, true>;
+        if (p.FH == 3 && p.FW == 3 && p.IC == 4 && p.sw == 1 && p.OW % kDirOWB == 0)
+            kern = conv_direct_fwd_kernel<3, 3, 1, 1, false>;  // the RGB stems
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, kDirThreads, smem, st>>>(p);
     } else {
         p.dY = g.A;  // run(): dW gets A = dY, B = X
         p.X = g.B;

@@ -22,7 +22,7 @@ struct Aux {
 // mode bit 8: converters also issue fence.proxy.async + tcgen05 fences
 // mode bit 16: the MMA warp issues nmma tf32 MMAs per k-block (M=128, N=BN, K=8): TS form (A in
 //              TMEM) unless bit 32 (SS form, A in smem); operands are garbage (timing only)
-template <int SS, int ST, int BN>
+template <int SS, int ST, int BN, int BM = 128>
 __global__ void __launch_bounds__(576, 1) ring_kernel(int iters, int mode, int nconvw, int nmma) {
     __shared__ Aux aux;
     __shared__ uint32_t tbase;
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(int iters, int mode, int n
             if (elect_one()) {
                 if (mode & 16) {
                     const uint32_t base = (smem_u32(dyn) + 1023u) & ~1023u;
-                    constexpr uint32_t IDESC = idesc_tf32(128, BN, false, true);
+                    constexpr uint32_t IDESC = idesc_tf32(BM, BN, false, true);
                     const uint64_t bd = make_sdesc(base, 4096u, 512u, kLayoutSW128Base32);
                     const uint64_t ad = make_sdesc(base + 65536, 16u, 1024u, kLayoutSW128);
                     for (int i = 0; i < nmma; ++i) {
@@ -112,27 +112,32 @@ int main() {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int smem = 140 * 1024;
-    cudaFuncSetAttribute(ring_kernel<6, 3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(ring_kernel<6, 3, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    struct Case { int mode, nconvw, nmma, bn; };
-    const Case cases[] = {{0, 8, 0, 64},   {3, 8, 0, 64},   {11, 8, 0, 64},  {18, 8, 12, 64}, {18, 8, 24, 64},
-                          {50, 8, 24, 64}, {27, 8, 24, 64}, {18, 8, 12, 128}, {18, 8, 24, 128}, {50, 8, 24, 128},
-                          {18, 8, 48, 64}, {18, 8, 96, 64}};
+    struct Case { int mode, nmma, bm, bn; };
+    const Case cases[] = {{18, 24, 128, 64}, {18, 24, 128, 128}, {18, 24, 128, 256}, {50, 24, 128, 256},
+                          {18, 24, 64, 64},  {18, 24, 64, 128},  {18, 24, 64, 256},  {50, 24, 64, 256},
+                          {50, 24, 64, 128}, {18, 48, 128, 32}};
     for (const Case& c : cases) {
-        auto k = c.bn == 64 ? ring_kernel<6, 3, 64> : ring_kernel<6, 3, 128>;
-        k<<<148, 576, smem>>>(iters, c.mode, c.nconvw, c.nmma);
+        void (*k)(int, int, int, int) = nullptr;
+        if (c.bm == 128 && c.bn == 32) k = ring_kernel<6, 3, 32, 128>;
+        if (c.bm == 128 && c.bn == 64) k = ring_kernel<6, 3, 64, 128>;
+        if (c.bm == 128 && c.bn == 128) k = ring_kernel<6, 3, 128, 128>;
+        if (c.bm == 128 && c.bn == 256) k = ring_kernel<6, 3, 256, 128>;
+        if (c.bm == 64 && c.bn == 64) k = ring_kernel<6, 3, 64, 64>;
+        if (c.bm == 64 && c.bn == 128) k = ring_kernel<6, 3, 128, 64>;
+        if (c.bm == 64 && c.bn == 256) k = ring_kernel<6, 3, 256, 64>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k<<<148, 576, smem>>>(iters, c.mode, 8, c.nmma);
         cudaEventRecord(e0);
-        for (int rep = 0; rep < 5; ++rep) k<<<148, 576, smem>>>(iters, c.mode, c.nconvw, c.nmma);
+        for (int rep = 0; rep < 5; ++rep) k<<<148, 576, smem>>>(iters, c.mode, 8, c.nmma);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
         cudaError_t err = cudaGetLastError();
         const double ns = ms / 5 * 1e6 / iters;
-        const double flop = 2.0 * 128 * c.bn * 8 * c.nmma * iters * 148;
-        printf("mode=%2d conv=%d commit=%d fences=%d mma=%d(%s) x%d N=%d: %.1f ns per k-block, %.0f TFLOP/s tf32  %s\n",
-               c.mode, c.mode & 1, (c.mode >> 1) & 1, (c.mode >> 3) & 1, (c.mode >> 4) & 1, (c.mode & 32) ? "ss" : "ts",
-               c.nmma, c.bn, ns, flop / (ms / 5 * 1e-3) / 1e12, cudaGetErrorString(err));
+        const double flop = 2.0 * c.bm * c.bn * 8 * c.nmma * iters * 148;
+        printf("mma=%s M=%d N=%d x%d: %.1f ns per k-block, %.0f TFLOP/s tf32  %s\n", (c.mode & 32) ? "ss" : "ts", c.bm,
+               c.bn, c.nmma, ns, flop / (ms / 5 * 1e-3) / 1e12, cudaGetErrorString(err));
     }
     return 0;
 }
