@@ -392,10 +392,10 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
         if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: reduce launch failed: %s", op_name(op), cudaGetErrorString(e));
     }
     if (pl.zero_mask) {  // after the reduce: its workspace never held the empty phases
-        const long long n4 = pl.out_elems / 4;
-        int blocks = (int)((n4 + 255) / 256);
-        if (blocks > kSMs * 8) blocks = kSMs * 8;
-        zero_phases_kernel<0><<<blocks, 256, 0, st>>>((float4*)out, n4, d.IC / 4, d.IH, d.IW, d.sh, d.sw, pl.zero_mask);
+        const long long rows = (long long)d.N * d.IH;
+        const int blocks = (int)(rows < kSMs * 8 ? rows : kSMs * 8);
+        zero_phases_kernel<0><<<blocks, 256, 0, st>>>((float4*)out, (long long)d.N * d.IH, d.IC / 4, d.IH, d.IW, d.sh, d.sw,
+                                                      pl.zero_mask);
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: zero-fill launch failed: %s", op_name(op), cudaGetErrorString(e));
     }
