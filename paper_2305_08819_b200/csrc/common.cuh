@@ -195,6 +195,71 @@ SMCONV_HD uint32_t mnmaj_off(uint32_t k, uint32_t mn) {
     return (mn >> 5) * 4096u + k * 128u + (((((mn >> 3) & 3u) ^ (k & 3u))) << 5) + (((mn >> 2) & 1u) << 4);
 }
 
+// ------------------------------------------------------------------ CTA pairs (cta_group::2)
+// A 2-CTA cluster runs one M = 256 MMA per instruction: each CTA holds 128 rows of A (here in its
+// own TMEM) and N/2 columns of B in its shared memory, each CTA's TMEM receives its 128 rows x N of
+// the accumulator.  Measured (tools/pair_bench.cu vs tools/ring_bench.cu, random operands, at the
+// power cap): N = 64 tiles 894 vs 507 TFLOP/s TF32, N = 128 tiles 898 vs 759.
+SMCONV_DEV uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+SMCONV_DEV void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// arrive (release, cluster scope) on the mbarrier at the same shared-memory offset in CTA `cta`
+SMCONV_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+        "r"(cta)
+        : "memory");
+}
+
+// wait with cluster-scope acquire (the arrivals came from the peer CTA)
+SMCONV_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "SMCONV_WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SMCONV_WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// both CTAs' warps with the same warp id execute these
+SMCONV_DEV void tmem_alloc2(uint32_t* dst, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+SMCONV_DEV void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// D[tmem, both CTAs] (+)= A[tmem, both CTAs] * B[smem, N/2 per CTA]^T; issued by one thread of CTA 0
+SMCONV_DEV void mma2_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+
+// arrive once on the mbarrier at this offset in both CTAs of the pair when the issued MMAs complete
+SMCONV_DEV void mma2_commit_both(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
 // ------------------------------------------------------------------ TF32 split
 SMCONV_DEV float tf32_rna(float x) {
     uint32_t r;

@@ -22,6 +22,7 @@ int env_int(const char* name, int dflt) {
 const int g_knob_G = env_int("SMCONV_TMA_G", 0);
 const int g_knob_promo = env_int("SMCONV_TMA_L2PROMO", 3);
 const int g_knob_chunk = env_int("SMCONV_TMA_CHUNK", 8);
+std::atomic<int> g_pair{env_int("SMCONV_PAIR", 0)};  // CTA pairs (smconv_set_pair)
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::atomic<int> g_encode_state{0};
@@ -60,15 +61,15 @@ bool encode(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, co
     return r == CUDA_SUCCESS;
 }
 
-template <int OP, int BN, int PLANES>
+template <int OP, int BN, int PLANES, bool PAIR>
 int launch_t(const TmaParams& tp, const GenParams& g, dim3 grid, cudaStream_t st, char* err, size_t errlen) {
-    using C = TmaCfg<OP, BN, PLANES>;
+    using C = TmaCfg<OP, BN, PLANES, PAIR>;
     static std::atomic<unsigned long long> attr_done{0};
     int dev = 0;
     cudaGetDevice(&dev);
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(attr_done.load() & bit)) {
-        if (cudaFuncSetAttribute(conv_tma_kernel<OP, BN, PLANES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(conv_tma_kernel<OP, BN, PLANES, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::SMEM_BYTES) != cudaSuccess) {
             snprintf(err, errlen, "cudaFuncSetAttribute(tma smem=%d): %s", C::SMEM_BYTES,
                      cudaGetErrorString(cudaGetLastError()));
@@ -76,19 +77,44 @@ int launch_t(const TmaParams& tp, const GenParams& g, dim3 grid, cudaStream_t st
         }
         attr_done.fetch_or(bit);
     }
-    conv_tma_kernel<OP, BN, PLANES><<<grid, C::NTHREADS, C::SMEM_BYTES, st>>>(tp, g);
+    if (PAIR) {  // 2-CTA clusters: one M = 256 tile per pair
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(C::NTHREADS, 1, 1);
+        cfg.dynamicSmemBytes = C::SMEM_BYTES;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, conv_tma_kernel<OP, BN, PLANES, PAIR>, tp, g);
+        if (e != cudaSuccess) {
+            snprintf(err, errlen, "cudaLaunchKernelEx(tma pair): %s", cudaGetErrorString(e));
+            return CONV_ECUDA;
+        }
+        return CONV_OK;
+    }
+    conv_tma_kernel<OP, BN, PLANES, PAIR><<<grid, C::NTHREADS, C::SMEM_BYTES, st>>>(tp, g);
     return CONV_OK;
 }
 
 template <int OP, int PLANES>
 int launch_bn(int BN, const TmaParams& tp, const GenParams& g, dim3 grid, cudaStream_t st, char* err, size_t n) {
+    constexpr bool PAIRABLE = PLANES == 2 && (OP == OP_FWD || OP == OP_DX);
+    if (PAIRABLE && tp.pair) {
+        if (BN == 64) return launch_t<OP, 64, PLANES, PAIRABLE>(tp, g, grid, st, err, n);
+        return launch_t<OP, 128, PLANES, PAIRABLE>(tp, g, grid, st, err, n);
+    }
     switch (BN) {
-        case 32: return launch_t<OP, 32, PLANES>(tp, g, grid, st, err, n);
-        case 64: return launch_t<OP, 64, PLANES>(tp, g, grid, st, err, n);
-        case 128: return launch_t<OP, 128, PLANES>(tp, g, grid, st, err, n);
+        case 32: return launch_t<OP, 32, PLANES, false>(tp, g, grid, st, err, n);
+        case 64: return launch_t<OP, 64, PLANES, false>(tp, g, grid, st, err, n);
+        case 128: return launch_t<OP, 128, PLANES, false>(tp, g, grid, st, err, n);
         default:
-            if (PLANES == 2) return launch_t<OP, 128, PLANES>(tp, g, grid, st, err, n);  // unreachable (BN capped)
-            return launch_t<OP, (PLANES == 2 ? 128 : 256), PLANES>(tp, g, grid, st, err, n);
+            if (PLANES == 2) return launch_t<OP, 128, PLANES, false>(tp, g, grid, st, err, n);  // unreachable (BN capped)
+            return launch_t<OP, (PLANES == 2 ? 128 : 256), PLANES, false>(tp, g, grid, st, err, n);
     }
 }
 
@@ -99,6 +125,8 @@ int launch_op(int BN, int planes, const TmaParams& tp, const GenParams& g, dim3 
 }
 
 }  // namespace
+
+int tma_set_pair(int on) { return g_pair.exchange(on); }
 
 bool tma_encode_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
                     const uint32_t* box, CUtensorMapSwizzle sw) {
@@ -131,6 +159,30 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
         tp.CB = g.IC / 32;
     } else if (op == CONV_OP_BWD_DATA) {
         tp.CB = g.OC / 32;
+    }
+    // CTA pairs (cta_group::2): fwd / dx in 3xTF32 when 256-row pair tiles (two 128-image blocks at
+    // one position) tile every phase exactly
+    const int pair_mode = g_pair.load();
+    if ((op == CONV_OP_FWD || op == CONV_OP_BWD_DATA) && planes == 2 && pair_mode && tp.G == 128 &&
+        g.N % 256 == 0 && (BN == 64 || BN == 128) && tp.m_tiles % 2 == 0) {
+        bool even = true;
+        if (op == CONV_OP_BWD_DATA)
+            for (int k = 0; k <= g.nphase; ++k) even &= g.phase_tile0[k] % 2 == 0;
+        if (even) {
+            tp.pair = 1;
+            if (pair_mode == 2 && BN == 128) {  // experiment: N = 64 pair tiles (6 TMEM stages instead of 4)
+                BN = 64;
+                tp.n_tiles = (g.Ngemm + BN - 1) / BN;
+            }
+            if (op == CONV_OP_BWD_DATA)
+                for (int k = 0; k <= g.nphase; ++k) g.phase_tile0[k] /= 2;
+            tp.m_tiles /= 2;
+            tp.work = tp.m_tiles * tp.n_tiles * g.splits;
+            const int pairs = tp.work < 74 ? tp.work : 74;
+            grid = dim3(2 * pairs, 1, 1);
+        }
+    }
+    if (op == CONV_OP_FWD || op == CONV_OP_BWD_DATA) {
     } else {
         tp.NB32 = g.N / 32;
         // one X box per (tap, contiguous channel run): gcd(cols, IC) GEMM columns never cross a tap
@@ -165,7 +217,7 @@ int tma_launch(int op, int BN, int planes, const GenParams& g, TmaParams& tp, di
         uint32_t ba[4] = {32, 1, 1, (uint32_t)tp.G};
         ok &= encode(&tp.mapA, g.A, 4, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B);
         uint64_t db[3] = {IC, T, OC}, sb[2] = {IC * 4, T * IC * 4};
-        uint32_t bb[3] = {32, 1, (uint32_t)BN};
+        uint32_t bb[3] = {32, 1, (uint32_t)(tp.pair ? BN / 2 : BN)};  // a pair splits B by columns
         ok &= encode(&tp.mapB, g.B, 3, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B);
     } else if (op == CONV_OP_BWD_DATA) {
         // A = dY (OC, OW, OH, N); B = W viewed (32 ic, OC, IC/32, T), MN-major
@@ -173,7 +225,7 @@ int tma_launch(int op, int BN, int planes, const GenParams& g, TmaParams& tp, di
         uint32_t ba[4] = {32, 1, 1, (uint32_t)tp.G};
         ok &= encode(&tp.mapA, g.A, 4, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B);
         uint64_t db[4] = {32, OC, IC / 32, T}, sb[3] = {T * IC * 4, 128, IC * 4};
-        uint32_t bb[4] = {32, 32, (uint32_t)(BN / 32), 1};
+        uint32_t bb[4] = {32, 32, (uint32_t)((tp.pair ? BN / 2 : BN) / 32), 1};
         ok &= encode(&tp.mapB, g.B, 4, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     } else if (g.dwt) {
         // transposed dW: A = X viewed (32 ic, N, IC/32, IW, IH), B = dY viewed (32 oc, N, OC/32, OH*OW)

@@ -48,21 +48,23 @@ struct __align__(64) TmaParams {
     int a_boxes;     // dwT: A boxes (X patches) per 128-row tile
     int a_box_cols;  // dwT: GEMM rows per A box (never crosses a tap)
     int chunk_kb;    // promotion interval in k-blocks (3xTF32)
+    int pair;          // fwd/dx 3xTF32: CTA pairs (cta_group::2, M = 256); work items are pair tiles
     int dw_tap_tiles;  // dw: IC / BN when every n-tile lies inside one filter tap (else 0): the tile's
                        // k-blocks whose source pixels are all padding are skipped
     int m_tiles, n_tiles;  // work decomposition (dx: m_tiles over all phases)
     int work;        // m_tiles * splits * n_tiles
 };
 
-template <int OP, int BN, int PLANES>
+template <int OP, int BN, int PLANES, bool PAIR = false>
 struct TmaCfg {
     static constexpr int BM = 128, BK = 32;
+    static constexpr int BNC = PAIR ? BN / 2 : BN;  // B columns staged by this CTA (a pair splits B)
     static constexpr int NEPI = 8;  // epilogue warps 0-7
     static constexpr int TMA_W = 8, MMA_W = 9, CONV_W0 = 10;
     static constexpr int NCONV = PLANES == 2 ? 8 : 0;  // converters: 8 warps keep up with N=64 MMAs
     static constexpr int NTHREADS = (10 + NCONV) * 32;
     static constexpr int A_BYTES = BM * BK * 4;
-    static constexpr int B_BYTES = BN * BK * 4;
+    static constexpr int B_BYTES = BNC * BK * 4;
     // 3xTF32 with a K-major A (fwd, dX): the converters write a_hi and a_lo straight into TMEM
     // (tcgen05.st) and the MMAs read A from TMEM, so A is read from shared memory once per k-block
     // instead of three times and no a_lo plane is stored there (the kernel is smem-bandwidth bound).
@@ -83,6 +85,7 @@ struct TmaCfg {
     static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + AUX_BYTES;
     static_assert(STAGES >= 2, "stage does not fit");
     static_assert(PLANES == 1 || BN <= 128, "3xTF32 promotion keeps BN/2 fp32 per epilogue thread");
+    static_assert(!PAIR || (PLANES == 2 && !IS_DW && BN >= 64), "CTA pairs: fwd / dx, 3xTF32");
 };
 
 struct TmaAux {
@@ -132,7 +135,7 @@ struct TileInfo {
     int nkb_eff;             // k-blocks that are issued (dw: positions where the tile's tap is in range)
     int vr_lo, vr_hi, vc_lo, vc_hi;  // dw single-tap tiles: output rows / cols whose source is in range
 
-    SMCONV_DEV void init(const TmaParams& tp, const GenParams& p, int w) {
+    SMCONV_DEV void init(const TmaParams& tp, const GenParams& p, int w, int rank = 0) {
         const int nt = w % tp.n_tiles;
         const int rest = w / tp.n_tiles;
         int mt;
@@ -159,7 +162,9 @@ struct TileInfo {
             // from L2 instead of re-read from HBM (a position-major walk thrashed L2: 3x X reads)
             const int P = OP == OP_DX ? p.phase_IHp[phase] * p.phase_IWp[phase] : p.OH * p.OW;
             const int ib = mt / P, pos = mt - ib * P;
-            m0 = pos * p.N + ib * 128;
+            // pair tiles: the two CTAs take image blocks 2*ib and 2*ib+1 at the same position, so
+            // both halves of the M = 256 tile have the same taps (one shared k-loop)
+            m0 = tp.pair ? pos * p.N + (2 * ib + rank) * 128 : pos * p.N + ib * 128;
         }
         n0 = nt;  // caller multiplies by BN
         ngrp = 0;
@@ -249,10 +254,10 @@ struct TileInfo {
     }
 };
 
-template <int OP, int BN, int PLANES>
-__global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
+template <int OP, int BN, int PLANES, bool PAIR = false>
+__global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
     conv_tma_kernel(const __grid_constant__ TmaParams tp, const __grid_constant__ GenParams p) {
-    using C = TmaCfg<OP, BN, PLANES>;
+    using C = TmaCfg<OP, BN, PLANES, PAIR>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     const uint32_t tiles_addr = (raw_addr + 1023u) & ~1023u;
@@ -261,16 +266,21 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int CHK = PLANES == 2 ? tp.chunk_kb : (1 << 30);
+    // pairs: both CTAs of a cluster walk the same pair tiles; CTA 0 issues the MMAs and owns the
+    // conv / tempty barriers (per-warp arrivals from both CTAs), commits arrive in both CTAs
+    const int rank = PAIR ? (int)cluster_ctarank() : 0;
+    const int wfirst = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int wstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&aux->full[s], 1);
-            mbar_init(&aux->conv[s], C::NCONV * 32);
+            mbar_init(&aux->conv[s], PAIR ? 2 * C::NCONV : C::NCONV * 32);
             mbar_init(&aux->empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&aux->tfull[b], 1);
-            mbar_init(&aux->tempty[b], C::NEPI * 32);
+            mbar_init(&aux->tempty[b], PAIR ? 2 * C::NEPI : C::NEPI * 32);
         }
         fence_mbar_init();
     }
@@ -278,9 +288,13 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
         prefetch_tmap(&tp.mapA);
         prefetch_tmap(&tp.mapB);
     }
-    if (warp == C::MMA_W) tmem_alloc(&aux->tmem_base, C::TMEM_COLS);
+    if (warp == C::MMA_W) {
+        if (PAIR) tmem_alloc2(&aux->tmem_base, C::TMEM_COLS);
+        else tmem_alloc(&aux->tmem_base, C::TMEM_COLS);
+    }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();  // the peer's barriers exist before any remote arrival
     tc_fence_after();
     const uint32_t tmem = aux->tmem_base;
 
@@ -293,9 +307,9 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
             int s = 0;
             uint32_t r = 0;  // stage index, ring round
             int4* taps = aux->ptaps;
-            for (int w = blockIdx.x; w < tp.work; w += gridDim.x) {
+            for (int w = wfirst; w < tp.work; w += wstep) {
                 TileInfo<OP> ti;
-                ti.init(tp, p, w);
+                ti.init(tp, p, w, rank);
                 const int n0 = ti.n0 * BN;
                 const int nkb = ti.kb_end - ti.kb_begin;
                 if (ti.nkb_eff <= 0) continue;
@@ -309,7 +323,10 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                     int j = ti.kb_begin / tp.CB, cb = ti.kb_begin - j * tp.CB;
                     int4 tap = taps[j];
                     for (int it = 0; it < nkb; ++it) {
-                        if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
+                        if (r > 0) {
+                            if (PAIR) mbar_wait_cluster(&aux->empty[s], (r - 1) & 1);
+                            else mbar_wait(&aux->empty[s], (r - 1) & 1);
+                        }
                         const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
                         const uint32_t sB = sA + C::B_OFF;
                         if (elect_one()) {
@@ -318,8 +335,9 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                             for (int g = 0; g < 4; ++g)
                                 if (g < ti.ngrp) tma_load_4d(sA + g * tp.G * 128, &tp.mapA, &aux->full[s], cb * 32,
                                             ti.grp[g].y + tap.y, ti.grp[g].x + tap.x, ti.grp[g].z);
-                            if (OP == OP_FWD) tma_load_3d(sB, &tp.mapB, &aux->full[s], cb * 32, tap.z, n0);
-                            else tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, cb * 32, n0 / 32, tap.z);
+                            const int nb0 = n0 + rank * C::BNC;  // this CTA's half of B (pairs)
+                            if (OP == OP_FWD) tma_load_3d(sB, &tp.mapB, &aux->full[s], cb * 32, tap.z, nb0);
+                            else tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, cb * 32, nb0 / 32, tap.z);
                         }
                         __syncwarp();
                         if (++cb == tp.CB) {
@@ -367,7 +385,10 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                             }
                             continue;
                         }
-                        if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
+                        if (r > 0) {
+                            if (PAIR) mbar_wait_cluster(&aux->empty[s], (r - 1) & 1);
+                            else mbar_wait(&aux->empty[s], (r - 1) & 1);
+                        }
                         const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
                         const uint32_t sB = sA + C::B_OFF;
                         const uint32_t sX = OP == OP_DWT ? sA : sB;
@@ -400,8 +421,9 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
         __syncwarp();
     } else if (warp == C::MMA_W) {
         // ======================= MMA issuer (whole warp runs the loop, one elected lane issues)
-        {
-            constexpr uint32_t IDESC = idesc_tf32(128, BN, C::A_TMEM ? false : C::A_MN, C::B_MN);  // TMEM A: K along columns
+        // pairs: CTA 0 issues M = 256 MMAs for both CTAs; CTA 1's MMA warp only owns its TMEM
+        if (!PAIR || rank == 0) {
+            constexpr uint32_t IDESC = idesc_tf32(PAIR ? 256 : 128, BN, C::A_TMEM ? false : C::A_MN, C::B_MN);  // TMEM A: K along columns
             const uint32_t albo = C::A_MN ? 4096u : 16u, blbo = C::B_MN ? 4096u : 16u;
             const uint32_t asbo = C::A_MN ? 512u : 1024u, bsbo = C::B_MN ? 512u : 1024u;
             const uint32_t alay = C::A_MN ? kLayoutSW128Base32 : kLayoutSW128;
@@ -413,17 +435,19 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
             constexpr uint64_t A_G = C::A_MN ? 64 : 2, B_G = C::B_MN ? 64 : 2;  // (1024 or 32 bytes) >> 4
             int s = 0, in_chunk = 0;
             uint32_t r = 0, c = 0;  // stage, ring round, chunk counter (all global across tiles)
-            for (int w = blockIdx.x; w < tp.work; w += gridDim.x) {
+            for (int w = wfirst; w < tp.work; w += wstep) {
                 TileInfo<OP> ti;
-                ti.init(tp, p, w);
+                ti.init(tp, p, w, rank);
                 const int nkb = ti.nkb_eff;
                 for (int it = 0; it < nkb; ++it) {
                     const int buf = c & 1;
                     if (in_chunk == 0 && c >= 2) {
-                        mbar_wait(&aux->tempty[buf], ((c >> 1) - 1) & 1);
+                        if (PAIR) mbar_wait_cluster(&aux->tempty[buf], ((c >> 1) - 1) & 1);
+                        else mbar_wait(&aux->tempty[buf], ((c >> 1) - 1) & 1);
                         tc_fence_after();
                     }
-                    mbar_wait(PLANES == 2 ? &aux->conv[s] : &aux->full[s], r & 1);
+                    if (PAIR) mbar_wait_cluster(&aux->conv[s], r & 1);
+                    else mbar_wait(PLANES == 2 ? &aux->conv[s] : &aux->full[s], r & 1);
                     tc_fence_after();
                     const uint32_t d = tmem + (uint32_t)(buf * BN);
                     const uint64_t so = (uint64_t)(s * C::STAGE_BYTES) >> 4;
@@ -433,7 +457,12 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                         for (int g = 0; g < C::BK / 8; ++g) {
                             const uint64_t adH = adH0 + so + g * A_G, bdH = bdH0 + so + g * B_G;
                             const uint32_t acc0 = (in_chunk > 0 || g > 0) ? 1u : 0u;
-                            if (C::A_TMEM) {
+                            if (PAIR) {
+                                const uint32_t ahi = tmem + (uint32_t)(C::A_TCOL0 + s * 64 + g * 8);
+                                mma2_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);
+                                mma2_tf32_ts(d, ahi, bdH + B_LO, IDESC, 1u);
+                                mma2_tf32_ts(d, ahi, bdH, IDESC, 1u);
+                            } else if (C::A_TMEM) {
                                 const uint32_t ahi = tmem + (uint32_t)(C::A_TCOL0 + s * 64 + g * 8);
                                 mma_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);
                                 mma_tf32_ts(d, ahi, bdH + B_LO, IDESC, 1u);
@@ -446,8 +475,13 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                                 mma_tf32_ss(d, adH, bdH, IDESC, acc0);
                             }
                         }
-                        mma_commit(&aux->empty[s]);
-                        if (last) mma_commit(&aux->tfull[buf]);
+                        if (PAIR) {
+                            mma2_commit_both(&aux->empty[s]);
+                            if (last) mma2_commit_both(&aux->tfull[buf]);
+                        } else {
+                            mma_commit(&aux->empty[s]);
+                            if (last) mma_commit(&aux->tfull[buf]);
+                        }
                     }
                     __syncwarp();
                     if (last) {
@@ -469,9 +503,9 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
         const int ct = tid - C::CONV_W0 * 32;
         constexpr int NCT = C::NCONV > 0 ? C::NCONV * 32 : 32;  // (dead code when PLANES == 1)
         uint32_t q = 0;
-        for (int w = blockIdx.x; w < tp.work; w += gridDim.x) {
+        for (int w = wfirst; w < tp.work; w += wstep) {
             TileInfo<OP> ti;
-            ti.init(tp, p, w);
+            ti.init(tp, p, w, rank);
             const int nkb = ti.nkb_eff;
             for (int it = 0; it < nkb; ++it, ++q) {
                 const int s = q % C::STAGES;
@@ -540,7 +574,12 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                 if (C::A_TMEM) tmem_st_wait();
                 fence_proxy_async_smem();
                 tc_fence_before();
-                mbar_arrive(&aux->conv[s]);
+                if (PAIR) {  // one arrival per warp, on CTA 0's barrier (it issues the MMAs)
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(&aux->conv[s], 0);
+                } else {
+                    mbar_arrive(&aux->conv[s]);
+                }
             }
         }
     } else {
@@ -550,9 +589,9 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
         constexpr int HALF = BN / 2;
         const uint32_t lane_addr = (uint32_t)(qd * 32) << 16;
         uint32_t c = 0;
-        for (int w = blockIdx.x; w < tp.work; w += gridDim.x) {
+        for (int w = wfirst; w < tp.work; w += wstep) {
             TileInfo<OP> ti;
-            ti.init(tp, p, w);
+            ti.init(tp, p, w, rank);
             const int n0 = ti.n0 * BN;
             const int nkb = ti.nkb_eff;
             const int nch = nkb > 0 ? (nkb + CHK - 1) / CHK : 0;
@@ -586,7 +625,8 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                 for (int e = 0; e < HALF; ++e) acc[e] = 0.f;
                 for (int k = 0; k < nch; ++k, ++c) {
                     const int buf = c & 1;
-                    mbar_wait(&aux->tfull[buf], (c >> 1) & 1);
+                    if (PAIR) mbar_wait_cluster(&aux->tfull[buf], (c >> 1) & 1);
+                    else mbar_wait(&aux->tfull[buf], (c >> 1) & 1);
                     tc_fence_after();
 #pragma unroll
                     for (int c0 = 0; c0 < HALF; c0 += 16) {
@@ -597,7 +637,12 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
                         for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
                     }
                     tc_fence_before();
-                    mbar_arrive(&aux->tempty[buf]);
+                    if (PAIR) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_remote(&aux->tempty[buf], 0);
+                    } else {
+                        mbar_arrive(&aux->tempty[buf]);
+                    }
                 }
                 if (obase >= 0) {
 #pragma unroll
@@ -609,7 +654,8 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
             } else {
                 const int buf = c & 1;
                 if (nch > 0) {
-                    mbar_wait(&aux->tfull[buf], (c >> 1) & 1);
+                    if (PAIR) mbar_wait_cluster(&aux->tfull[buf], (c >> 1) & 1);
+                    else mbar_wait(&aux->tfull[buf], (c >> 1) & 1);
                     tc_fence_after();
                 }
 #pragma unroll 1
@@ -643,9 +689,11 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES>::NTHREADS, 1)
 
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();  // the peer's MMAs / arrivals are done before TMEM is released
     if (warp == C::MMA_W) {
         tc_fence_after();
-        tmem_dealloc(tmem, C::TMEM_COLS);
+        if (PAIR) tmem_dealloc2(tmem, C::TMEM_COLS);
+        else tmem_dealloc(tmem, C::TMEM_COLS);
     }
 }
 

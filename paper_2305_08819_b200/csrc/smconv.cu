@@ -21,6 +21,7 @@ namespace smconv {  // conv_direct.cu
 bool direct_supported(int op, int IC, int OC, int FH, int FW, int OW, int sw);
 int direct_dw_blocks(int N, int OH);
 int direct_launch(int op, const GenParams& g, int blocks, cudaStream_t st, char* err, size_t errlen);
+int tma_set_pair(int on);
 bool dws_supported(int op, int IC, int OC, int FH, int FW, int sh, int sw, int OH, int OW);
 int dws_splits(int N, int OH, int OW, int* kb_per_split);
 int dws_launch(int planes, const GenParams& g, int splits, int kb_per_split, cudaStream_t st, char* err,
@@ -487,6 +488,8 @@ const char* conv2d_strerror(int code) {
 
 const char* conv2d_last_error_detail(void) { return g_detail; }
 
+int smconv_set_pair(int on) { return tma_set_pair(on ? 1 : 0); }
+
 int conv2d_force_variant(int op, int variant) {
     if (op < 0 || op > 2 || variant < 0 || variant > 5) return fail(CONV_EARG, "conv2d_force_variant: bad op/variant");
     read_env_once();
@@ -503,13 +506,13 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
     rc = make_plan(op, d, math, pl);
     if (rc) return rc;
     if (buf && len)
-        snprintf(buf, len, "variant=%s BN=%d planes=%d splits=%d grid=%ux%ux%u ws=%zu kernels=%d",
+        snprintf(buf, len, "variant=%s%s BN=%d planes=%d splits=%d grid=%ux%ux%u ws=%zu kernels=%d",
                  pl.variant == CONV_VARIANT_DWS      ? "dws"
                  : pl.variant == CONV_VARIANT_DIRECT ? "direct"
                  : pl.variant == CONV_VARIANT_STRIP ? "strip"
                  : pl.variant == CONV_VARIANT_TMA   ? "tma"
                                                     : "generic",
-                 pl.BN, pl.planes, pl.splits, pl.grid.x,
+                 (pl.variant == CONV_VARIANT_TMA && pl.tp.pair) ? " pair=2cta" : "", pl.BN, pl.planes, pl.splits, pl.grid.x,
                  pl.grid.y, pl.grid.z, pl.ws_bytes, 1 + (pl.splits > 1) + (pl.zero_mask != 0));
     return CONV_OK;
 }

@@ -252,15 +252,24 @@ SWEEP_TMA = [
     # dW single-tap tiles skip the k-blocks whose source pixel is padding (IC % BN == 0):
     (32, 7, 5, 128, 64, 3, 3, 2, 2, 2, 1),     # stride 2, asymmetric pad: partial row / column ranges
     (64, 3, 3, 128, 32, 3, 3, 1, 1, 2, 2),     # pad 2: some taps in range at few positions only
+    # CTA pairs (cta_group::2, M = 256) for fwd / dX in 3xTF32 need N % 256 == 0:
+    (256, 6, 6, 128, 128, 3, 3, 1, 1, 1, 1),   # BN 128 pairs
+    (256, 8, 8, 64, 64, 3, 3, 1, 1, 1, 1),     # BN 64 pairs (32-column B halves)
+    (256, 8, 8, 64, 128, 3, 3, 2, 2, 1, 1),    # stride-2 dX: 4 phases of pair tiles
+    (512, 3, 3, 96, 160, 3, 3, 1, 1, 1, 1),    # 2 pair image blocks, ragged N tile (160 = 128 + 32)
 ]
 
 
-@pytest.fixture
-def force_tma(env):
+@pytest.fixture(params=["single", "pair"])
+def force_tma(env, request):
+    """TMA variant forced; run once with 1-CTA tiles and once with CTA-pair (cta_group::2) tiles
+    (pairs apply to fwd / dX in 3xTF32 when N % 256 == 0, other cases are unchanged)."""
     _, _, sm = env
     for op in (0, 1, 2):
         sm.force_variant(op, sm.CONV_VARIANT_TMA)
+    old = sm.set_pair(request.param == "pair")
     yield
+    sm.set_pair(old)
     for op in (0, 1, 2):
         sm.force_variant(op, sm.CONV_VARIANT_AUTO)
 

@@ -5,6 +5,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../include tools/ring_bench.cu -o /tmp/ring_bench
 //   /tmp/ring_bench
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -42,6 +43,27 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(int iters, int mode, int n
         fence_mbar_init();
     }
     if (warp == 9) tmem_alloc(&tbase, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp < 4) {  // non-zero operands (power depends on data toggling): random smem, random TMEM A columns
+        uint32_t x = 0x9E3779B9u * (threadIdx.x + 1) + blockIdx.x;
+        float* f = reinterpret_cast<float*>(dyn);
+        for (int i = threadIdx.x; i < 130 * 1024 / 4; i += 128) {
+            x = x * 1664525u + 1013904223u;
+            f[i] = __uint_as_float((x >> 9) | 0x3F800000u) - 1.5f;
+        }
+        uint32_t v[16];
+        for (int c = 0; c < 256; c += 16) {
+            for (int e = 0; e < 16; ++e) {
+                x = x * 1664525u + 1013904223u;
+                v[e] = __float_as_uint(__uint_as_float((x >> 9) | 0x3F800000u) - 1.5f);
+            }
+            tmem_st_32x32b_x16(tbase + ((uint32_t)(warp * 32) << 16) + 256 + c, v);
+        }
+        tmem_st_wait();
+        fence_proxy_async_smem();
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -106,8 +128,9 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(int iters, int mode, int n
     }
 }
 
-int main() {
-    const int iters = 2657;
+int main(int argc, char** argv) {
+    const int iters = argc > 1 ? atoi(argv[1]) : 2657;
+    const int only = argc > 2 ? atoi(argv[2]) : -1;  // run only case #only
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -116,7 +139,9 @@ int main() {
     const Case cases[] = {{18, 24, 128, 64}, {18, 24, 128, 128}, {18, 24, 128, 256}, {50, 24, 128, 256},
                           {18, 24, 64, 64},  {18, 24, 64, 128},  {18, 24, 64, 256},  {50, 24, 64, 256},
                           {50, 24, 64, 128}, {18, 48, 128, 32}};
+    int ci = -1;
     for (const Case& c : cases) {
+        if (++ci, only >= 0 && ci != only) continue;
         void (*k)(int, int, int, int) = nullptr;
         if (c.bm == 128 && c.bn == 32) k = ring_kernel<6, 3, 32, 128>;
         if (c.bm == 128 && c.bn == 64) k = ring_kernel<6, 3, 64, 128>;
