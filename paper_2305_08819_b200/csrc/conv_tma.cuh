@@ -71,15 +71,18 @@ struct TmaCfg {
     static constexpr bool A_TMEM = (PLANES == 2);
     static constexpr int B_OFF = A_TMEM ? A_BYTES : PLANES * A_BYTES;  // B (hi) offset in a stage
     static constexpr int STAGE_BYTES = A_TMEM ? A_BYTES + 2 * B_BYTES : PLANES * (A_BYTES + B_BYTES);
+    // shared-memory stages (TMA ring) and TMEM A slots (converter -> MMA ring) are separate rings:
+    // an A slot is held only from its conversion to its MMAs' completion, a stage from the TMA issue
+    // on, so tying both to one index capped the TMA look-ahead at the TMEM slot count (4 at BN 128)
     static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-    static constexpr int STAGES_TM = A_TMEM ? (512 - 2 * BN) / 64 : 8;  // TMEM slots for A (64 cols each)
-    static constexpr int STAGES_C = STAGES_RAW < STAGES_TM ? STAGES_RAW : STAGES_TM;
-    static constexpr int STAGES = STAGES_C > 8 ? 8 : STAGES_C;
+    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+    static constexpr int NT_RAW = A_TMEM ? (512 - 2 * BN) / 64 : 1;  // TMEM A slots (64 cols each)
+    static constexpr int NT = NT_RAW > 8 ? 8 : NT_RAW;
     static constexpr bool IS_DW = (OP == OP_DW || OP == OP_DWT);
     static constexpr bool A_MN = IS_DW;
     static constexpr bool B_MN = (OP != OP_FWD);
     static constexpr int A_TCOL0 = 2 * BN;  // TMEM column of A slot 0 (A_TMEM)
-    static constexpr int ACC_COLS = 2 * BN + (A_TMEM ? STAGES * 64 : 0);
+    static constexpr int ACC_COLS = 2 * BN + (A_TMEM ? NT * 64 : 0);
     static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128 : ACC_COLS <= 256 ? 256 : 512;
     static constexpr int AUX_BYTES = 1024 + kMaxTaps * 16;
     static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + AUX_BYTES;
@@ -89,7 +92,7 @@ struct TmaCfg {
 };
 
 struct TmaAux {
-    uint64_t full[8], conv[8], empty[8];
+    uint64_t full[8], conv[8], empty[8], tfree[8];
     uint64_t tfull[2], tempty[2];
     uint32_t tmem_base;
     int4 ptaps[kMaxTaps];  // producer-private per-tile tap list / X-box geometry
@@ -275,8 +278,11 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&aux->full[s], 1);
-            mbar_init(&aux->conv[s], PAIR ? 2 * C::NCONV : C::NCONV * 32);
             mbar_init(&aux->empty[s], 1);
+        }
+        for (int t = 0; t < C::NT; ++t) {
+            mbar_init(&aux->conv[t], PAIR ? 2 * C::NCONV : C::NCONV * 32);
+            mbar_init(&aux->tfree[t], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&aux->tfull[b], 1);
@@ -434,7 +440,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             constexpr uint64_t A_LO = C::A_BYTES >> 4, B_LO = C::B_BYTES >> 4;
             constexpr uint64_t A_G = C::A_MN ? 64 : 2, B_G = C::B_MN ? 64 : 2;  // (1024 or 32 bytes) >> 4
             int s = 0, in_chunk = 0;
-            uint32_t r = 0, c = 0;  // stage, ring round, chunk counter (all global across tiles)
+            uint32_t r = 0, c = 0, q = 0;  // stage, ring round, chunk counter, k-block (global across tiles)
             for (int w = wfirst; w < tp.work; w += wstep) {
                 TileInfo<OP> ti;
                 ti.init(tp, p, w, rank);
@@ -446,8 +452,10 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                         else mbar_wait(&aux->tempty[buf], ((c >> 1) - 1) & 1);
                         tc_fence_after();
                     }
-                    if (PAIR) mbar_wait_cluster(&aux->conv[s], r & 1);
-                    else mbar_wait(PLANES == 2 ? &aux->conv[s] : &aux->full[s], r & 1);
+                    const uint32_t t = q % C::NT, rt = q / C::NT;  // TMEM A slot
+                    if (PAIR) mbar_wait_cluster(&aux->conv[t], rt & 1);
+                    else if (PLANES == 2) mbar_wait(&aux->conv[t], rt & 1);
+                    else mbar_wait(&aux->full[s], r & 1);
                     tc_fence_after();
                     const uint32_t d = tmem + (uint32_t)(buf * BN);
                     const uint64_t so = (uint64_t)(s * C::STAGE_BYTES) >> 4;
@@ -458,12 +466,12 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                             const uint64_t adH = adH0 + so + g * A_G, bdH = bdH0 + so + g * B_G;
                             const uint32_t acc0 = (in_chunk > 0 || g > 0) ? 1u : 0u;
                             if (PAIR) {
-                                const uint32_t ahi = tmem + (uint32_t)(C::A_TCOL0 + s * 64 + g * 8);
+                                const uint32_t ahi = tmem + (uint32_t)(C::A_TCOL0 + t * 64 + g * 8);
                                 mma2_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);
                                 mma2_tf32_ts(d, ahi, bdH + B_LO, IDESC, 1u);
                                 mma2_tf32_ts(d, ahi, bdH, IDESC, 1u);
                             } else if (C::A_TMEM) {
-                                const uint32_t ahi = tmem + (uint32_t)(C::A_TCOL0 + s * 64 + g * 8);
+                                const uint32_t ahi = tmem + (uint32_t)(C::A_TCOL0 + t * 64 + g * 8);
                                 mma_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);
                                 mma_tf32_ts(d, ahi, bdH + B_LO, IDESC, 1u);
                                 mma_tf32_ts(d, ahi, bdH, IDESC, 1u);
@@ -477,9 +485,11 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                         }
                         if (PAIR) {
                             mma2_commit_both(&aux->empty[s]);
+                            mma2_commit_both(&aux->tfree[t]);
                             if (last) mma2_commit_both(&aux->tfull[buf]);
                         } else {
                             mma_commit(&aux->empty[s]);
+                            if (C::A_TMEM) mma_commit(&aux->tfree[t]);
                             if (last) mma_commit(&aux->tfull[buf]);
                         }
                     }
@@ -494,6 +504,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                         s = 0;
                         ++r;
                     }
+                    ++q;
                 }
             }
         }
@@ -510,7 +521,13 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             for (int it = 0; it < nkb; ++it, ++q) {
                 const int s = q % C::STAGES;
                 const uint32_t r = q / C::STAGES;
+                const uint32_t t = q % C::NT, rt = q / C::NT;  // TMEM A slot
                 mbar_wait(&aux->full[s], r & 1);
+                if (C::A_TMEM && rt > 0) {  // slot t's previous k-block has been multiplied
+                    if (PAIR) mbar_wait_cluster(&aux->tfree[t], (rt - 1) & 1);
+                    else mbar_wait(&aux->tfree[t], (rt - 1) & 1);
+                    tc_fence_after();
+                }
                 uint8_t* st = tiles_ptr + s * C::STAGE_BYTES;
                 const float4* bH = reinterpret_cast<const float4*>(st + C::B_OFF);
                 float4* bL = reinterpret_cast<float4*>(st + C::B_OFF + C::B_BYTES);
@@ -555,7 +572,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                         hi[k] = hb;
                         lo[k] = __float_as_uint(e[k] - __uint_as_float(hb));
                     }
-                    const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(C::A_TCOL0 + s * 64 + h * 16);
+                    const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(C::A_TCOL0 + t * 64 + h * 16);
                     tmem_st_32x32b_x16(ta, hi);
                     tmem_st_32x32b_x16(ta + 32, lo);
                 } else {
@@ -576,9 +593,9 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                 tc_fence_before();
                 if (PAIR) {  // one arrival per warp, on CTA 0's barrier (it issues the MMAs)
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_remote(&aux->conv[s], 0);
+                    if (lane == 0) mbar_arrive_remote(&aux->conv[t], 0);
                 } else {
-                    mbar_arrive(&aux->conv[s]);
+                    mbar_arrive(&aux->conv[t]);
                 }
             }
         }
