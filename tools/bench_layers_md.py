@@ -28,7 +28,7 @@ def main():
     for e in extra:
         d = last_json(e)
         c = d.get("config", {})
-        print("* `%s` %s: **%.0f %s**, %.3f ms/step, roofline %s %.3f of %s (%s), SM clock %s MHz\n" % (
+        print("* `%s` %s: **%.0f %s**, %.3f ms/step, dominant call %s-bound at %.3f of its peak (%s; %s), SM clock %s MHz\n" % (
             c.get("workload", d.get("impl", "")), c.get("math", ""), d["value"], d["unit"], d["ms_per_step"],
             (d.get("roofline") or {}).get("bound"), (d.get("roofline") or {}).get("frac") or 0.0,
             (d.get("roofline") or {}).get("unit"), ((d.get("roofline") or {}).get("kernel") or "")[:60],

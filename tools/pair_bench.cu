@@ -20,14 +20,16 @@ __device__ __forceinline__ void cluster_sync() {
 }
 
 template <int BN, bool SS>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) pair_kernel(int iters, int nmma) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) pair_kernel(int iters, int nmma, int commits_per_iter) {
     __shared__ uint64_t bar;
+    __shared__ uint64_t bar2[4];
     __shared__ uint32_t tbase;
     extern __shared__ __align__(1024) uint8_t dyn[];
     const int warp = threadIdx.x >> 5;
     const uint32_t rank = cluster_rank();
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
+        for (int i = 0; i < 4; ++i) mbar_init(&bar2[i], 1);
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -68,6 +70,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) pair_kernel(
         const uint64_t ad = make_sdesc(base + 65536, 16u, 1024u, kLayoutSW128);
         for (int q = 0; q < iters; ++q) {
             if (elect_one()) {
+                if (commits_per_iter > 0 && q > 0)
+                    for (int cc = 0; cc < commits_per_iter; ++cc)
+                        asm volatile(
+                            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                                smem_u32(&bar2[cc])),
+                            "h"((uint16_t)3)
+                            : "memory");
                 for (int i = 0; i < nmma; ++i) {
                     const uint32_t acc = i > 0 ? 1u : 0u;
                     if (SS)
@@ -111,28 +120,29 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int smem = 140 * 1024;
-    struct Case { int bn; bool ss; int nmma; };
-    const Case cases[] = {{64, false, 24}, {128, false, 24}, {256, false, 24}, {64, true, 24}, {128, true, 24}, {32, false, 24}};
+    struct Case { int bn; bool ss; int nmma; int commits; };
+    const Case cases[] = {{64, false, 24, 0}, {128, false, 24, 0}, {64, false, 24, 2}, {128, false, 24, 2},
+                          {64, false, 12, 2}, {128, false, 12, 2}, {128, false, 12, 0}};
     int ci = -1;
     for (const Case& c : cases) {
         if (++ci, only >= 0 && ci != only) continue;
-        void (*k)(int, int) = nullptr;
+        void (*k)(int, int, int) = nullptr;
         if (c.bn == 32) k = c.ss ? pair_kernel<32, true> : pair_kernel<32, false>;
         if (c.bn == 64) k = c.ss ? pair_kernel<64, true> : pair_kernel<64, false>;
         if (c.bn == 128) k = c.ss ? pair_kernel<128, true> : pair_kernel<128, false>;
         if (c.bn == 256) k = c.ss ? pair_kernel<256, true> : pair_kernel<256, false>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        k<<<148, 128, smem>>>(iters, c.nmma);
+        k<<<148, 128, smem>>>(iters, c.nmma, c.commits);
         cudaEventRecord(e0);
-        for (int rep = 0; rep < 5; ++rep) k<<<148, 128, smem>>>(iters, c.nmma);
+        for (int rep = 0; rep < 5; ++rep) k<<<148, 128, smem>>>(iters, c.nmma, c.commits);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
         cudaError_t err = cudaGetLastError();
         const double flop = 2.0 * 256 * c.bn * 8 * c.nmma * (double)iters * 74;
-        printf("cta_group::2 %s M=256 N=%d x%d: %.1f ns per k-block (per pair), %.0f TFLOP/s tf32  %s\n",
-               c.ss ? "ss" : "ts", c.bn, c.nmma, ms / 5 * 1e6 / iters, flop / (ms / 5 * 1e-3) / 1e12,
+        printf("cta_group::2 %s M=256 N=%d x%d commits/iter %d: %.1f ns per k-block (per pair), %.0f TFLOP/s tf32  %s\n",
+               c.ss ? "ss" : "ts", c.bn, c.nmma, c.commits, ms / 5 * 1e6 / iters, flop / (ms / 5 * 1e-3) / 1e12,
                cudaGetErrorString(err));
     }
     return 0;
