@@ -46,19 +46,21 @@ struct StripCfg {
     static constexpr int B_OFF = A_TMEM ? A_BYTES : PLANES * A_BYTES;
     static constexpr int STAGE_BYTES = A_TMEM ? A_BYTES + 2 * B_BYTES : PLANES * (A_BYTES + B_BYTES);
     static constexpr int A_SLOT_COLS = R * FW * 64;  // TMEM columns per stage: (j, fw) windows x (hi 32 + lo 32)
-    static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-    static constexpr int STAGES_TM = A_TMEM ? (512 - 2 * R * BN) / A_SLOT_COLS : 6;
-    static constexpr int STAGES_C = STAGES_RAW < STAGES_TM ? STAGES_RAW : STAGES_TM;
-    static constexpr int STAGES = STAGES_C > 6 ? 6 : STAGES_C;
+    // smem stages (TMA ring) and TMEM A-window slots (converter -> MMA ring) are separate rings, as
+    // in conv_tma.cuh: at BN = 64 in 3xTF32 TMEM holds only 2 slots but 3 smem stages fit in 216 KB
+    static constexpr int STAGES_RAW = (214 * 1024) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
+    static constexpr int NT_RAW = A_TMEM ? (512 - 2 * R * BN) / A_SLOT_COLS : 1;
+    static constexpr int NT = NT_RAW > 6 ? 6 : NT_RAW;
     static constexpr int NEPI = 8, TMA_W = 8, MMA_W = 9, CONV_W0 = 10;
     static constexpr int NCONV = PLANES == 2 ? 8 : 0;
     static constexpr int NTHREADS = (10 + NCONV) * 32;
     static constexpr bool B_MN = (OP == OP_DX);
     static constexpr int A_TCOL0 = 2 * R * BN;
-    static constexpr int ACC_COLS = 2 * R * BN + (A_TMEM ? STAGES * A_SLOT_COLS : 0);
+    static constexpr int ACC_COLS = 2 * R * BN + (A_TMEM ? NT * A_SLOT_COLS : 0);
     static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128 : ACC_COLS <= 256 ? 256 : 512;
     static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 1024;
-    static_assert(STAGES >= 2, "strip stage does not fit");
+    static_assert(STAGES >= 2 && NT >= 1, "strip stage does not fit");
     static_assert(ACC_COLS <= 512, "TMEM");
     static_assert(PLANES == 1 || R * BN <= 128, "3xTF32 promotion keeps R*BN/2 fp32 per epilogue thread");
 };
@@ -101,9 +103,12 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
     const int CHK = PLANES == 2 ? sp.chunk_kb : (1 << 30);
 
     if (tid == 0) {
+        for (int t = 0; t < C::NT; ++t) {
+            mbar_init(&aux->conv[t], C::NCONV * 32);
+            mbar_init(&aux->tfree[t], 1);
+        }
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&aux->full[s], 1);
-            mbar_init(&aux->conv[s], C::NCONV * 32);
             mbar_init(&aux->empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -160,18 +165,20 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
         constexpr uint64_t A_LO = C::A_BYTES >> 4, B_LO = C::B_BYTES >> 4;
         constexpr uint64_t B_G = C::B_MN ? 64 : 2, B_TAP = (BN * 128) >> 4;
         int s = 0, in_chunk = 0;
-        uint32_t r = 0, c = 0;
+        uint32_t r = 0, c = 0, q = 0;
         for (int w = blockIdx.x; w < sp.work; w += gridDim.x) {
             StripTile t;
             t.init(sp, w);
             const int nkb = strip_rows<OP>(sp, p, t.orow) * sp.CB;
-            for (int it = 0; it < nkb; ++it) {
+            for (int it = 0; it < nkb; ++it, ++q) {
                 const int buf = c & 1;
+                const uint32_t ts = q % C::NT, rts = q / C::NT;  // TMEM A-window slot
                 if (in_chunk == 0 && c >= 2) {
                     mbar_wait(&aux->tempty[buf], ((c >> 1) - 1) & 1);
                     tc_fence_after();
                 }
-                mbar_wait(PLANES == 2 ? &aux->conv[s] : &aux->full[s], r & 1);
+                if (PLANES == 2) mbar_wait(&aux->conv[ts], rts & 1);
+                else mbar_wait(&aux->full[s], r & 1);
                 tc_fence_after();
                 const uint64_t so = (uint64_t)(s * C::STAGE_BYTES) >> 4;
                 const bool last = (in_chunk + 1 == CHK || it == nkb - 1);
@@ -190,7 +197,7 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                                 const uint32_t acc0 = (in_chunk > 0 || fw > 0 || g > 0) ? 1u : 0u;
                                 if (C::A_TMEM) {
                                     const uint32_t ahi =
-                                        tmem + (uint32_t)(C::A_TCOL0 + s * C::A_SLOT_COLS + (j * C::FW + fw) * 64 + g * 8);
+                                        tmem + (uint32_t)(C::A_TCOL0 + ts * C::A_SLOT_COLS + (j * C::FW + fw) * 64 + g * 8);
                                     mma_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);
                                     mma_tf32_ts(d, ahi, bdH + B_LO, IDESC, 1u);
                                     mma_tf32_ts(d, ahi, bdH, IDESC, 1u);
@@ -205,6 +212,7 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                         }
                     }
                     mma_commit(&aux->empty[s]);
+                    if (C::A_TMEM) mma_commit(&aux->tfree[ts]);
                     if (last) mma_commit(&aux->tfull[buf]);
                 }
                 __syncwarp();
@@ -225,13 +233,18 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
         const int ct = tid - C::CONV_W0 * 32;
         constexpr int NCT = C::NCONV > 0 ? C::NCONV * 32 : 32;
         int s = 0;
-        uint32_t r = 0;
+        uint32_t r = 0, q = 0;
         for (int w = blockIdx.x; w < sp.work; w += gridDim.x) {
             StripTile t;
             t.init(sp, w);
             const int nkb = strip_rows<OP>(sp, p, t.orow) * sp.CB;
-            for (int it = 0; it < nkb; ++it) {
+            for (int it = 0; it < nkb; ++it, ++q) {
+                const uint32_t ts = q % C::NT, rts = q / C::NT;  // TMEM A-window slot
                 mbar_wait(&aux->full[s], r & 1);
+                if (C::A_TMEM && rts > 0) {  // the slot's previous windows have been multiplied
+                    mbar_wait(&aux->tfree[ts], (rts - 1) & 1);
+                    tc_fence_after();
+                }
                 uint8_t* st = tiles_ptr + s * C::STAGE_BYTES;
                 auto lo4 = [](float4 v) {
                     float4 o;
@@ -264,7 +277,7 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                                 }
                             }
                             const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) +
-                                                (uint32_t)(C::A_TCOL0 + s * C::A_SLOT_COLS + (j * C::FW + fw) * 64 + h * 16);
+                                                (uint32_t)(C::A_TCOL0 + ts * C::A_SLOT_COLS + (j * C::FW + fw) * 64 + h * 16);
                             tmem_st_32x32b_x16(ta, hi);
                             tmem_st_32x32b_x16(ta + 32, lo);
                         }
@@ -295,7 +308,7 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                 if (C::A_TMEM) tmem_st_wait();
                 fence_proxy_async_smem();
                 tc_fence_before();
-                mbar_arrive(&aux->conv[s]);
+                mbar_arrive(&aux->conv[ts]);
                 if (++s == C::STAGES) {
                     s = 0;
                     ++r;
