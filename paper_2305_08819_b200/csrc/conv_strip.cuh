@@ -61,6 +61,7 @@ struct StripCfg {
     static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128 : ACC_COLS <= 256 ? 256 : 512;
     static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 1024;
     static_assert(STAGES >= 2 && NT >= 1, "strip stage does not fit");
+    static_assert(!A_TMEM || (R == 1 && NT * FW <= 8), "3xTF32 strips: one window per filter column, per-window barriers");
     static_assert(ACC_COLS <= 512, "TMEM");
     static_assert(PLANES == 1 || R * BN <= 128, "3xTF32 promotion keeps R*BN/2 fp32 per epilogue thread");
 };
@@ -103,10 +104,10 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
     const int CHK = PLANES == 2 ? sp.chunk_kb : (1 << 30);
 
     if (tid == 0) {
-        for (int t = 0; t < C::NT; ++t) {
-            mbar_init(&aux->conv[t], C::NCONV * 32);
-            mbar_init(&aux->tfree[t], 1);
-        }
+        for (int t = 0; t < C::NT; ++t) mbar_init(&aux->tfree[t], 1);
+        // 3xTF32: one conv barrier per (slot, filter column) so the MMAs of window 0 start while
+        // windows 1 and 2 are still being split (the converters' per-stage latency bounded the strip)
+        for (int t = 0; t < (C::A_TMEM ? C::NT * C::FW : C::NT); ++t) mbar_init(&aux->conv[t], C::NCONV * 32);
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&aux->full[s], 1);
             mbar_init(&aux->empty[s], 1);
@@ -177,22 +178,30 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                     mbar_wait(&aux->tempty[buf], ((c >> 1) - 1) & 1);
                     tc_fence_after();
                 }
-                if (PLANES == 2) mbar_wait(&aux->conv[ts], rts & 1);
-                else mbar_wait(&aux->full[s], r & 1);
-                tc_fence_after();
+                if (!C::A_TMEM) {
+                    if (PLANES == 2) mbar_wait(&aux->conv[ts], rts & 1);
+                    else mbar_wait(&aux->full[s], r & 1);
+                    tc_fence_after();
+                }
                 const uint64_t so = (uint64_t)(s * C::STAGE_BYTES) >> 4;
                 const bool last = (in_chunk + 1 == CHK || it == nkb - 1);
-                if (elect_one()) {
+                {
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
                         const uint32_t d = tmem + (uint32_t)((buf * R + j) * BN);
 #pragma unroll
                         for (int fw = 0; fw < C::FW; ++fw) {
+                            if (C::A_TMEM) {
+                                mbar_wait(&aux->conv[ts * C::FW + fw], rts & 1);
+                                tc_fence_after();
+                            }
                             const int woff = OP == OP_FWD ? fw : C::FW - 1 - fw;
                             const uint64_t a0 = adH0 + so + (uint64_t)((4 * j + woff) * 4096 >> 4);
                             const uint64_t b0 = bdH0 + so + fw * B_TAP;
+                            const bool issuer = elect_one();
 #pragma unroll
                             for (int g = 0; g < 4; ++g) {
+                                if (!issuer) break;
                                 const uint64_t adH = a0 + g * 2, bdH = b0 + g * B_G;
                                 const uint32_t acc0 = (in_chunk > 0 || fw > 0 || g > 0) ? 1u : 0u;
                                 if (C::A_TMEM) {
@@ -209,11 +218,14 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                                     mma_tf32_ss(d, adH, bdH, IDESC, acc0);
                                 }
                             }
+                            __syncwarp();
                         }
                     }
-                    mma_commit(&aux->empty[s]);
-                    if (C::A_TMEM) mma_commit(&aux->tfree[ts]);
-                    if (last) mma_commit(&aux->tfull[buf]);
+                    if (elect_one()) {
+                        mma_commit(&aux->empty[s]);
+                        if (C::A_TMEM) mma_commit(&aux->tfree[ts]);
+                        if (last) mma_commit(&aux->tfull[buf]);
+                    }
                 }
                 __syncwarp();
                 if (last) {
@@ -255,32 +267,41 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                     return o;
                 };
                 if (C::A_TMEM) {
-                    // window (j, fw) row 32*qd+lane = slab 4j+woff(fw)+qd, image lane; K half h
+                    // window fw row 32*qd+lane = slab woff(fw)+qd, image lane; K half h.  Per filter
+                    // column: split the window into TMEM and that tap's B block into b_lo, then
+                    // release it to the MMA warp (conv[ts * FW + fw]) before starting the next one
                     const int qd = warp & 3, h = (warp - C::CONV_W0) >> 2;
+                    const float4* bH = reinterpret_cast<const float4*>(st + C::B_OFF);
+                    float4* bL = reinterpret_cast<float4*>(st + C::B_OFF + C::B_BYTES);
+                    constexpr int NBT = C::B_BYTES / C::FW / 16;  // float4 per tap block
 #pragma unroll
-                    for (int j = 0; j < R; ++j)
+                    for (int fw = 0; fw < C::FW; ++fw) {
+                        const int woff = OP == OP_FWD ? fw : C::FW - 1 - fw;
+                        const uint8_t* slab = st + (woff + qd) * 4096;
+                        uint32_t hi[16], lo[16];
 #pragma unroll
-                        for (int fw = 0; fw < C::FW; ++fw) {
-                            const int woff = OP == OP_FWD ? fw : C::FW - 1 - fw;
-                            const uint8_t* slab = st + (4 * j + woff + qd) * 4096;
-                            uint32_t hi[16], lo[16];
+                        for (int cq = 0; cq < 4; ++cq) {
+                            const float4 v = *reinterpret_cast<const float4*>(
+                                slab + kmaj_off((uint32_t)lane, (uint32_t)(4 * h + cq)));
+                            const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                            for (int cq = 0; cq < 4; ++cq) {
-                                const float4 v = *reinterpret_cast<const float4*>(
-                                    slab + kmaj_off((uint32_t)lane, (uint32_t)(4 * h + cq)));
-                                const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                                for (int k = 0; k < 4; ++k) {
-                                    const uint32_t hb = __float_as_uint(e[k]) & 0xFFFFE000u;
-                                    hi[4 * cq + k] = hb;
-                                    lo[4 * cq + k] = __float_as_uint(e[k] - __uint_as_float(hb));
-                                }
+                            for (int k = 0; k < 4; ++k) {
+                                const uint32_t hb = __float_as_uint(e[k]) & 0xFFFFE000u;
+                                hi[4 * cq + k] = hb;
+                                lo[4 * cq + k] = __float_as_uint(e[k] - __uint_as_float(hb));
                             }
-                            const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) +
-                                                (uint32_t)(C::A_TCOL0 + ts * C::A_SLOT_COLS + (j * C::FW + fw) * 64 + h * 16);
-                            tmem_st_32x32b_x16(ta, hi);
-                            tmem_st_32x32b_x16(ta + 32, lo);
                         }
+                        const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) +
+                                            (uint32_t)(C::A_TCOL0 + ts * C::A_SLOT_COLS + fw * 64 + h * 16);
+                        tmem_st_32x32b_x16(ta, hi);
+                        tmem_st_32x32b_x16(ta + 32, lo);
+#pragma unroll
+                        for (int i = ct; i < NBT; i += NCT) bL[fw * NBT + i] = lo4(bH[fw * NBT + i]);
+                        tmem_st_wait();
+                        fence_proxy_async_smem();
+                        tc_fence_before();
+                        mbar_arrive(&aux->conv[ts * C::FW + fw]);
+                    }
                 } else {
                     const float4* aH = reinterpret_cast<const float4*>(st);
                     float4* aL = reinterpret_cast<float4*>(st + C::A_BYTES);
@@ -292,23 +313,20 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
 #pragma unroll
                     for (int i = 0; i < NA; ++i)
                         if (ct + i * NCT < C::A_BYTES / 16) aL[ct + i * NCT] = lo4(v[i]);
-                }
-                {
                     const float4* bH = reinterpret_cast<const float4*>(st + C::B_OFF);
                     float4* bL = reinterpret_cast<float4*>(st + C::B_OFF + C::B_BYTES);
                     constexpr int NB = (C::B_BYTES / 16 + NCT - 1) / NCT;
-                    float4 v[NB];
+                    float4 vb[NB];
 #pragma unroll
                     for (int i = 0; i < NB; ++i)
-                        if (ct + i * NCT < C::B_BYTES / 16) v[i] = bH[ct + i * NCT];
+                        if (ct + i * NCT < C::B_BYTES / 16) vb[i] = bH[ct + i * NCT];
 #pragma unroll
                     for (int i = 0; i < NB; ++i)
-                        if (ct + i * NCT < C::B_BYTES / 16) bL[ct + i * NCT] = lo4(v[i]);
+                        if (ct + i * NCT < C::B_BYTES / 16) bL[ct + i * NCT] = lo4(vb[i]);
+                    fence_proxy_async_smem();
+                    tc_fence_before();
+                    mbar_arrive(&aux->conv[ts]);
                 }
-                if (C::A_TMEM) tmem_st_wait();
-                fence_proxy_async_smem();
-                tc_fence_before();
-                mbar_arrive(&aux->conv[ts]);
                 if (++s == C::STAGES) {
                     s = 0;
                     ++r;
