@@ -79,7 +79,7 @@ struct DwsCfg {
 
 struct DwsAux {
     uint64_t full[8], empty[8];
-    uint64_t conv[8], tfree[8];
+    uint64_t conv[16], tfree[8];
     uint64_t tfull, tempty;
     uint32_t tmem_base;
 };
@@ -115,7 +115,10 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
             mbar_init(&aux->empty[s], 1 + C::NCONV);  // MMA commit + next k-block's converter warps
         }
         for (int t = 0; t < C::ST; ++t) {
-            mbar_init(&aux->conv[t], C::NCONV);  // one elected arrival per converter warp
+            // one barrier per (slot, m-tile): the MMAs of m-tile 0 start while m-tile 1 is being split;
+            // one elected arrival per converter warp
+            mbar_init(&aux->conv[2 * t], C::NCONV);
+            mbar_init(&aux->conv[2 * t + 1], C::NCONV);
             mbar_init(&aux->tfree[t], 1);
         }
         mbar_init(&aux->tfull, 1);
@@ -179,14 +182,16 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
                     mbar_wait(&aux->tempty, (c - 1) & 1);  // epilogue drained the previous chunk
                     tc_fence_after();
                 }
-                mbar_wait(&aux->conv[t], rt & 1);
-                tc_fence_after();
                 const bool last = (in_chunk + 1 == CHK || i == nkb - 1);
-                if (elect_one()) {
+                {
                     const uint64_t so = (uint64_t)(s * C::STAGE_BYTES) >> 4;
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
-                        if (j < it.ntile) {
+                        // both barriers complete once per k-block (also for 1-tile items), so their
+                        // phase parity stays rt & 1
+                        mbar_wait(&aux->conv[2 * t + j], rt & 1);
+                        tc_fence_after();
+                        if (j < it.ntile && elect_one()) {
                             const uint32_t d = tmem + (uint32_t)(j * C::BN);
 #pragma unroll
                             for (int g4 = 0; g4 < 4; ++g4) {
@@ -202,10 +207,13 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
                                 }
                             }
                         }
+                        __syncwarp();
                     }
-                    mma_commit(&aux->empty[s]);
-                    mma_commit(&aux->tfree[t]);
-                    if (last) mma_commit(&aux->tfull);
+                    if (elect_one()) {
+                        mma_commit(&aux->empty[s]);
+                        mma_commit(&aux->tfree[t]);
+                        if (last) mma_commit(&aux->tfull);
+                    }
                 }
                 __syncwarp();
                 if (last) {
@@ -295,18 +303,17 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
                                             (uint32_t)(C::ACC_COLS + t * C::SLOT_COLS + j * C::TILE_COLS + h * 16);
                         tmem_st_32x32b_x16(ta, hi);
                         if (PLANES == 2) tmem_st_32x32b_x16(ta + 32, lo);
+                        tmem_st_wait();
                     }
+                    if (j == 0) fence_proxy_async_smem();  // b_lo (written above) before the first release
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&aux->conv[2 * t + j]);  // per warp; also for empty m-tiles
                 }
-                tmem_st_wait();
-                fence_proxy_async_smem();
-                tc_fence_before();
                 __syncwarp();
-                if (lane == 0) {  // per-warp arrivals: 256 per-thread mbarrier arrivals cost issue slots
-                    mbar_arrive(&aux->conv[t]);
-                    // the previous stage (its last slab row was read above) may be refilled once its own
-                    // MMAs are done too; the CTA's first k-block has no predecessor
-                    if (q > 0) mbar_arrive(&aux->empty[sp]);
-                }
+                // the previous stage (its last slab row was read above) may be refilled once its own
+                // MMAs are done too; the CTA's first k-block has no predecessor
+                if (lane == 0 && q > 0) mbar_arrive(&aux->empty[sp]);
             }
         }
     } else {
