@@ -41,6 +41,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--bucket-mb", type=float, default=16.0)
+    ap.add_argument("--graph", default="off", choices=["auto", "on", "off"],
+                    help="replay the timed steps as one CUDA graph (auto: on at 1 GPU).  Measured: no gain at "
+                         "batch 4096/512 or VGG b128 (the GPU, not the host, bounds the step), and per-call "
+                         "event nodes inside a graph are less reliable, so the default stays eager")
     ap.add_argument("--layers-out", default=os.path.join(ROOT, "gpurun_out", "bench_layers.json"))
     a = ap.parse_args()
     if a.global_batch is None:
@@ -227,11 +231,35 @@ def main():
     barrier()
     torch.cuda.synchronize()
     events = []
+    use_graph = a.graph == "on" or (a.graph == "auto" and world == 1)
+    graph = None
+    if use_graph:
+        # the K timed steps captured as ONE CUDA graph (per-call timing events are event-record
+        # nodes in it), so the host enqueues nothing per call inside the timed region
+        try:
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                step.step(None)
+            torch.cuda.current_stream(dev).wait_stream(side)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                for _ in range(a.steps):
+                    step.step(None, events=events, external_events=True)
+            torch.cuda.synchronize()
+        except Exception as exc:  # graph capture unavailable: time the eager steps instead
+            print("warning: CUDA graph capture failed (%s); timing eager steps" % exc, file=sys.stderr)
+            graph, events = None, []
+            torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(a.steps):
-        step.step(pg, events=events)
+    if graph is not None:
+        graph.replay()
+    else:
+        for _ in range(a.steps):
+            step.step(pg, events=events)
     e1.record()
     torch.cuda.synchronize()
     barrier()
@@ -295,6 +323,7 @@ def main():
            "config": {"workload": "%s-cifar10 conv stack fwd+dX+dW (conv-only chain), global batch %d"
                                   % (a.net, a.global_batch),
                       "global_batch": a.global_batch, "per_gpu_batch": B, "math": a.math,
+                      "cuda_graph": graph is not None,
                       "parallelism": "dp%d" % world, "l2": "inputs larger than L2 (per-step working set "
                       "%.1f GB >> 126 MB)" % (sum(t.numel() for b in step.bufs for t in (b.X, b.Y) if t is not None)
                                               * 4 / 1e9),
@@ -314,11 +343,20 @@ def main():
         torch.cuda.synchronize()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
+        g1 = None
+        if graph is not None:  # one step per replay here: each step's H2D / D2H sit between replays
+            g1 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g1):
+                step.step(None)
+            torch.cuda.synchronize()
         f0.record()
         for _ in range(a.steps):
             for h, t in zip(host_in, step.inputs):
                 t.copy_(h, non_blocking=True)
-            step.step(pg)
+            if g1 is not None:
+                g1.replay()
+            else:
+                step.step(pg)
             host_dw.copy_(step.dw_flat, non_blocking=True)
         f1.record()
         torch.cuda.synchronize()

@@ -199,15 +199,17 @@ class ConvNetStep:
                     ws.data_ptr() if (ws is not None and b.ws_bytes[op]) else 0,
                     b.ws_bytes[op] if ws is not None else 0, stream)
 
-    def step(self, pg=None, events: Optional[list] = None):
-        """Enqueue fwd for all layers, then dX/dW in reverse with bucketed async all-reduce."""
+    def step(self, pg=None, events: Optional[list] = None, external_events: bool = False):
+        """Enqueue fwd for all layers, then dX/dW in reverse with bucketed async all-reduce.
+        external_events: timing events that stay valid inside CUDA-graph capture."""
         torch = self.torch
         stream = torch.cuda.current_stream(self.device).cuda_stream
         rec = events is not None
 
         def mark(key):
             if rec:
-                e = torch.cuda.Event(enable_timing=True)
+                e = torch.cuda.Event(enable_timing=True, external=True) if external_events else \
+                    torch.cuda.Event(enable_timing=True)
                 e.record()
                 events.append((key, e))
 
