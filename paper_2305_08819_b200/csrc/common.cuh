@@ -133,6 +133,30 @@ SMCONV_DEV void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
         : "memory");
 }
 
+// 32 lanes x 32 bit, 8 consecutive columns <- 8 registers per thread.
+SMCONV_DEV void tmem_st_32x32b_x8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+
+// two fp32 -> packed bf16x2 (round to nearest even); `lo` lands in bits 0-15 (the lower K index)
+SMCONV_DEV uint32_t pack_bf16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16 with bf16 operands and an fp32 accumulator (K = 16)
+SMCONV_DEV void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+
 SMCONV_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // Arrive (once) on an mbarrier when all previously issued tcgen05 ops of this thread complete.
@@ -159,6 +183,12 @@ SMCONV_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" :
 // 16 B MN-major, [17,23) N>>3, [24,29) M>>4.
 SMCONV_HD constexpr uint32_t idesc_tf32(int M, int N, bool a_mn_major, bool b_mn_major) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// kind::f16 with bf16 A and B (A/B fmt 1), fp32 D; same field positions as idesc_tf32.
+SMCONV_HD constexpr uint32_t idesc_bf16(int M, int N, bool a_mn_major, bool b_mn_major) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
            ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
@@ -193,6 +223,25 @@ SMCONV_DEV uint64_t make_sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_
 SMCONV_HD uint32_t kmaj_off(uint32_t r, uint32_t c) { return (r >> 3) * 1024u + (r & 7u) * 128u + ((c ^ (r & 7u)) << 4); }
 SMCONV_HD uint32_t mnmaj_off(uint32_t k, uint32_t mn) {
     return (mn >> 5) * 4096u + k * 128u + (((((mn >> 3) & 3u) ^ (k & 3u))) << 5) + (((mn >> 2) & 1u) << 4);
+}
+
+// ------------------------------------------------------------------ 3xTF32 operand split
+// x = x_hi + x_lo with x_hi = trunc_tf32(x) (what kind::tf32 reads from an fp32 word) and x_lo exact.
+// The product a*b = a_hi*b_hi + [a_hi*b_lo + a_lo*b]: the first term runs as a TF32 MMA, the
+// bracket (~2^-10 of it) as ONE bf16 MMA pair with K doubled, A' = [bf16(a_hi) | bf16(a_lo)],
+// B' = [bf16(b_lo) | bf16(b)] (bf16 keeps 8 bits of a term already 2^-10 small: ~2^-18 relative,
+// and a bf16 flop costs half a TF32 flop of tensor-pipe time and energy).
+
+// one A row, 16 consecutive k: hi[] = a_hi bits (TF32 operand columns), xh[] / xl[] = bf16 pairs
+SMCONV_DEV void split_a16(const float (&e)[16], uint32_t (&hi)[16], uint32_t (&xh)[8], uint32_t (&xl)[8]) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) hi[k] = __float_as_uint(e[k]) & 0xFFFFE000u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const float h0 = __uint_as_float(hi[2 * i]), h1 = __uint_as_float(hi[2 * i + 1]);
+        xh[i] = pack_bf16x2(h0, h1);
+        xl[i] = pack_bf16x2(e[2 * i] - h0, e[2 * i + 1] - h1);
+    }
 }
 
 // ------------------------------------------------------------------ CTA pairs (cta_group::2)
@@ -247,6 +296,15 @@ SMCONV_DEV void mma2_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, 
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+
+SMCONV_DEV void mma2_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
         : "memory");
 }

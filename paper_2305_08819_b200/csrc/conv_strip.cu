@@ -13,6 +13,7 @@ namespace smconv {
 
 bool tma_encode_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
                     const uint32_t* box, CUtensorMapSwizzle sw);  // conv_tma.cu
+bool tma_encode_wx(CUtensorMap* m, const void* base, int Nn, int Kc, int T, int BNC);  // conv_tma.cu
 
 namespace {
 
@@ -100,6 +101,8 @@ int strip_launch(int op, int BN, int planes, const GenParams& g, cudaStream_t st
         uint32_t bb[4] = {32, 32, (uint32_t)(BN / 32), (uint32_t)kStripFW};
         ok &= tma_encode_f32(&sp.mapB, g.B, 4, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     }
+    if (planes == 2)
+        ok &= g.Bx && tma_encode_wx(&sp.mapBx, g.Bx, fwd ? g.OC : g.IC, fwd ? g.IC : g.OC, (int)T, BN);
     if (!ok) {
         snprintf(err, errlen, "strip: cuTensorMapEncodeTiled failed (op %d)", op);
         return CONV_ECUDA;

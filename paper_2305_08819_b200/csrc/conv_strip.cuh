@@ -13,7 +13,8 @@
 //
 // Row of an accumulator: position p = row / 32 of its 4-group, image = row % 32, so epilogue
 // warp quadrant q handles position 4j + q.  Zero padding / ragged strips = TMA OOB zero fill.
-// Roles, 3xTF32 handling and TMEM double buffering are those of conv_tma.cuh.
+// Roles, 3xTF32 handling (TF32 a_hi*b_hi + bf16 cross terms on the precomputed W' plane) and
+// TMEM double buffering are those of conv_tma.cuh.
 #pragma once
 #include "conv_tma.cuh"
 
@@ -24,6 +25,7 @@ constexpr int kStripFW = 3;
 struct __align__(64) StripParams {
     CUtensorMap mapA;  // activations viewed (32 ch, N, W, H, C/32)
     CUtensorMap mapB;  // fwd: W viewed (IC, OC, T); dX: W viewed (32 ic, OC, IC/32, T)
+    CUtensorMap mapBx;  // 3xTF32: the precomputed bf16 W' plane (wx_prep_kernel), box (64, 1, BN, 1)
     int CB;            // 32-channel blocks of the reduction (fwd: IC/32, dX: OC/32)
     int NG;            // 32-image groups
     int OHo, OWo;      // output extent (fwd: OH x OW, dX: IH x IW)
@@ -121,6 +123,7 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
     if (warp == C::TMA_W && lane == 0) {
         prefetch_tmap(&sp.mapA);
         prefetch_tmap(&sp.mapB);
+        if (C::A_TMEM) prefetch_tmap(&sp.mapBx);
     }
     if (warp == C::MMA_W) tmem_alloc(&aux->tmem_base, C::TMEM_COLS);
     tc_fence_before();
@@ -144,10 +147,15 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                     const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
                     const uint32_t sB = sA + C::B_OFF;
                     if (elect_one()) {
-                        mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + C::B_BYTES);
+                        mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + (C::A_TMEM ? 2 : 1) * C::B_BYTES);
                         tma_load_5d(sA, &sp.mapA, &aux->full[s], 0, t.g * 32, col0, srow, cb);
                         if (OP == OP_FWD) tma_load_3d(sB, &sp.mapB, &aux->full[s], cb * 32, t.nt * BN, fh * C::FW);
                         else tma_load_4d(sB, &sp.mapB, &aux->full[s], 0, cb * 32, t.nt * BN / 32, fh * C::FW);
+                        if (C::A_TMEM)  // W' planes of the FW taps: [fw][BN rows][128 B]
+#pragma unroll
+                            for (int fw = 0; fw < C::FW; ++fw)
+                                tma_load_4d(sB + C::B_BYTES + fw * BN * 128, &sp.mapBx, &aux->full[s], 0, cb, t.nt * BN,
+                                            fh * C::FW + fw);
                     }
                     __syncwarp();
                     if (++s == C::STAGES) {
@@ -163,7 +171,9 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
         const uint64_t adH0 = make_sdesc(tiles_addr, 16u, 1024u, kLayoutSW128);
         const uint64_t bdH0 = make_sdesc(tiles_addr + C::B_OFF, C::B_MN ? 4096u : 16u,
                                          C::B_MN ? 512u : 1024u, C::B_MN ? kLayoutSW128Base32 : kLayoutSW128);
-        constexpr uint64_t A_LO = C::A_BYTES >> 4, B_LO = C::B_BYTES >> 4;
+        // 3xTF32 cross terms: bf16 B' planes [b_lo | b] (K-major, 128 B per row) after the b_hi taps
+        constexpr uint32_t IDESC_X = idesc_bf16(128, BN, false, false);
+        const uint64_t bx0 = make_sdesc(tiles_addr + C::B_OFF + C::B_BYTES, 16u, 1024u, kLayoutSW128);
         constexpr uint64_t B_G = C::B_MN ? 64 : 2, B_TAP = (BN * 128) >> 4;
         int s = 0, in_chunk = 0;
         uint32_t r = 0, c = 0, q = 0;
@@ -207,16 +217,16 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                                 if (C::A_TMEM) {
                                     const uint32_t ahi =
                                         tmem + (uint32_t)(C::A_TCOL0 + ts * C::A_SLOT_COLS + (j * C::FW + fw) * 64 + g * 8);
-                                    mma_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);
-                                    mma_tf32_ts(d, ahi, bdH + B_LO, IDESC, 1u);
-                                    mma_tf32_ts(d, ahi, bdH, IDESC, 1u);
-                                } else if (PLANES == 2) {
-                                    mma_tf32_ss(d, adH + A_LO, bdH, IDESC, acc0);
-                                    mma_tf32_ss(d, adH, bdH + B_LO, IDESC, 1u);
-                                    mma_tf32_ss(d, adH, bdH, IDESC, 1u);
+                                    mma_tf32_ts(d, ahi, bdH, IDESC, acc0);  // a_hi * b_hi
                                 } else {
                                     mma_tf32_ss(d, adH, bdH, IDESC, acc0);
                                 }
+                            }
+                            if (C::A_TMEM && issuer) {  // cross terms, bf16, K = 64 in 4 MMAs
+                                const uint32_t ax = tmem + (uint32_t)(C::A_TCOL0 + ts * C::A_SLOT_COLS + (j * C::FW + fw) * 64 + 32);
+#pragma unroll
+                                for (int jj = 0; jj < 4; ++jj)
+                                    mma_bf16_ts(d, ax + jj * 8, bx0 + so + fw * B_TAP + jj * 2, IDESC_X, 1u);
                             }
                             __syncwarp();
                         }
@@ -271,32 +281,25 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                     // column: split the window into TMEM and that tap's B block into b_lo, then
                     // release it to the MMA warp (conv[ts * FW + fw]) before starting the next one
                     const int qd = warp & 3, h = (warp - C::CONV_W0) >> 2;
-                    const float4* bH = reinterpret_cast<const float4*>(st + C::B_OFF);
-                    float4* bL = reinterpret_cast<float4*>(st + C::B_OFF + C::B_BYTES);
-                    constexpr int NBT = C::B_BYTES / C::FW / 16;  // float4 per tap block
 #pragma unroll
                     for (int fw = 0; fw < C::FW; ++fw) {
                         const int woff = OP == OP_FWD ? fw : C::FW - 1 - fw;
                         const uint8_t* slab = st + (woff + qd) * 4096;
-                        uint32_t hi[16], lo[16];
+                        float e[16];
 #pragma unroll
                         for (int cq = 0; cq < 4; ++cq) {
                             const float4 v = *reinterpret_cast<const float4*>(
                                 slab + kmaj_off((uint32_t)lane, (uint32_t)(4 * h + cq)));
-                            const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                const uint32_t hb = __float_as_uint(e[k]) & 0xFFFFE000u;
-                                hi[4 * cq + k] = hb;
-                                lo[4 * cq + k] = __float_as_uint(e[k] - __uint_as_float(hb));
-                            }
+                            e[4 * cq] = v.x, e[4 * cq + 1] = v.y, e[4 * cq + 2] = v.z, e[4 * cq + 3] = v.w;
                         }
+                        // window columns: [0,32) a_hi, [32,48) bf16(a_hi) pairs, [48,64) bf16(a_lo) pairs
+                        uint32_t hi[16], xh[8], xl[8];
+                        split_a16(e, hi, xh, xl);
                         const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) +
-                                            (uint32_t)(C::A_TCOL0 + ts * C::A_SLOT_COLS + fw * 64 + h * 16);
-                        tmem_st_32x32b_x16(ta, hi);
-                        tmem_st_32x32b_x16(ta + 32, lo);
-#pragma unroll
-                        for (int i = ct; i < NBT; i += NCT) bL[fw * NBT + i] = lo4(bH[fw * NBT + i]);
+                                            (uint32_t)(C::A_TCOL0 + ts * C::A_SLOT_COLS + fw * 64);
+                        tmem_st_32x32b_x16(ta + h * 16, hi);
+                        tmem_st_32x32b_x8(ta + 32 + h * 8, xh);
+                        tmem_st_32x32b_x8(ta + 48 + h * 8, xl);
                         tmem_st_wait();
                         fence_proxy_async_smem();
                         tc_fence_before();

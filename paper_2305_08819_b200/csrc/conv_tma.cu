@@ -44,7 +44,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 
 // Encode an fp32 tiled map. dims/strides/box in TMA order (dim 0 innermost, stride[0] = 4 implied).
 bool encode(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-            const uint32_t* box, CUtensorMapSwizzle sw) {
+            const uint32_t* box, CUtensorMapSwizzle sw, CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
     auto fn = encoder();
     if (!fn) return false;
     cuuint64_t gd[5], gs[4];
@@ -55,7 +55,7 @@ bool encode(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, co
         es[i] = 1;
     }
     for (int i = 0; i < rank - 1; ++i) gs[i] = strides_bytes[i];
-    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), gd, gs, bd, es,
+    CUresult r = fn(m, dt, rank, const_cast<void*>(base), gd, gs, bd, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, (CUtensorMapL2promotion)g_knob_promo,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -131,6 +131,15 @@ int tma_set_pair(int on) { return g_pair.exchange(on); }
 bool tma_encode_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
                     const uint32_t* box, CUtensorMapSwizzle sw) {
     return encode(m, base, rank, dims, strides, box, sw);
+}
+
+// the bf16 W' plane (wx_prep_kernel): rows (tap, n, cb) of 64 bf16, box (64, 1, BNC, 1) -> BNC
+// K-major 128-B rows in shared memory, 128B swizzle (the UMMA SWIZZLE_128B K-major layout)
+bool tma_encode_wx(CUtensorMap* m, const void* base, int Nn, int Kc, int T, int BNC) {
+    const uint64_t CB = Kc / 32;
+    uint64_t d[4] = {64, CB, (uint64_t)Nn, (uint64_t)T}, s[3] = {128, CB * 128, (uint64_t)Nn * CB * 128};
+    uint32_t b[4] = {64, 1, (uint32_t)BNC, 1};
+    return encode(m, base, 4, d, s, b, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
 }
 
 bool tma_supported(int op, int N, int IC, int OC, int FH, int FW, int sh, int sw) {
@@ -219,6 +228,7 @@ int tma_launch(int op, int BN, int planes, const GenParams& g, TmaParams& tp, di
         uint64_t db[3] = {IC, T, OC}, sb[2] = {IC * 4, T * IC * 4};
         uint32_t bb[3] = {32, 1, (uint32_t)(tp.pair ? BN / 2 : BN)};  // a pair splits B by columns
         ok &= encode(&tp.mapB, g.B, 3, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B);
+        if (planes == 2) ok &= g.Bx && tma_encode_wx(&tp.mapBx, g.Bx, (int)OC, (int)IC, (int)T, tp.pair ? BN / 2 : BN);
     } else if (op == CONV_OP_BWD_DATA) {
         // A = dY (OC, OW, OH, N); B = W viewed (32 ic, OC, IC/32, T), MN-major
         uint64_t da[4] = {OC, OW, OH, N}, sa[3] = {OC * 4, OW * OC * 4, OH * OW * OC * 4};
@@ -227,6 +237,7 @@ int tma_launch(int op, int BN, int planes, const GenParams& g, TmaParams& tp, di
         uint64_t db[4] = {32, OC, IC / 32, T}, sb[3] = {T * IC * 4, 128, IC * 4};
         uint32_t bb[4] = {32, 32, (uint32_t)((tp.pair ? BN / 2 : BN) / 32), 1};
         ok &= encode(&tp.mapB, g.B, 4, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+        if (planes == 2) ok &= g.Bx && tma_encode_wx(&tp.mapBx, g.Bx, (int)IC, (int)OC, (int)T, tp.pair ? BN / 2 : BN);
     } else if (g.dwt) {
         // transposed dW: A = X viewed (32 ic, N, IC/32, IW, IH), B = dY viewed (32 oc, N, OC/32, OH*OW)
         uint64_t da[5] = {32, N, IC / 32, IW, IH}, sa[4] = {IH * IW * IC * 4, 128, IC * 4, IW * IC * 4};

@@ -24,8 +24,12 @@
 // warp 9 TMEM owner + MMA issuer (1 lane), warps 10-13 (3xTF32 only) split converters.
 //
 // 3xTF32 exploits what the probe measured: tcgen05 kind::tf32 reads an fp32
-// operand by TRUNCATION to TF32, so the raw TMA tile IS a_hi = trunc_tf32(a); converters only
-// write a_lo = a - trunc_tf32(a) (exact in fp32).  Per k-step: a_lo*b_hi + a_hi*b_lo + a_hi*b_hi.
+// operand by TRUNCATION to TF32, so the raw TMA tile IS b_hi = trunc_tf32(b).  fwd / dX: per
+// k-block a_hi*b_hi as 4 TF32 MMAs, and the cross terms a_hi*b_lo + a_lo*b as 4 bf16 MMAs (K = 64)
+// on A' = [bf16(a_hi) | bf16(a_lo)] (written to TMEM by the converters) and the precomputed W'
+// plane B' = [bf16(b_lo) | bf16(b)] (wx_prep_kernel, TMA-loaded): 2 TF32-MMA-equivalents of
+// tensor-pipe time and energy instead of 3 (the step runs at the power cap).  dW (B = an
+// activation tile): a_lo*b_hi + a_hi*b_lo + a_hi*b_hi, b_lo split by the converters.
 // The accumulator adds by truncation too, so K is cut into chunks of chunk_kb k-blocks that
 // alternate between the two TMEM buffers and are promoted into fp32 registers (round to
 // nearest) by the epilogue warps while the next chunk runs (SURVEY.md §7 hard part 1).
@@ -40,6 +44,7 @@ namespace smconv {
 struct __align__(64) TmaParams {
     CUtensorMap mapA;
     CUtensorMap mapB;
+    CUtensorMap mapBx;  // 3xTF32 fwd / dX: the precomputed bf16 W' plane (wx_prep_kernel), box (64, 1, BNC, 1)
     int G;           // images per A box (fwd/dx): 128 when N % 128 == 0, else 32
     int CB;          // fwd/dx: channel blocks of 32 per tap (IC/32 resp. OC/32)
     int NB32;        // dw: N / 32 (image blocks per position)
@@ -79,6 +84,11 @@ struct TmaCfg {
     static constexpr int NT_RAW = A_TMEM ? (512 - 2 * BN) / 64 : 1;  // TMEM A slots (64 cols each)
     static constexpr int NT = NT_RAW > 8 ? 8 : NT_RAW;
     static constexpr bool IS_DW = (OP == OP_DW || OP == OP_DWT);
+    // fwd / dX in 3xTF32: a_hi*b_hi as a TF32 MMA plus the cross terms as bf16 MMAs on the
+    // precomputed W' plane (common.cuh "3xTF32 operand split"); dW keeps three TF32 MMAs with a
+    // b_lo plane split by the converters (its B is an activation tile; the bf16 split of an
+    // MN-major activation tile cost more converter time than the tensor pipe saved, r01l)
+    static constexpr bool HYB = A_TMEM && !IS_DW;
     static constexpr bool A_MN = IS_DW;
     static constexpr bool B_MN = (OP != OP_FWD);
     static constexpr int A_TCOL0 = 2 * BN;  // TMEM column of A slot 0 (A_TMEM)
@@ -154,6 +164,8 @@ struct TileInfo {
         }
         phase = 0;
         if (OP == OP_DX) {
+            // phase-major walk.  (An image-block-major walk across the phases cut the l2.0a dX DRAM
+            // reads 2.35 -> 0.93 GB but ran 1.44 -> 1.81 ms: measured r01g, reverted.)
             while (phase + 1 < p.nphase && mt >= p.phase_tile0[phase + 1]) ++phase;
             mt -= p.phase_tile0[phase];
         }
@@ -293,6 +305,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
     if (warp == C::TMA_W && lane == 0) {
         prefetch_tmap(&tp.mapA);
         prefetch_tmap(&tp.mapB);
+        if (C::HYB) prefetch_tmap(&tp.mapBx);
     }
     if (warp == C::MMA_W) {
         if (PAIR) tmem_alloc2(&aux->tmem_base, C::TMEM_COLS);
@@ -336,7 +349,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                         const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
                         const uint32_t sB = sA + C::B_OFF;
                         if (elect_one()) {
-                            mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + C::B_BYTES);
+                            mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + (C::HYB ? 2 : 1) * C::B_BYTES);
 #pragma unroll
                             for (int g = 0; g < 4; ++g)
                                 if (g < ti.ngrp) tma_load_4d(sA + g * tp.G * 128, &tp.mapA, &aux->full[s], cb * 32,
@@ -344,6 +357,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                             const int nb0 = n0 + rank * C::BNC;  // this CTA's half of B (pairs)
                             if (OP == OP_FWD) tma_load_3d(sB, &tp.mapB, &aux->full[s], cb * 32, tap.z, nb0);
                             else tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, cb * 32, nb0 / 32, tap.z);
+                            if (C::HYB) tma_load_4d(sB + C::B_BYTES, &tp.mapBx, &aux->full[s], 0, cb, nb0, tap.z);
                         }
                         __syncwarp();
                         if (++cb == tp.CB) {
@@ -437,8 +451,10 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             // descriptors of stage 0; stage s / k-step g only add to the 14-bit start-address field
             const uint64_t adH0 = make_sdesc(tiles_addr, albo, asbo, alay);
             const uint64_t bdH0 = make_sdesc(tiles_addr + C::B_OFF, blbo, bsbo, blay);
-            constexpr uint64_t A_LO = C::A_BYTES >> 4, B_LO = C::B_BYTES >> 4;
             constexpr uint64_t A_G = C::A_MN ? 64 : 2, B_G = C::B_MN ? 64 : 2;  // (1024 or 32 bytes) >> 4
+            // 3xTF32 cross terms: bf16 B' plane [b_lo | b] (K-major, 128 B per row) after b_hi
+            constexpr uint32_t IDESC_X = idesc_bf16(PAIR ? 256 : 128, BN, false, false);
+            const uint64_t bx0 = make_sdesc(tiles_addr + C::B_OFF + C::B_BYTES, 16u, 1024u, kLayoutSW128);
             int s = 0, in_chunk = 0;
             uint32_t r = 0, c = 0, q = 0;  // stage, ring round, chunk counter, k-block (global across tiles)
             for (int w = wfirst; w < tp.work; w += wstep) {
@@ -465,22 +481,27 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                         for (int g = 0; g < C::BK / 8; ++g) {
                             const uint64_t adH = adH0 + so + g * A_G, bdH = bdH0 + so + g * B_G;
                             const uint32_t acc0 = (in_chunk > 0 || g > 0) ? 1u : 0u;
+                            const uint32_t ahi = tmem + (uint32_t)(C::A_TCOL0 + t * 64 + g * 8);
                             if (PAIR) {
-                                const uint32_t ahi = tmem + (uint32_t)(C::A_TCOL0 + t * 64 + g * 8);
-                                mma2_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);
-                                mma2_tf32_ts(d, ahi, bdH + B_LO, IDESC, 1u);
-                                mma2_tf32_ts(d, ahi, bdH, IDESC, 1u);
-                            } else if (C::A_TMEM) {
-                                const uint32_t ahi = tmem + (uint32_t)(C::A_TCOL0 + t * 64 + g * 8);
+                                mma2_tf32_ts(d, ahi, bdH, IDESC, acc0);  // a_hi * b_hi (TF32)
+                            } else if (C::HYB) {
+                                mma_tf32_ts(d, ahi, bdH, IDESC, acc0);
+                            } else if (C::A_TMEM) {  // dW: three TF32 MMAs, b_lo plane after b_hi
                                 mma_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);
-                                mma_tf32_ts(d, ahi, bdH + B_LO, IDESC, 1u);
+                                mma_tf32_ts(d, ahi, bdH + (C::B_BYTES >> 4), IDESC, 1u);
                                 mma_tf32_ts(d, ahi, bdH, IDESC, 1u);
-                            } else if (PLANES == 2) {
-                                mma_tf32_ss(d, adH + A_LO, bdH, IDESC, acc0);
-                                mma_tf32_ss(d, adH, bdH + B_LO, IDESC, 1u);
-                                mma_tf32_ss(d, adH, bdH, IDESC, 1u);
                             } else {
                                 mma_tf32_ss(d, adH, bdH, IDESC, acc0);
+                            }
+                        }
+                        if (C::HYB) {
+                            // cross terms a_hi*b_lo + a_lo*b in bf16: A' = [bf16(a_hi) | bf16(a_lo)]
+                            // (TMEM, 32 columns), B' = [bf16(b_lo) | bf16(b)]: K = 64 in 4 MMAs
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const uint32_t ax = tmem + (uint32_t)(C::A_TCOL0 + t * 64 + 32 + j * 8);
+                                if (PAIR) mma2_bf16_ts(d, ax, bx0 + so + j * 2, IDESC_X, 1u);
+                                else mma_bf16_ts(d, ax, bx0 + so + j * 2, IDESC_X, 1u);
                             }
                         }
                         if (PAIR) {
@@ -529,8 +550,6 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     tc_fence_after();
                 }
                 uint8_t* st = tiles_ptr + s * C::STAGE_BYTES;
-                const float4* bH = reinterpret_cast<const float4*>(st + C::B_OFF);
-                float4* bL = reinterpret_cast<float4*>(st + C::B_OFF + C::B_BYTES);
                 constexpr int NB = C::B_BYTES / 16 / NCT;
                 static_assert(NB * NCT * 16 == C::B_BYTES, "converter split");
                 auto lo4 = [](float4 v) {
@@ -541,9 +560,6 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
                     return o;
                 };
-                float4 vb[NB];
-#pragma unroll
-                for (int i = 0; i < NB; ++i) vb[i] = bH[ct + i * NCT];
                 if (C::A_TMEM) {
                     // this thread: A row 32*(warp%4)+lane, K half h: hi/lo -> TMEM slot s (tcgen05.st)
                     const int qd = warp & 3, h = (warp - C::CONV_W0) >> 2;
@@ -565,16 +581,27 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                             e[4 * c + 3] = v.w;
                         }
                     }
-                    uint32_t hi[16], lo[16];
+                    // slot columns: [0,32) a_hi (TF32 operand), [32,48) bf16(a_hi) for k = 0..31 in
+                    // pairs, [48,64) bf16(a_lo) likewise; this thread has k in [16h, 16h+16)
+                    // (dW: [32,64) a_lo fp32 for the third TF32 MMA)
+                    const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(C::A_TCOL0 + t * 64);
+                    if (C::HYB) {
+                        uint32_t hi[16], xh[8], xl[8];
+                        split_a16(e, hi, xh, xl);
+                        tmem_st_32x32b_x16(ta + h * 16, hi);
+                        tmem_st_32x32b_x8(ta + 32 + h * 8, xh);
+                        tmem_st_32x32b_x8(ta + 48 + h * 8, xl);
+                    } else {
+                        uint32_t hi[16], lo[16];
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const uint32_t hb = __float_as_uint(e[k]) & 0xFFFFE000u;
-                        hi[k] = hb;
-                        lo[k] = __float_as_uint(e[k] - __uint_as_float(hb));
+                        for (int k = 0; k < 16; ++k) {
+                            const uint32_t hb = __float_as_uint(e[k]) & 0xFFFFE000u;
+                            hi[k] = hb;
+                            lo[k] = __float_as_uint(e[k] - __uint_as_float(hb));
+                        }
+                        tmem_st_32x32b_x16(ta + h * 16, hi);
+                        tmem_st_32x32b_x16(ta + 32 + h * 16, lo);
                     }
-                    const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(C::A_TCOL0 + t * 64 + h * 16);
-                    tmem_st_32x32b_x16(ta, hi);
-                    tmem_st_32x32b_x16(ta + 32, lo);
                 } else {
                     const float4* aH = reinterpret_cast<const float4*>(st);
                     float4* aL = reinterpret_cast<float4*>(st + C::A_BYTES);
@@ -586,8 +613,15 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
 #pragma unroll
                     for (int i = 0; i < NA; ++i) aL[ct + i * NCT] = lo4(va[i]);
                 }
+                if (!C::HYB) {  // b_lo plane (dW, and the TF32-free SS fallback)
+                    const float4* bH = reinterpret_cast<const float4*>(st + C::B_OFF);
+                    float4* bL = reinterpret_cast<float4*>(st + C::B_OFF + C::B_BYTES);
+                    float4 vb[NB];
 #pragma unroll
-                for (int i = 0; i < NB; ++i) bL[ct + i * NCT] = lo4(vb[i]);
+                    for (int i = 0; i < NB; ++i) vb[i] = bH[ct + i * NCT];
+#pragma unroll
+                    for (int i = 0; i < NB; ++i) bL[ct + i * NCT] = lo4(vb[i]);
+                }
                 if (C::A_TMEM) tmem_st_wait();
                 fence_proxy_async_smem();
                 tc_fence_before();

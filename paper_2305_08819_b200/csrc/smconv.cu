@@ -114,6 +114,7 @@ struct Plan {
     uint32_t zero_mask;  // dX stride phases with no tap (zero_phases_kernel)
     dim3 grid;
     size_t ws_bytes;
+    size_t wx_off, wx_bytes;  // 3xTF32 fwd / dX (TMA, STRIP): bf16 W' plane in the workspace
     long long out_elems;
     GenParams gp;
     TmaParams tp;
@@ -308,6 +309,14 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
     pl.out_elems = out_elems;
     pl.ws_bytes = splits > 1 ? (size_t)splits * out_elems * sizeof(float) : 0;
     g.split_stride = splits > 1 ? out_elems : 0;
+    pl.wx_off = pl.wx_bytes = 0;
+    if (pl.planes == 2 && op != CONV_OP_BWD_FILTER &&
+        (pl.variant == CONV_VARIANT_TMA || pl.variant == CONV_VARIANT_STRIP)) {
+        // W' = [bf16(w_lo) | bf16(w)] per (tap, GEMM column, 32-k block): 4 bytes per weight
+        pl.wx_off = (pl.ws_bytes + 1023) & ~(size_t)1023;
+        pl.wx_bytes = (size_t)d.FH * d.FW * d.IC * d.OC * 4;
+        pl.ws_bytes = pl.wx_off + pl.wx_bytes;
+    }
     pl.grid = dim3(m_tiles, n_tiles, splits);
     if (pl.variant == CONV_VARIANT_TMA) {
         int rc = tma_make_plan(op, g, pl.BN, pl.planes, pl.tp, pl.grid, g_detail, sizeof g_detail);
@@ -350,6 +359,50 @@ int launch_gen_op(const Plan& pl, const GenParams& g, cudaStream_t st) {
     return pl.planes == 2 ? launch_gen_bn<OP, 2>(pl.BN, g, pl.grid, st) : launch_gen_bn<OP, 1>(pl.BN, g, pl.grid, st);
 }
 
+// W' for the 3xTF32 cross terms (common.cuh "3xTF32 operand split"): row (tap, n, cb) of 64 bf16 =
+// [bf16(w_lo) for k = 32cb..32cb+31 | bf16(w) for the same k], w_lo = w - trunc_tf32(w); the GEMM
+// column n / reduction index k are (oc, ic) for fwd and (ic, oc) for dX.  One thread per row.
+__global__ void __launch_bounds__(256) wx_prep_kernel(const float* __restrict__ W, uint4* __restrict__ Wx, int OC,
+                                                      int IC, int T, int dx) {
+    const int Nn = dx ? IC : OC, Kc = dx ? OC : IC, CB = Kc / 32;
+    const long long rows = (long long)T * Nn * CB;
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows; r += (long long)gridDim.x * blockDim.x) {
+        int tap, n, cb;
+        if (dx) {  // n fastest across threads: the strided W reads coalesce
+            n = (int)(r % Nn);
+            const long long q = r / Nn;
+            cb = (int)(q % CB);
+            tap = (int)(q / CB);
+        } else {  // cb fastest: each thread reads 128 contiguous bytes
+            cb = (int)(r % CB);
+            const long long q = r / CB;
+            n = (int)(q % Nn);
+            tap = (int)(q / Nn);
+        }
+        uint32_t lo[16], hi[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            float w0, w1;
+            if (dx) {
+                w0 = W[((size_t)(32 * cb + 2 * i) * T + tap) * IC + n];
+                w1 = W[((size_t)(32 * cb + 2 * i + 1) * T + tap) * IC + n];
+            } else {
+                const float2 v = *reinterpret_cast<const float2*>(W + ((size_t)n * T + tap) * IC + 32 * cb + 2 * i);
+                w0 = v.x;
+                w1 = v.y;
+            }
+            lo[i] = pack_bf16x2(w0 - __uint_as_float(__float_as_uint(w0) & 0xFFFFE000u),
+                                w1 - __uint_as_float(__float_as_uint(w1) & 0xFFFFE000u));
+            hi[i] = pack_bf16x2(w0, w1);
+        }
+        uint4* o = Wx + (((size_t)tap * Nn + n) * CB + cb) * 8;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] = make_uint4(lo[4 * i], lo[4 * i + 1], lo[4 * i + 2], lo[4 * i + 3]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[4 + i] = make_uint4(hi[4 * i], hi[4 * i + 1], hi[4 * i + 2], hi[4 * i + 3]);
+    }
+}
+
 int run(int op, const float* A, const float* B, float* out, const Dims& d, int math, void* ws, size_t ws_bytes,
         conv_stream_t stream_) {
     cudaStream_t st = (cudaStream_t)stream_;
@@ -364,7 +417,14 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
     g.A = A;
     g.B = B;
     g.out = pl.splits > 1 ? (float*)ws : out;
+    g.Bx = nullptr;
     cudaGetLastError();  // clear sticky-free earlier errors of the caller
+    if (pl.wx_bytes) {
+        g.Bx = (char*)ws + pl.wx_off;
+        const long long rows = (long long)d.FH * d.FW * d.IC * d.OC / 32;
+        const int blocks = (int)((rows + 255) / 256 < kSMs * 4 ? (rows + 255) / 256 : kSMs * 4);
+        wx_prep_kernel<<<blocks, 256, 0, st>>>(B, (uint4*)g.Bx, d.OC, d.IC, d.FH * d.FW, op == CONV_OP_BWD_DATA);
+    }
     if (pl.variant == CONV_VARIANT_DIRECT) {
         rc = direct_launch(op, g, pl.splits, st, g_detail, sizeof g_detail);
     } else if (pl.variant == CONV_VARIANT_STRIP) {
@@ -513,7 +573,7 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
                  : pl.variant == CONV_VARIANT_TMA   ? "tma"
                                                     : "generic",
                  (pl.variant == CONV_VARIANT_TMA && pl.tp.pair) ? " pair=2cta" : "", pl.BN, pl.planes, pl.splits, pl.grid.x,
-                 pl.grid.y, pl.grid.z, pl.ws_bytes, 1 + (pl.splits > 1) + (pl.zero_mask != 0));
+                 pl.grid.y, pl.grid.z, pl.ws_bytes, 1 + (pl.splits > 1) + (pl.zero_mask != 0) + (pl.wx_bytes != 0));
     return CONV_OK;
 }
 
@@ -523,7 +583,7 @@ int conv2d_plan_kernels(int op, int N, int IH, int IW, int IC, int OC, int FH, i
     if (check_dims(op, d, math)) return -1;
     Plan pl;
     if (make_plan(op, d, math, pl)) return -1;
-    return 1 + (pl.splits > 1) + (pl.zero_mask != 0);
+    return 1 + (pl.splits > 1) + (pl.zero_mask != 0) + (pl.wx_bytes != 0);
 }
 
 int smconv_selftest_host(void) {

@@ -120,9 +120,11 @@ def test_plans_cover_network_shapes(sm):
                     d = sm.plan_describe(op, l.dims(128), math)
                     assert "variant=" in d
                     # main kernel [+ split-K reduce] [+ zero fill of tap-less dX stride phases]
+                    # [+ the bf16 W' prep of 3xTF32 fwd / dX on the TMA and STRIP variants]
                     k = sm.plan_kernels(op, l.dims(128), math)
+                    wx = math == 0 and op != 2 and ("variant=tma" in d or "variant=strip" in d)
                     assert k == 1 + ("splits=1 " not in d) + (op == 1 and l.sh * l.sw > 1 and
-                                                               "variant=tma" in d and l.FH == 1), (l.name, op, d)
+                                                               "variant=tma" in d and l.FH == 1) + wx, (l.name, op, d)
 
 
 def test_force_variant(sm):
