@@ -291,7 +291,10 @@ def main():
                            "plan": sm.plan_describe({"fwd": 0, "dx": 1, "dw": 2}[op], l.dims(B), step.math)})
     layer_rows.sort(key=lambda r: -r["ms"])
     top = layer_rows[0]
-    mathdiv = 3.0 if a.math == "3xtf32" else 1.0
+    # tensor-pipe cost per product in TF32-MMA units: 3xTF32 dW = 3 TF32 MMAs; 3xTF32 fwd / dX on the
+    # TMA / STRIP variants = 1 TF32 MMA + 1 bf16 MMA of twice the K at twice the rate = 2
+    hyb = top["op"] != "dw" and ("variant=tma" in top["plan"] or "variant=strip" in top["plan"])
+    mathdiv = (2.0 if hyb else 3.0) if a.math == "3xtf32" else 1.0
     peak_t = P["tf32_sustained"] / mathdiv
     ridge = peak_t * 1e12 / (P["hbm_gbs"] * 1e9)
     ai = top["flops"] / top["bytes"]
@@ -312,7 +315,8 @@ def main():
             pass
     roof["kernel"] = "%s %s (%s)" % (top["op"], top["layer"], top["plan"])
     roof["peak_src"] = "%s; TF32 = bf16_tflops_sustained x 1.1/2.25%s" % (
-        P["src"], " / 3 (3xTF32 issues 3 MMAs per product)" if mathdiv == 3 else "")
+        P["src"], {3.0: " / 3 (3xTF32 dW issues 3 TF32 MMAs per product)",
+                   2.0: " / 2 (3xTF32 fwd/dX: 1 TF32 MMA + 1 K-doubled bf16 MMA per product)"}.get(mathdiv, ""))
     roof["share_of_step"] = top["ms"] * a.steps / ms
 
     imgs = a.global_batch * a.steps
