@@ -259,12 +259,18 @@ SMCONV_DEV void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// arrive (release, cluster scope) on the mbarrier at the same shared-memory offset in CTA `cta`
+// arrive on the mbarrier at the same shared-memory offset in CTA `cta`.  Default semantics
+// (release at CTA scope, no fence in the SASS): what crosses the CTA boundary here is TMEM state
+// (converter tcgen05.st / epilogue tcgen05.ld), ordered by tcgen05.wait::{st,ld} +
+// tcgen05.fence::before_thread_sync on this side and fence::after_thread_sync after the wait.
+// The explicit `.release.cluster` form compiles to MEMBAR.ALL.GPU + ERRBAR, which waited for
+// every outstanding global store of the arriving warp (ncu r01n: 'membar' the second stall
+// reason of the pair kernel, pairs 1.7x slower than single-CTA tiles).
 SMCONV_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
     asm volatile(
         "{\n\t.reg .b32 ra;\n\t"
         "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
-        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+        "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
         "r"(cta)
         : "memory");
 }

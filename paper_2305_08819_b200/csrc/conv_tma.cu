@@ -22,7 +22,7 @@ int env_int(const char* name, int dflt) {
 const int g_knob_G = env_int("SMCONV_TMA_G", 0);
 const int g_knob_promo = env_int("SMCONV_TMA_L2PROMO", 3);
 const int g_knob_chunk = env_int("SMCONV_TMA_CHUNK", 8);
-std::atomic<int> g_pair{env_int("SMCONV_PAIR", 0)};  // CTA pairs (smconv_set_pair)
+std::atomic<int> g_pair{env_int("SMCONV_PAIR", 1)};  // CTA pairs (smconv_set_pair); on by default since r01o
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::atomic<int> g_encode_state{0};

@@ -120,7 +120,7 @@ def force_variant(op, variant):
 
 
 def set_pair(on):
-    """CTA-pair (cta_group::2) tiles for TMA fwd/dX in 3xTF32 (off by default); returns the old value."""
+    """CTA-pair (cta_group::2) tiles for TMA fwd/dX in 3xTF32 (on by default); returns the old value."""
     return int(lib().smconv_set_pair(1 if on else 0))
 
 
