@@ -14,20 +14,21 @@ namespace smconv {
 bool tma_encode_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
                     const uint32_t* box, CUtensorMapSwizzle sw);  // conv_tma.cu
 bool tma_encode_wx(CUtensorMap* m, const void* base, int Nn, int Kc, int T, int BNC);  // conv_tma.cu
+int tma_get_pair();                                                                      // conv_tma.cu
 
 namespace {
 
 const int g_knob_chunk_s = getenv("SMCONV_TMA_CHUNK") ? atoi(getenv("SMCONV_TMA_CHUNK")) : 8;
 
-template <int OP, int BN, int PLANES, int R>
+template <int OP, int BN, int PLANES, int R, bool PAIR = false>
 int launch_t(const StripParams& sp, const GenParams& g, cudaStream_t st, char* err, size_t errlen) {
-    using C = StripCfg<OP, BN, PLANES, R>;
+    using C = StripCfg<OP, BN, PLANES, R, PAIR>;
     static std::atomic<unsigned long long> attr_done{0};
     int dev = 0;
     cudaGetDevice(&dev);
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(attr_done.load() & bit)) {
-        if (cudaFuncSetAttribute(conv_strip_kernel<OP, BN, PLANES, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(conv_strip_kernel<OP, BN, PLANES, R, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::SMEM_BYTES) != cudaSuccess) {
             snprintf(err, errlen, "cudaFuncSetAttribute(strip smem=%d): %s", C::SMEM_BYTES,
                      cudaGetErrorString(cudaGetLastError()));
@@ -35,14 +36,36 @@ int launch_t(const StripParams& sp, const GenParams& g, cudaStream_t st, char* e
         }
         attr_done.fetch_or(bit);
     }
+    if (PAIR) {  // 2-CTA clusters: one M = 256 tile (two 32-image strips) per pair
+        const int pairs = sp.work < 74 ? sp.work : 74;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * pairs, 1, 1);
+        cfg.blockDim = dim3(C::NTHREADS, 1, 1);
+        cfg.dynamicSmemBytes = C::SMEM_BYTES;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, conv_strip_kernel<OP, BN, PLANES, R, PAIR>, sp, g);
+        if (e != cudaSuccess) {
+            snprintf(err, errlen, "cudaLaunchKernelEx(strip pair): %s", cudaGetErrorString(e));
+            return CONV_ECUDA;
+        }
+        return CONV_OK;
+    }
     const int grid = sp.work < 148 ? sp.work : 148;
-    conv_strip_kernel<OP, BN, PLANES, R><<<grid, C::NTHREADS, C::SMEM_BYTES, st>>>(sp, g);
+    conv_strip_kernel<OP, BN, PLANES, R, PAIR><<<grid, C::NTHREADS, C::SMEM_BYTES, st>>>(sp, g);
     return CONV_OK;
 }
 
 template <int OP>
 int launch_op(int BN, int planes, const StripParams& sp, const GenParams& g, cudaStream_t st, char* err, size_t n) {
     if (planes == 2) {
+        if (sp.pair) return launch_t<OP, 64, 2, 1, true>(sp, g, st, err, n);
         if (BN == 32) return launch_t<OP, 32, 2, 1>(sp, g, st, err, n);
         return launch_t<OP, 64, 2, 1>(sp, g, st, err, n);
     }
@@ -56,6 +79,13 @@ int launch_op(int BN, int planes, const StripParams& sp, const GenParams& g, cud
 int strip_R(int BN, int planes) {
     if (planes == 2) return 1;
     return BN == 32 ? 4 : BN == 64 ? 2 : 1;
+}
+
+// CTA-pair strips (conv_strip.cuh PAIR): 3xTF32, BN 64, an even number of 32-image groups;
+// follows the TMA variant's pair switch (smconv_set_pair / SMCONV_PAIR)
+bool strip_pair(int op, int N, int BN, int planes) {
+    (void)op;
+    return planes == 2 && BN == 64 && N % 64 == 0 && tma_get_pair() != 0;
 }
 
 bool strip_supported(int op, int N, int IC, int OC, int FW, int sh, int sw, int OWo, int BN, int planes) {
@@ -83,7 +113,9 @@ int strip_launch(int op, int BN, int planes, const GenParams& g, cudaStream_t st
     sp.SW = (int)W;
     sp.strips = (sp.OWo + 4 * R - 1) / (4 * R);
     sp.n_tiles = (g.Ngemm + BN - 1) / BN;
-    sp.work = sp.NG * sp.OHo * sp.strips * sp.n_tiles;
+    sp.pair = strip_pair(op, g.N, BN, planes) ? 1 : 0;
+    sp.work = (sp.pair ? sp.NG / 2 : sp.NG) * sp.OHo * sp.strips * sp.n_tiles;
+    const int BNC = sp.pair ? BN / 2 : BN;  // B columns staged per CTA
     sp.chunk_kb = g_knob_chunk_s > 0 ? g_knob_chunk_s : 8;
     sp.row_off = fwd ? -g.ph : g.ph;
     sp.col_off = fwd ? -g.pw : g.pw - (kStripFW - 1);
@@ -94,15 +126,15 @@ int strip_launch(int op, int BN, int planes, const GenParams& g, cudaStream_t st
     bool ok = tma_encode_f32(&sp.mapA, g.A, 5, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B);
     if (fwd) {
         uint64_t db[3] = {(uint64_t)g.IC, (uint64_t)g.OC, T}, sb[2] = {T * g.IC * 4, (uint64_t)g.IC * 4};
-        uint32_t bb[3] = {32, (uint32_t)BN, (uint32_t)kStripFW};
+        uint32_t bb[3] = {32, (uint32_t)BNC, (uint32_t)kStripFW};
         ok &= tma_encode_f32(&sp.mapB, g.B, 3, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B);
     } else {
         uint64_t db[4] = {32, (uint64_t)g.OC, (uint64_t)g.IC / 32, T}, sb[3] = {T * g.IC * 4, 128, (uint64_t)g.IC * 4};
-        uint32_t bb[4] = {32, 32, (uint32_t)(BN / 32), (uint32_t)kStripFW};
+        uint32_t bb[4] = {32, 32, (uint32_t)(BNC / 32), (uint32_t)kStripFW};
         ok &= tma_encode_f32(&sp.mapB, g.B, 4, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     }
     if (planes == 2)
-        ok &= g.Bx && tma_encode_wx(&sp.mapBx, g.Bx, fwd ? g.OC : g.IC, fwd ? g.IC : g.OC, (int)T, BN);
+        ok &= g.Bx && tma_encode_wx(&sp.mapBx, g.Bx, fwd ? g.OC : g.IC, fwd ? g.IC : g.OC, (int)T, BNC);
     if (!ok) {
         snprintf(err, errlen, "strip: cuTensorMapEncodeTiled failed (op %d)", op);
         return CONV_ECUDA;

@@ -15,6 +15,11 @@
 // warp quadrant q handles position 4j + q.  Zero padding / ragged strips = TMA OOB zero fill.
 // Roles, 3xTF32 handling (TF32 a_hi*b_hi + bf16 cross terms on the precomputed W' plane) and
 // TMEM double buffering are those of conv_tma.cuh.
+//
+// PAIR (3xTF32, BN = 64): a 2-CTA cluster runs two strips of the same output row and columns for
+// consecutive 32-image groups as ONE M = 256 tile (tcgen05 cta_group::2): each CTA stages its own
+// slabs (A windows in its own TMEM) and half of B (32 filter columns); CTA 0 issues the MMAs, the
+// commits arrive in both CTAs.  N = 64 MMAs run at ~57 % of the pair rate on one CTA.
 #pragma once
 #include "conv_tma.cuh"
 
@@ -34,14 +39,16 @@ struct __align__(64) StripParams {
     int n_tiles, work, chunk_kb;
     int row_off;       // source row = out row + row_off + (fwd: fh | dX: -fh)   (fwd: -ph, dX: +ph)
     int col_off;       // first slab column = strip origin + col_off (fwd: -pw, dX: pw - (FW-1))
+    int pair;          // work items are pair tiles (two 32-image groups), kernel template PAIR
 };
 
-template <int OP, int BN, int PLANES, int R>
+template <int OP, int BN, int PLANES, int R, bool PAIR = false>
 struct StripCfg {
     static constexpr int FW = kStripFW;
     static constexpr int SLABS = 4 * R + FW - 1;
     static constexpr int A_BYTES = SLABS * 4096;
-    static constexpr int B_BYTES = FW * BN * 128;
+    static constexpr int BNC = PAIR ? BN / 2 : BN;  // B columns staged by this CTA (a pair splits B)
+    static constexpr int B_BYTES = FW * BNC * 128;
     // 3xTF32: the converters write the R*FW A windows (hi and lo) into TMEM, so the 3 MMAs per
     // k-step read A from TMEM and only b_lo is stored in shared memory (smem-bandwidth bound path)
     static constexpr bool A_TMEM = (PLANES == 2);
@@ -66,17 +73,19 @@ struct StripCfg {
     static_assert(!A_TMEM || (R == 1 && NT * FW <= 8), "3xTF32 strips: one window per filter column, per-window barriers");
     static_assert(ACC_COLS <= 512, "TMEM");
     static_assert(PLANES == 1 || R * BN <= 128, "3xTF32 promotion keeps R*BN/2 fp32 per epilogue thread");
+    static_assert(!PAIR || (A_TMEM && R == 1 && BN == 64), "strip pairs: 3xTF32, BN 64");
 };
 
 struct StripTile {
     int g, orow, s, nt;
-    SMCONV_DEV void init(const StripParams& sp, int w) {
+    SMCONV_DEV void init(const StripParams& sp, int w, int rank = 0) {
         nt = w % sp.n_tiles;
         int r = w / sp.n_tiles;
         s = r % sp.strips;
         r /= sp.strips;
         orow = r % sp.OHo;
         g = r / sp.OHo;
+        if (sp.pair) g = 2 * g + rank;  // pair tile: image groups 2g' (CTA 0) and 2g'+1 (CTA 1)
     }
 };
 
@@ -93,10 +102,10 @@ SMCONV_DEV int strip_rows(const StripParams& sp, const GenParams& p, int orow) {
     return n;
 }
 
-template <int OP, int BN, int PLANES, int R>
-__global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
+template <int OP, int BN, int PLANES, int R, bool PAIR = false>
+__global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1)
     conv_strip_kernel(const __grid_constant__ StripParams sp, const __grid_constant__ GenParams p) {
-    using C = StripCfg<OP, BN, PLANES, R>;
+    using C = StripCfg<OP, BN, PLANES, R, PAIR>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     const uint32_t tiles_addr = (raw_addr + 1023u) & ~1023u;
@@ -104,19 +113,25 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
     TmaAux* aux = reinterpret_cast<TmaAux*>(tiles_ptr + C::STAGES * C::STAGE_BYTES);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int CHK = PLANES == 2 ? sp.chunk_kb : (1 << 30);
+    // pairs: both CTAs of a cluster walk the same pair tiles; CTA 0 issues the MMAs and owns the
+    // conv / tempty barriers (per-warp arrivals from both CTAs), commits arrive in both CTAs
+    const int rank = PAIR ? (int)cluster_ctarank() : 0;
+    const int wfirst = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int wstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
     if (tid == 0) {
         for (int t = 0; t < C::NT; ++t) mbar_init(&aux->tfree[t], 1);
         // 3xTF32: one conv barrier per (slot, filter column) so the MMAs of window 0 start while
         // windows 1 and 2 are still being split (the converters' per-stage latency bounded the strip)
-        for (int t = 0; t < (C::A_TMEM ? C::NT * C::FW : C::NT); ++t) mbar_init(&aux->conv[t], C::NCONV * 32);
+        for (int t = 0; t < (C::A_TMEM ? C::NT * C::FW : C::NT); ++t)
+            mbar_init(&aux->conv[t], PAIR ? 2 * C::NCONV : C::NCONV * 32);
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&aux->full[s], 1);
             mbar_init(&aux->empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&aux->tfull[b], 1);
-            mbar_init(&aux->tempty[b], C::NEPI * 32);
+            mbar_init(&aux->tempty[b], PAIR ? 2 * C::NEPI : C::NEPI * 32);
         }
         fence_mbar_init();
     }
@@ -125,9 +140,13 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
         prefetch_tmap(&sp.mapB);
         if (C::A_TMEM) prefetch_tmap(&sp.mapBx);
     }
-    if (warp == C::MMA_W) tmem_alloc(&aux->tmem_base, C::TMEM_COLS);
+    if (warp == C::MMA_W) {
+        if (PAIR) tmem_alloc2(&aux->tmem_base, C::TMEM_COLS);
+        else tmem_alloc(&aux->tmem_base, C::TMEM_COLS);
+    }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();  // the peer's barriers exist before any remote arrival
     tc_fence_after();
     const uint32_t tmem = aux->tmem_base;
 
@@ -135,26 +154,30 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
         // ======================= TMA producer: 2 boxes per stage (slab row, FW filter taps)
         int s = 0;
         uint32_t r = 0;
-        for (int w = blockIdx.x; w < sp.work; w += gridDim.x) {
+        for (int w = wfirst; w < sp.work; w += wstep) {
             StripTile t;
-            t.init(sp, w);
+            t.init(sp, w, rank);
             const int col0 = t.s * 4 * R + sp.col_off;
+            const int nb0 = t.nt * BN + rank * C::BNC;  // this CTA's half of B (pairs)
             for (int fh = 0; fh < p.FH; ++fh) {
                 const int srow = strip_src_row<OP>(sp, t.orow, fh);
                 if ((unsigned)srow >= (unsigned)sp.SH) continue;
                 for (int cb = 0; cb < sp.CB; ++cb) {
-                    if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
+                    if (r > 0) {
+                        if (PAIR) mbar_wait_cluster(&aux->empty[s], (r - 1) & 1);
+                        else mbar_wait(&aux->empty[s], (r - 1) & 1);
+                    }
                     const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
                     const uint32_t sB = sA + C::B_OFF;
                     if (elect_one()) {
                         mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + (C::A_TMEM ? 2 : 1) * C::B_BYTES);
                         tma_load_5d(sA, &sp.mapA, &aux->full[s], 0, t.g * 32, col0, srow, cb);
-                        if (OP == OP_FWD) tma_load_3d(sB, &sp.mapB, &aux->full[s], cb * 32, t.nt * BN, fh * C::FW);
-                        else tma_load_4d(sB, &sp.mapB, &aux->full[s], 0, cb * 32, t.nt * BN / 32, fh * C::FW);
-                        if (C::A_TMEM)  // W' planes of the FW taps: [fw][BN rows][128 B]
+                        if (OP == OP_FWD) tma_load_3d(sB, &sp.mapB, &aux->full[s], cb * 32, nb0, fh * C::FW);
+                        else tma_load_4d(sB, &sp.mapB, &aux->full[s], 0, cb * 32, nb0 / 32, fh * C::FW);
+                        if (C::A_TMEM)  // W' planes of the FW taps: [fw][BNC rows][128 B]
 #pragma unroll
                             for (int fw = 0; fw < C::FW; ++fw)
-                                tma_load_4d(sB + C::B_BYTES + fw * BN * 128, &sp.mapBx, &aux->full[s], 0, cb, t.nt * BN,
+                                tma_load_4d(sB + C::B_BYTES + fw * C::BNC * 128, &sp.mapBx, &aux->full[s], 0, cb, nb0,
                                             fh * C::FW + fw);
                     }
                     __syncwarp();
@@ -167,25 +190,28 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
         }
     } else if (warp == C::MMA_W) {
         // ======================= MMA issuer: R accumulators x FW taps x 4 k-steps per stage
-        constexpr uint32_t IDESC = idesc_tf32(128, BN, false, C::B_MN);
+        // (pairs: CTA 0 issues M = 256 MMAs for both CTAs; CTA 1's MMA warp only owns its TMEM)
+        if (PAIR && rank != 0) goto strip_done;
+        constexpr uint32_t IDESC = idesc_tf32(PAIR ? 256 : 128, BN, false, C::B_MN);
         const uint64_t adH0 = make_sdesc(tiles_addr, 16u, 1024u, kLayoutSW128);
         const uint64_t bdH0 = make_sdesc(tiles_addr + C::B_OFF, C::B_MN ? 4096u : 16u,
                                          C::B_MN ? 512u : 1024u, C::B_MN ? kLayoutSW128Base32 : kLayoutSW128);
         // 3xTF32 cross terms: bf16 B' planes [b_lo | b] (K-major, 128 B per row) after the b_hi taps
-        constexpr uint32_t IDESC_X = idesc_bf16(128, BN, false, false);
+        constexpr uint32_t IDESC_X = idesc_bf16(PAIR ? 256 : 128, BN, false, false);
         const uint64_t bx0 = make_sdesc(tiles_addr + C::B_OFF + C::B_BYTES, 16u, 1024u, kLayoutSW128);
-        constexpr uint64_t B_G = C::B_MN ? 64 : 2, B_TAP = (BN * 128) >> 4;
+        constexpr uint64_t B_G = C::B_MN ? 64 : 2, B_TAP = (C::BNC * 128) >> 4;
         int s = 0, in_chunk = 0;
         uint32_t r = 0, c = 0, q = 0;
-        for (int w = blockIdx.x; w < sp.work; w += gridDim.x) {
+        for (int w = wfirst; w < sp.work; w += wstep) {
             StripTile t;
-            t.init(sp, w);
+            t.init(sp, w, rank);
             const int nkb = strip_rows<OP>(sp, p, t.orow) * sp.CB;
             for (int it = 0; it < nkb; ++it, ++q) {
                 const int buf = c & 1;
                 const uint32_t ts = q % C::NT, rts = q / C::NT;  // TMEM A-window slot
                 if (in_chunk == 0 && c >= 2) {
-                    mbar_wait(&aux->tempty[buf], ((c >> 1) - 1) & 1);
+                    if (PAIR) mbar_wait_cluster(&aux->tempty[buf], ((c >> 1) - 1) & 1);
+                    else mbar_wait(&aux->tempty[buf], ((c >> 1) - 1) & 1);
                     tc_fence_after();
                 }
                 if (!C::A_TMEM) {
@@ -202,7 +228,8 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
 #pragma unroll
                         for (int fw = 0; fw < C::FW; ++fw) {
                             if (C::A_TMEM) {
-                                mbar_wait(&aux->conv[ts * C::FW + fw], rts & 1);
+                                if (PAIR) mbar_wait_cluster(&aux->conv[ts * C::FW + fw], rts & 1);
+                                else mbar_wait(&aux->conv[ts * C::FW + fw], rts & 1);
                                 tc_fence_after();
                             }
                             const int woff = OP == OP_FWD ? fw : C::FW - 1 - fw;
@@ -217,7 +244,8 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                                 if (C::A_TMEM) {
                                     const uint32_t ahi =
                                         tmem + (uint32_t)(C::A_TCOL0 + ts * C::A_SLOT_COLS + (j * C::FW + fw) * 64 + g * 8);
-                                    mma_tf32_ts(d, ahi, bdH, IDESC, acc0);  // a_hi * b_hi
+                                    if (PAIR) mma2_tf32_ts(d, ahi, bdH, IDESC, acc0);  // a_hi * b_hi
+                                    else mma_tf32_ts(d, ahi, bdH, IDESC, acc0);
                                 } else {
                                     mma_tf32_ss(d, adH, bdH, IDESC, acc0);
                                 }
@@ -225,16 +253,24 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                             if (C::A_TMEM && issuer) {  // cross terms, bf16, K = 64 in 4 MMAs
                                 const uint32_t ax = tmem + (uint32_t)(C::A_TCOL0 + ts * C::A_SLOT_COLS + (j * C::FW + fw) * 64 + 32);
 #pragma unroll
-                                for (int jj = 0; jj < 4; ++jj)
-                                    mma_bf16_ts(d, ax + jj * 8, bx0 + so + fw * B_TAP + jj * 2, IDESC_X, 1u);
+                                for (int jj = 0; jj < 4; ++jj) {
+                                    if (PAIR) mma2_bf16_ts(d, ax + jj * 8, bx0 + so + fw * B_TAP + jj * 2, IDESC_X, 1u);
+                                    else mma_bf16_ts(d, ax + jj * 8, bx0 + so + fw * B_TAP + jj * 2, IDESC_X, 1u);
+                                }
                             }
                             __syncwarp();
                         }
                     }
                     if (elect_one()) {
-                        mma_commit(&aux->empty[s]);
-                        if (C::A_TMEM) mma_commit(&aux->tfree[ts]);
-                        if (last) mma_commit(&aux->tfull[buf]);
+                        if (PAIR) {
+                            mma2_commit_both(&aux->empty[s]);
+                            mma2_commit_both(&aux->tfree[ts]);
+                            if (last) mma2_commit_both(&aux->tfull[buf]);
+                        } else {
+                            mma_commit(&aux->empty[s]);
+                            if (C::A_TMEM) mma_commit(&aux->tfree[ts]);
+                            if (last) mma_commit(&aux->tfull[buf]);
+                        }
                     }
                 }
                 __syncwarp();
@@ -256,15 +292,16 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
         constexpr int NCT = C::NCONV > 0 ? C::NCONV * 32 : 32;
         int s = 0;
         uint32_t r = 0, q = 0;
-        for (int w = blockIdx.x; w < sp.work; w += gridDim.x) {
+        for (int w = wfirst; w < sp.work; w += wstep) {
             StripTile t;
-            t.init(sp, w);
+            t.init(sp, w, rank);
             const int nkb = strip_rows<OP>(sp, p, t.orow) * sp.CB;
             for (int it = 0; it < nkb; ++it, ++q) {
                 const uint32_t ts = q % C::NT, rts = q / C::NT;  // TMEM A-window slot
                 mbar_wait(&aux->full[s], r & 1);
                 if (C::A_TMEM && rts > 0) {  // the slot's previous windows have been multiplied
-                    mbar_wait(&aux->tfree[ts], (rts - 1) & 1);
+                    if (PAIR) mbar_wait_cluster(&aux->tfree[ts], (rts - 1) & 1);
+                    else mbar_wait(&aux->tfree[ts], (rts - 1) & 1);
                     tc_fence_after();
                 }
                 uint8_t* st = tiles_ptr + s * C::STAGE_BYTES;
@@ -303,7 +340,12 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                         tmem_st_wait();
                         fence_proxy_async_smem();
                         tc_fence_before();
-                        mbar_arrive(&aux->conv[ts * C::FW + fw]);
+                        if (PAIR) {  // one arrival per warp, on CTA 0's barrier (it issues the MMAs)
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_remote(&aux->conv[ts * C::FW + fw], 0);
+                        } else {
+                            mbar_arrive(&aux->conv[ts * C::FW + fw]);
+                        }
                     }
                 } else {
                     const float4* aH = reinterpret_cast<const float4*>(st);
@@ -342,9 +384,9 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
         constexpr int HALF = BN / 2;
         const uint32_t lane_addr = (uint32_t)(qd * 32) << 16;
         uint32_t c = 0;
-        for (int w = blockIdx.x; w < sp.work; w += gridDim.x) {
+        for (int w = wfirst; w < sp.work; w += wstep) {
             StripTile t;
-            t.init(sp, w);
+            t.init(sp, w, rank);
             const int nkb = strip_rows<OP>(sp, p, t.orow) * sp.CB;
             const int nch = nkb > 0 ? (nkb + CHK - 1) / CHK : 0;
             const int n0 = t.nt * BN;
@@ -366,7 +408,8 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                     for (int e = 0; e < HALF; ++e) acc[j][e] = 0.f;
                 for (int k = 0; k < nch; ++k, ++c) {
                     const int buf = c & 1;
-                    mbar_wait(&aux->tfull[buf], (c >> 1) & 1);
+                    if (PAIR) mbar_wait_cluster(&aux->tfull[buf], (c >> 1) & 1);
+                    else mbar_wait(&aux->tfull[buf], (c >> 1) & 1);
                     tc_fence_after();
 #pragma unroll
                     for (int j = 0; j < R; ++j)
@@ -379,7 +422,12 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
                             for (int e = 0; e < 16; ++e) acc[j][c0 + e] += __uint_as_float(v[e]);
                         }
                     tc_fence_before();
-                    mbar_arrive(&aux->tempty[buf]);
+                    if (PAIR) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_remote(&aux->tempty[buf], 0);
+                    } else {
+                        mbar_arrive(&aux->tempty[buf]);
+                    }
                 }
 #pragma unroll
                 for (int j = 0; j < R; ++j)
@@ -429,16 +477,20 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R>::NTHREADS, 1)
         }
     }
 
+strip_done:
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();  // the peer's MMAs / arrivals are done before TMEM is released
     if (warp == C::MMA_W) {
         tc_fence_after();
-        tmem_dealloc(tmem, C::TMEM_COLS);
+        if (PAIR) tmem_dealloc2(tmem, C::TMEM_COLS);
+        else tmem_dealloc(tmem, C::TMEM_COLS);
     }
 }
 
 bool strip_supported(int op, int N, int IC, int OC, int FW, int sh, int sw, int OWo, int BN, int planes);
 int strip_launch(int op, int BN, int planes, const GenParams& g, cudaStream_t st, char* err, size_t errlen);
 int strip_R(int BN, int planes);
+bool strip_pair(int op, int N, int BN, int planes);
 
 }  // namespace smconv

@@ -127,6 +127,7 @@ int launch_op(int BN, int planes, const TmaParams& tp, const GenParams& g, dim3 
 }  // namespace
 
 int tma_set_pair(int on) { return g_pair.exchange(on); }
+int tma_get_pair() { return g_pair.load(); }
 
 bool tma_encode_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
                     const uint32_t* box, CUtensorMapSwizzle sw) {

@@ -572,7 +572,10 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
                  : pl.variant == CONV_VARIANT_STRIP ? "strip"
                  : pl.variant == CONV_VARIANT_TMA   ? "tma"
                                                     : "generic",
-                 (pl.variant == CONV_VARIANT_TMA && pl.tp.pair) ? " pair=2cta" : "", pl.BN, pl.planes, pl.splits, pl.grid.x,
+                 ((pl.variant == CONV_VARIANT_TMA && pl.tp.pair) ||
+                  (pl.variant == CONV_VARIANT_STRIP && strip_pair(op, N, pl.BN, pl.planes)))
+                     ? " pair=2cta"
+                     : "", pl.BN, pl.planes, pl.splits, pl.grid.x,
                  pl.grid.y, pl.grid.z, pl.ws_bytes, 1 + (pl.splits > 1) + (pl.zero_mask != 0) + (pl.wx_bytes != 0));
     return CONV_OK;
 }

@@ -305,15 +305,24 @@ SWEEP_STRIP = [
     (32, 6, 6, 64, 64, 3, 3, 1, 1, 0, 0),       # no padding
     (32, 5, 9, 32, 64, 5, 3, 1, 1, 2, 1),       # FH 5 rows, pad 2 / 1
     (96, 4, 4, 64, 64, 3, 3, 1, 1, 1, 1),       # 3 image groups, 4x4 map
+    # CTA-pair strips (3xTF32, BN 64, N % 64 == 0: two 32-image groups per M = 256 tile)
+    (64, 32, 32, 64, 64, 3, 3, 1, 1, 1, 1),     # l1 class, one pair image block
+    (192, 7, 10, 64, 64, 3, 3, 1, 1, 1, 1),     # 3 pair blocks, ragged strip
+    (64, 5, 9, 64, 64, 5, 3, 1, 1, 2, 1),       # FH 5 rows, pad 2 / 1 (skipped filter rows)
+    (128, 6, 6, 96, 64, 3, 3, 1, 1, 0, 0),      # no padding, 3 channel blocks of fwd K (dX BN 96: not 3xTF32)
 ]
 
 
-@pytest.fixture
-def force_strip(env):
+@pytest.fixture(params=["single", "pair"])
+def force_strip(env, request):
+    """STRIP variant forced; once with 1-CTA strips and once with CTA-pair strips (pairs apply in
+    3xTF32 at BN 64 when N % 64 == 0; other cases are unchanged)."""
     _, _, sm = env
     for op in (0, 1):
         sm.force_variant(op, sm.CONV_VARIANT_STRIP)
+    old = sm.set_pair(request.param == "pair")
     yield
+    sm.set_pair(old)
     for op in (0, 1):
         sm.force_variant(op, sm.CONV_VARIANT_AUTO)
 
@@ -351,7 +360,7 @@ def test_strip_parity(env, force_strip, s, math):
                 assert np.array_equal(dx.astype(np.float64), ref)
             else:
                 assert normwise(dx, ref) <= TOL[math]
-        if math == "tf32" or s[4] <= 64:
+        if math == "tf32" or (s[3] <= 64 and s[4] <= 64):  # 3xTF32 strips: BN (fwd OC, dX IC) <= 64
             assert ran == 2, "strip variant should serve this shape"
 
 
