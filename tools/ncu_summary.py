@@ -2,7 +2,7 @@
 """Summarise ncu outputs brought back in gpurun_out/ into profiles/ (run here, no GPU needed).
 
   python tools/ncu_summary.py launches <launches.csv> <kernels_per_step> <steps> > profiles/rNN_launches.md
-  python tools/ncu_summary.py full <report.ncu-rep> [key] >> profiles/rNN_ncu_full.md
+  python tools/ncu_summary.py full <report.ncu-rep | raw.csv> [key] >> profiles/rNN_ncu_full.md
 
 `launches` aggregates the per-launch gpu__time_duration of the LAST <steps> steps (cold-cache,
 serialised: compare shares, not absolutes).  `full` prints the counters the roofline uses
@@ -54,7 +54,10 @@ def launches(path, per_step, steps):
 
 
 def full(path, key=None):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):  # `ncu -i rep --page raw --csv` exported on the GPU box
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     h, units = rows[0], rows[1]
     for r in rows[2:]:
