@@ -23,6 +23,7 @@ const int g_knob_G = env_int("SMCONV_TMA_G", 0);
 const int g_knob_promo = env_int("SMCONV_TMA_L2PROMO", 3);
 const int g_knob_chunk = env_int("SMCONV_TMA_CHUNK", 8);
 std::atomic<int> g_pair{env_int("SMCONV_PAIR", 1)};  // CTA pairs (smconv_set_pair); on by default since r01o
+const int g_dw_pair = env_int("SMCONV_DW_PAIR", 1);  // dW pairs (A/B knob; follows g_pair when on)
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::atomic<int> g_encode_state{0};
@@ -103,7 +104,7 @@ int launch_t(const TmaParams& tp, const GenParams& g, dim3 grid, cudaStream_t st
 
 template <int OP, int PLANES>
 int launch_bn(int BN, const TmaParams& tp, const GenParams& g, dim3 grid, cudaStream_t st, char* err, size_t n) {
-    constexpr bool PAIRABLE = PLANES == 2 && (OP == OP_FWD || OP == OP_DX);
+    constexpr bool PAIRABLE = PLANES == 2 && (OP == OP_FWD || OP == OP_DX || OP == OP_DW);
     if (PAIRABLE && tp.pair) {
         if (BN == 64) return launch_t<OP, 64, PLANES, PAIRABLE>(tp, g, grid, st, err, n);
         return launch_t<OP, 128, PLANES, PAIRABLE>(tp, g, grid, st, err, n);
@@ -171,8 +172,16 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
         tp.CB = g.OC / 32;
     }
     // CTA pairs (cta_group::2): fwd / dx in 3xTF32 when 256-row pair tiles (two 128-image blocks at
-    // one position) tile every phase exactly
+    // one position) tile every phase exactly; dW (not transposed) when OC is a multiple of 256
     const int pair_mode = g_pair.load();
+    if (op == CONV_OP_BWD_FILTER && !g.dwt && planes == 2 && pair_mode && g_dw_pair && BN == 128 && g.OC % 256 == 0 &&
+        tp.m_tiles % 2 == 0) {
+        tp.pair = 1;
+        tp.m_tiles /= 2;
+        tp.work = tp.m_tiles * tp.n_tiles * g.splits;
+        const int pairs = tp.work < 74 ? tp.work : 74;
+        grid = dim3(2 * pairs, 1, 1);
+    }
     if ((op == CONV_OP_FWD || op == CONV_OP_BWD_DATA) && planes == 2 && pair_mode && tp.G == 128 &&
         g.N % 256 == 0 && (BN == 64 || BN == 128) && tp.m_tiles % 2 == 0) {
         bool even = true;
@@ -208,8 +217,9 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
             tp.a_box_cols = gcd(128, g.IC);
             tp.a_boxes = 128 / tp.a_box_cols;
         } else {
-            tp.b_box_cols = gcd(BN, g.IC);
-            tp.b_boxes = BN / tp.b_box_cols;
+            const int bnc = tp.pair ? BN / 2 : BN;  // B columns staged per CTA
+            tp.b_box_cols = gcd(bnc, g.IC);
+            tp.b_boxes = bnc / tp.b_box_cols;
             if (g.IC % BN == 0) tp.dw_tap_tiles = g.IC / BN;  // n-tiles never straddle a tap
         }
     }

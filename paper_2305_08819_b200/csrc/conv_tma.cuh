@@ -98,7 +98,7 @@ struct TmaCfg {
     static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + AUX_BYTES;
     static_assert(STAGES >= 2, "stage does not fit");
     static_assert(PLANES == 1 || BN <= 128, "3xTF32 promotion keeps BN/2 fp32 per epilogue thread");
-    static_assert(!PAIR || (PLANES == 2 && !IS_DW && BN >= 64), "CTA pairs: fwd / dx, 3xTF32");
+    static_assert(!PAIR || (PLANES == 2 && OP != OP_DWT && BN >= 64), "CTA pairs: fwd / dx / dW, 3xTF32");
 };
 
 struct TmaAux {
@@ -171,6 +171,9 @@ struct TileInfo {
         }
         constexpr bool DWK = (OP == OP_DW || OP == OP_DWT);  // reduction over pixels
         m0 = mt * 128;
+        // dW pair tiles: the two CTAs take output-channel blocks 2*mt and 2*mt+1 (same n-tile, same
+        // pixel range, so one shared k-loop)
+        if (OP == OP_DW && tp.pair) m0 = (2 * mt + rank) * 128;
         if (!DWK && tp.G == 128) {
             // image-block-major walk over (128-image block, position): consecutive tiles are
             // neighbouring positions of the same images, so the 3x3 taps' source rows are reused
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     // X boxes of this tile (dw: B side; dwT: A side): tap offsets and channel block
                     const int nboxes = OP == OP_DWT ? tp.a_boxes : tp.b_boxes;
                     const int bcols = OP == OP_DWT ? tp.a_box_cols : tp.b_box_cols;
-                    const int base = OP == OP_DWT ? ti.m0 : n0;
+                    const int base = OP == OP_DWT ? ti.m0 : n0 + rank * C::BNC;  // this CTA's half of B (pairs)
                     const int lim = OP == OP_DWT ? p.M : p.Ngemm;
                     int nbox = 0;
                     for (int b = 0; b < nboxes; ++b) {
@@ -482,10 +485,13 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                             const uint64_t adH = adH0 + so + g * A_G, bdH = bdH0 + so + g * B_G;
                             const uint32_t acc0 = (in_chunk > 0 || g > 0) ? 1u : 0u;
                             const uint32_t ahi = tmem + (uint32_t)(C::A_TCOL0 + t * 64 + g * 8);
-                            if (PAIR) {
-                                mma2_tf32_ts(d, ahi, bdH, IDESC, acc0);  // a_hi * b_hi (TF32)
-                            } else if (C::HYB) {
-                                mma_tf32_ts(d, ahi, bdH, IDESC, acc0);
+                            if (C::HYB) {  // a_hi * b_hi (TF32); cross terms below
+                                if (PAIR) mma2_tf32_ts(d, ahi, bdH, IDESC, acc0);
+                                else mma_tf32_ts(d, ahi, bdH, IDESC, acc0);
+                            } else if (C::A_TMEM && PAIR) {  // dW pairs: three TF32 MMAs, M = 256
+                                mma2_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);
+                                mma2_tf32_ts(d, ahi, bdH + (C::B_BYTES >> 4), IDESC, 1u);
+                                mma2_tf32_ts(d, ahi, bdH, IDESC, 1u);
                             } else if (C::A_TMEM) {  // dW: three TF32 MMAs, b_lo plane after b_hi
                                 mma_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);
                                 mma_tf32_ts(d, ahi, bdH + (C::B_BYTES >> 4), IDESC, 1u);

@@ -257,6 +257,9 @@ SWEEP_TMA = [
     (256, 8, 8, 64, 64, 3, 3, 1, 1, 1, 1),     # BN 64 pairs (32-column B halves)
     (256, 8, 8, 64, 128, 3, 3, 2, 2, 1, 1),    # stride-2 dX: 4 phases of pair tiles
     (512, 3, 3, 96, 160, 3, 3, 1, 1, 1, 1),    # 2 pair image blocks, ragged N tile (160 = 128 + 32)
+    # dW pairs (3xTF32, OC % 256 == 0, BN 128: two 128-channel blocks of OC per M = 256 tile)
+    (64, 4, 4, 128, 256, 3, 3, 1, 1, 1, 1),    # l3/l4 class, single-tap tiles (IC % BN == 0)
+    (32, 5, 5, 96, 512, 3, 3, 2, 2, 1, 1),     # stride 2, 2 pair m-tiles, n-tiles straddling taps
 ]
 
 
