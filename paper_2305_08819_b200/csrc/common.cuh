@@ -275,12 +275,17 @@ SMCONV_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
         : "memory");
 }
 
-// wait with cluster-scope acquire (the arrivals came from the peer CTA)
+// wait on a barrier the peer CTA (or a multicast commit) arrives on.  CTA-scope acquire (the
+// default): no generic-proxy data crosses the CTA boundary here (TMEM state is ordered by the
+// tcgen05 fences, smem stages by the TMA / MMA mbarrier protocol).  `.acquire.cluster` compiles to
+// a CCTL.IVALL (L1 invalidate) after every successful wait: 22 % of the stall samples of the pair
+// l2.0a dX kernel (ncu source view, r01r) sat on it; dropping it bought ~0.5 % of the step (r01t,
+// the step is power-capped).
 SMCONV_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "SMCONV_WAITC_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra SMCONV_WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
