@@ -8,6 +8,7 @@
 // products (more accurate than 3xTF32), deterministic (dW partials reduced in a fixed order by
 // the split-K reduction kernel).
 #include <cstdio>
+#include <cstdlib>
 
 #include "../../include/smconv.h"
 #include "conv_gen.cuh"
@@ -30,7 +31,7 @@ struct DirectParams {
     int rows_per_block;
 };
 
-constexpr int kDirNB = 4;  // dW: cp.async row ring depth (3 rows in flight per block)
+constexpr int kDirNB = 4;  // dW: cp.async row ring depth (3 rows in flight per block; 8 measured slower, r01y)
 
 SMCONV_DEV void cp_async16(uint32_t dst, const void* src, bool valid) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
@@ -272,9 +273,11 @@ bool direct_supported(int op, int IC, int OC, int FH, int FW, int OW, int sw) {
 int direct_dw_blocks(int N, int OH) {
     // >= 32 rows per block: with fewer, the per-block ring fill and partition reduction and the
     // fixed-order sum of the per-block partials dominated (VGG stem dW at batch 128: 352 GB/s)
+    static const int min_rows = getenv("SMCONV_DIRECT_DW_ROWS") ? atoi(getenv("SMCONV_DIRECT_DW_ROWS")) : 32;
+    static const int max_blocks = getenv("SMCONV_DIRECT_DW_BLOCKS") ? atoi(getenv("SMCONV_DIRECT_DW_BLOCKS")) : 148 * 3;
     const int rows = N * OH;
-    int b = 148 * 3;
-    if (b > rows / 32) b = rows / 32;
+    int b = max_blocks;
+    if (b > rows / min_rows) b = rows / min_rows;
     return b < 1 ? 1 : b;
 }
 
