@@ -157,6 +157,9 @@ int est_taps(const Dims& d) {
     return t < 1 ? 1 : t;
 }
 
+const long long g_direct_dw_min_rows =
+    getenv("SMCONV_DIRECT_DW_MIN_ROWS") ? atoll(getenv("SMCONV_DIRECT_DW_MIN_ROWS")) : 32768;
+
 int make_plan(int op, const Dims& d, int math, Plan& pl) {
     memset(&pl, 0, sizeof pl);
     read_env_once();
@@ -176,7 +179,12 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
     }
     if (forced == CONV_VARIANT_AUTO || forced == CONV_VARIANT_DIRECT) {
         // few-channel stems: HBM-bound, K = FH*FW*IC tiny -> CUDA-core fp32 direct kernels
-        const bool direct_ok = direct_supported(op, d.IC, d.OC, d.FH, d.FW, d.OW, d.sw);
+        bool direct_ok = direct_supported(op, d.IC, d.OC, d.FH, d.FW, d.OW, d.sw);
+        // stem dW with < 32768 (n, oh) rows: the GENERIC tensor-core split-K variant is faster
+        // (r01z: VGG b128 60 vs 89 us, GoogLeNet b256 153 vs 417 us, ResNet b512 157 vs 175 us; equal
+        // at b1024); at ResNet b4096 (131k rows) DIRECT is (0.92 vs 1.39 ms)
+        if (direct_ok && forced == CONV_VARIANT_AUTO && op == CONV_OP_BWD_FILTER && (long long)d.N * d.OH < g_direct_dw_min_rows)
+            direct_ok = false;
         if (direct_ok) pl.variant = CONV_VARIANT_DIRECT;
         else if (forced == CONV_VARIANT_DIRECT)
             return fail(CONV_EUNSUPPORTED, "%s: DIRECT variant forced but unsupported for this shape", op_name(op));

@@ -127,6 +127,14 @@ def test_plans_cover_network_shapes(sm):
                                                                "variant=tma" in d and l.FH == 1) + wx, (l.name, op, d)
 
 
+def test_stem_dw_heuristic(sm):
+    """Stem dW: GENERIC split-K below 32768 (n, oh) rows, DIRECT above (measured crossover, r01z)."""
+    for N, want in ((128, "generic"), (512, "generic"), (1024, "direct"), (4096, "direct")):
+        s = (N, 32, 32, 4, 64, 3, 3, 1, 1, 1, 1)
+        assert "variant=" + want in sm.plan_describe(2, s, 0), (N, sm.plan_describe(2, s, 0))
+        assert "variant=direct" in sm.plan_describe(0, s, 0)  # fwd stays DIRECT
+
+
 def test_force_variant(sm):
     sm.force_variant(0, sm.CONV_VARIANT_GENERIC)
     assert "generic" in sm.plan_describe(0, GOOD)

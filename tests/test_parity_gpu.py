@@ -377,8 +377,19 @@ SWEEP_DIRECT = [
 ]
 
 
+@pytest.fixture
+def force_direct(env):
+    """DIRECT forced: the heuristic sends small-batch stem dW to GENERIC (r01z)."""
+    _, _, sm = env
+    for op in (0, 2):
+        sm.force_variant(op, sm.CONV_VARIANT_DIRECT)
+    yield
+    for op in (0, 2):
+        sm.force_variant(op, sm.CONV_VARIANT_AUTO)
+
+
 @pytest.mark.parametrize("s", SWEEP_DIRECT, ids=_id)
-def test_direct_parity(env, s):
+def test_direct_parity(env, force_direct, s):
     torch, oracle, sm = env
     N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw = s
     assert "direct" in sm.plan_describe(0, s) and "direct" in sm.plan_describe(2, s)
