@@ -61,6 +61,9 @@ struct GenParams {
     int8_t tf_n[kMaxPhases][2];
     int8_t tf_f[kMaxPhases][2][kMaxTF];
     int16_t tf_off[kMaxPhases][2][kMaxTF];
+    // super-pixel stride-2 dX run as a fwd conv (smconv.cu "s2dx"): output row (n, i', j') and
+    // column (pi, pj, ic) go to dX[n, 2i'-2+pi, 2j'-2+pj, ic] (rows / columns i' = 0 / j' = 0 dropped)
+    int s2dx, s2_IH, s2_IW, s2_IC;
 };
 
 template <int OP, int BN, int PLANES>

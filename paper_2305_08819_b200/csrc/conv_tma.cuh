@@ -662,7 +662,15 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                 if (m < p.M) obase = m;
             } else {
                 RowInfo ri = row_info<OP>(p, ti.phase, ti.m0 + row);
-                if (ri.ok) obase = (long long)ri.orow * p.Ngemm;
+                if (OP == OP_FWD && p.s2dx) {
+                    if (ri.ok) {
+                        const int pos = ri.orow - ri.n * p.OH * p.OW, oh = pos / p.OW, ow = pos - oh * p.OW;
+                        if (oh >= 1 && ow >= 1)
+                            obase = ((long long)(ri.n * p.s2_IH + 2 * oh - 2) * p.s2_IW + 2 * ow - 2) * p.s2_IC;
+                    }
+                } else if (ri.ok) {
+                    obase = (long long)ri.orow * p.Ngemm;
+                }
             }
             // 4 consecutive GEMM columns of this thread's row -> output
             auto st4 = [&](int col, float x, float y, float z, float w4) {
@@ -672,6 +680,10 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     o[p.M] = y;
                     o[2 * (long long)p.M] = z;
                     o[3 * (long long)p.M] = w4;
+                } else if (OP == OP_FWD && p.s2dx) {  // column (pi, pj, ic): dX row 2i'-2+pi
+                    const long long a = col >= 2 * p.s2_IC ? obase + col + (long long)(p.s2_IW - 2) * p.s2_IC
+                                                           : obase + col;
+                    *reinterpret_cast<float4*>(outp + a) = make_float4(x, y, z, w4);
                 } else {
                     *reinterpret_cast<float4*>(outp + obase + col) = make_float4(x, y, z, w4);
                 }

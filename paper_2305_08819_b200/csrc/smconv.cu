@@ -118,6 +118,8 @@ struct Plan {
     long long out_elems;
     GenParams gp;
     TmaParams tp;
+    int s2dx;                 // stride-2 3x3 dX as a super-pixel fwd conv (make_plan_s2dx)
+    size_t w2_off, w2_bytes;  // its 2x2 filter W2 [(pi, pj, ic)][2][2][OC] in the workspace
 };
 
 int pick_bn(int n) {
@@ -160,7 +162,70 @@ int est_taps(const Dims& d) {
 const long long g_direct_dw_min_rows =
     getenv("SMCONV_DIRECT_DW_MIN_ROWS") ? atoll(getenv("SMCONV_DIRECT_DW_MIN_ROWS")) : 32768;
 
+int make_plan_base(int op, const Dims& d, int math, Plan& pl);
+Dims mk(int N, int IH, int IW, int IC, int OC, int FH, int FW, int sh, int sw, int ph, int pw);
+
+// Stride-2 3x3 pad-1 deconvolution (dX of the ResNet stage-entry convs) as ONE stride-1 2x2
+// convolution of dY: for the "super-pixel" (i, j) all four stride phases (pi, pj) of dX
+// [n, 2i+pi, 2j+pj, :] read dY rows {i, i+1} x columns {j, j+1} only (O2 with ih = 2i+pi:
+// pi = 0 takes fh = 1 from oh = i; pi = 1 takes fh = 2 from oh = i and fh = 0 from oh = i+1), so
+//   Y2[n, i', j', (pi, pj, ic)] = sum_{a, b, oc} dY[n, i'-1+a, j'-1+b, oc] * W2[(pi, pj, ic), a, b, oc]
+// (pad 1, 17x17 outputs for 16x16 dY; i' = i + 1, row / column 0 dropped), with W2 built from W (9 of
+// its 16 (tap, phase) blocks non-zero).  dY is read once instead of once per phase and the GEMM is
+// N = 4 IC wide with K = 4 OC (full-rate MMAs); the phase walk streamed dY 4x in 128-B rows and
+// starved the MMAs (ncu r01r).  The same sums as O2, in a different order.
+const int g_s2dx = getenv("SMCONV_S2DX") ? atoi(getenv("SMCONV_S2DX")) : 1;
+
+int make_plan_s2dx(const Dims& d, int math, Plan& pl) {
+    if (!g_s2dx || g_force[CONV_OP_BWD_DATA].load() != CONV_VARIANT_AUTO) return -1;
+    if (d.FH != 3 || d.FW != 3 || d.sh != 2 || d.sw != 2 || d.ph != 1 || d.pw != 1) return -1;
+    if (d.IH != 2 * d.OH || d.IW != 2 * d.OW || d.IC % 64 || d.OC % 32 || d.N % 32) return -1;
+    // Only where the phase walk is starved (r01aa, b4096 3xTF32): dY maps of >= 16x16 positions
+    // (l2.0a: 1.71 -> 1.40 ms in the step; TF32 1.13 -> 0.73 ms).  On 8x8 / 4x4 maps dY stays in
+    // L2 across the phase passes and the 2x padded-MAC cost of the super-pixel GEMM loses
+    // (l3.0a 0.69 -> 1.08 ms, l4.0a 0.51 -> 0.93 ms).
+    if (d.OH * d.OW < 256) return -1;
+    Dims v = mk(d.N, d.OH, d.OW, d.OC, 4 * d.IC, 2, 2, 1, 1, 1, 1);
+    v.OH = d.OH + 1;  // (OH + 2 - 2) / 1 + 1
+    v.OW = d.OW + 1;
+    if (make_plan_base(CONV_OP_FWD, v, math, pl)) return -1;
+    if (pl.variant != CONV_VARIANT_TMA || pl.splits != 1 || pl.zero_mask) return -1;
+    pl.s2dx = 1;
+    pl.gp.s2dx = 1;
+    pl.gp.s2_IH = d.IH;
+    pl.gp.s2_IW = d.IW;
+    pl.gp.s2_IC = d.IC;
+    pl.w2_off = (pl.ws_bytes + 1023) & ~(size_t)1023;
+    pl.w2_bytes = (size_t)16 * d.IC * d.OC * sizeof(float);
+    pl.ws_bytes = pl.w2_off + pl.w2_bytes;
+    pl.out_elems = (long long)d.N * d.IH * d.IW * d.IC;
+    return 0;
+}
+
+// W2[(pi, pj, ic)][a][b][oc] = W[oc][fh(pi, a)][fw(pj, b)][ic], 0 where the phase has no such tap
+__global__ void __launch_bounds__(256) w2_build_kernel(const float* __restrict__ W, float* __restrict__ W2, int IC,
+                                                       int OC) {
+    const long long n = 16LL * IC * OC;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const int oc = (int)(e % OC);
+        long long r = e / OC;
+        const int b = (int)(r & 1), a = (int)((r >> 1) & 1);
+        r >>= 2;
+        const int ic = (int)(r % IC);
+        const int ph = (int)(r / IC), pi = ph >> 1, pj = ph & 1;
+        const int fh = pi == 0 ? (a == 0 ? 1 : -1) : (a == 0 ? 2 : 0);
+        const int fw = pj == 0 ? (b == 0 ? 1 : -1) : (b == 0 ? 2 : 0);
+        W2[e] = (fh >= 0 && fw >= 0) ? W[(((size_t)oc * 3 + fh) * 3 + fw) * IC + ic] : 0.f;
+    }
+}
+
 int make_plan(int op, const Dims& d, int math, Plan& pl) {
+    read_env_once();
+    if (op == CONV_OP_BWD_DATA && make_plan_s2dx(d, math, pl) == 0) return CONV_OK;
+    return make_plan_base(op, d, math, pl);
+}
+
+int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
     memset(&pl, 0, sizeof pl);
     read_env_once();
     pl.planes = math == CONV_MATH_FP32_3XTF32 ? 2 : 1;
@@ -427,6 +492,25 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
     g.out = pl.splits > 1 ? (float*)ws : out;
     g.Bx = nullptr;
     cudaGetLastError();  // clear sticky-free earlier errors of the caller
+    if (pl.s2dx) {  // super-pixel stride-2 dX: the virtual fwd conv's filter W2, then its W' plane
+        float* w2 = (float*)((char*)ws + pl.w2_off);
+        const long long n = 16LL * d.IC * d.OC;
+        const int blocks = (int)((n + 255) / 256 < kSMs * 8 ? (n + 255) / 256 : kSMs * 8);
+        w2_build_kernel<<<blocks, 256, 0, st>>>(B, w2, d.IC, d.OC);
+        g.B = w2;
+        if (pl.wx_bytes) {
+            g.Bx = (char*)ws + pl.wx_off;
+            const long long rows = 4LL * d.OC * 4 * d.IC / 32;
+            const int bl = (int)((rows + 255) / 256 < kSMs * 4 ? (rows + 255) / 256 : kSMs * 4);
+            wx_prep_kernel<<<bl, 256, 0, st>>>(w2, (uint4*)g.Bx, 4 * d.IC, d.OC, 4, 0);
+        }
+        TmaParams tp = pl.tp;
+        rc = tma_launch(CONV_OP_FWD, pl.BN, pl.planes, g, tp, pl.grid, st, g_detail, sizeof g_detail);
+        if (rc) return rc;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: s2dx launch failed: %s", op_name(op), cudaGetErrorString(e));
+        return CONV_OK;
+    }
     if (pl.wx_bytes) {
         g.Bx = (char*)ws + pl.wx_off;
         const long long rows = (long long)d.FH * d.FW * d.IC * d.OC / 32;
@@ -575,6 +659,7 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
     if (rc) return rc;
     if (buf && len)
         snprintf(buf, len, "variant=%s%s BN=%d planes=%d splits=%d grid=%ux%ux%u ws=%zu kernels=%d",
+                 pl.s2dx ? "tma s2dx" :
                  pl.variant == CONV_VARIANT_DWS      ? "dws"
                  : pl.variant == CONV_VARIANT_DIRECT ? "direct"
                  : pl.variant == CONV_VARIANT_STRIP ? "strip"
@@ -584,7 +669,8 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
                   (pl.variant == CONV_VARIANT_STRIP && strip_pair(op, N, pl.BN, pl.planes)))
                      ? " pair=2cta"
                      : "", pl.BN, pl.planes, pl.splits, pl.grid.x,
-                 pl.grid.y, pl.grid.z, pl.ws_bytes, 1 + (pl.splits > 1) + (pl.zero_mask != 0) + (pl.wx_bytes != 0));
+                 pl.grid.y, pl.grid.z, pl.ws_bytes,
+                 1 + (pl.splits > 1) + (pl.zero_mask != 0) + (pl.wx_bytes != 0) + (pl.s2dx != 0));
     return CONV_OK;
 }
 
@@ -594,7 +680,7 @@ int conv2d_plan_kernels(int op, int N, int IH, int IW, int IC, int OC, int FH, i
     if (check_dims(op, d, math)) return -1;
     Plan pl;
     if (make_plan(op, d, math, pl)) return -1;
-    return 1 + (pl.splits > 1) + (pl.zero_mask != 0) + (pl.wx_bytes != 0);
+    return 1 + (pl.splits > 1) + (pl.zero_mask != 0) + (pl.wx_bytes != 0) + (pl.s2dx != 0);
 }
 
 int smconv_selftest_host(void) {

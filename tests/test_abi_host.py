@@ -124,7 +124,8 @@ def test_plans_cover_network_shapes(sm):
                     k = sm.plan_kernels(op, l.dims(128), math)
                     wx = math == 0 and op != 2 and ("variant=tma" in d or "variant=strip" in d)
                     assert k == 1 + ("splits=1 " not in d) + (op == 1 and l.sh * l.sw > 1 and
-                                                               "variant=tma" in d and l.FH == 1) + wx, (l.name, op, d)
+                                                               "variant=tma" in d and l.FH == 1) + wx + \
+                        ("s2dx" in d), (l.name, op, d)
 
 
 def test_stem_dw_heuristic(sm):

@@ -367,6 +367,35 @@ def test_strip_parity(env, force_strip, s, math):
             assert ran == 2, "strip variant should serve this shape"
 
 
+# ---------------------------------------------------------------- super-pixel stride-2 dX (smconv.cu s2dx)
+SWEEP_S2DX = [  # eligible when dY has >= 16x16 positions
+    (32, 32, 32, 64, 64, 3, 3, 2, 2, 1, 1),     # l2.0a geometry, G = 32 image boxes
+    (256, 32, 32, 64, 128, 3, 3, 2, 2, 1, 1),   # N % 256: CTA-pair fwd tiles; l2.0a channels
+    (128, 32, 40, 128, 96, 3, 3, 2, 2, 1, 1),   # non-square, 2 x 128 virtual columns per phase row
+    (32, 48, 32, 64, 32, 3, 3, 2, 2, 1, 1),     # OC 32, 24x16 dY
+]
+
+
+@pytest.mark.parametrize("s", SWEEP_S2DX, ids=_id)
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+def test_s2dx_parity(env, s, math):
+    """dX of 3x3 stride-2 pad-1 convs as one super-pixel 2x2 fwd conv (all four phases at once)."""
+    torch, oracle, sm = env
+    N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw = s
+    desc = sm.plan_describe(1, s, sm.MATH[math])
+    # (TF32 plans with BN 256 may split K on the smaller shapes: then the phase path runs)
+    assert "s2dx" in desc or math == "tf32", desc
+    for integer in (1, 0):
+        X, W, dY = gen(s, 60 + integer, integer=integer)
+        w, dy = torch.from_numpy(W).cuda(), torch.from_numpy(dY).cuda()
+        dx = sm.conv2d_bwd_data(dy, w, (IH, IW), (sh, sw), (ph, pw), math=math).cpu().numpy()
+        ref = oracle.conv2d_bwd_data(dY, W, (IH, IW), (sh, sw), (ph, pw))
+        if integer:
+            assert np.array_equal(dx.astype(np.float64), ref)
+        else:
+            assert normwise(dx, ref) <= TOL[math], normwise(dx, ref)
+
+
 # ---------------------------------------------------------------- DIRECT variant (few-channel stems)
 SWEEP_DIRECT = [
     (4, 32, 32, 4, 64, 3, 3, 1, 1, 1, 1),     # the CIFAR stem (IC 3 -> 4)
