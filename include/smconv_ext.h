@@ -35,10 +35,12 @@ enum {
  * Returns CONV_EARG for an unknown op/variant. */
 int conv2d_force_variant(int op, int variant);
 
-/* CTA pairs (tcgen05 cta_group::2, M = 256 tiles, B split across the pair) for the TMA variant's
- * fwd / dX in 3xTF32 when N % 256 == 0: 1 = on (default; SMCONV_PAIR=0 at load time turns it off),
- * 0 = off.  Faster since the peer arrivals stopped emitting MEMBAR.ALL.GPU (ResNet-18
- * b4096 step 62.3 -> 59.9 ms).  Returns the previous value. */
+/* CTA pairs (tcgen05 cta_group::2, M = 256 tiles, B split across the pair), 3xTF32 only: the TMA
+ * variant's fwd / dX when N % 256 == 0 and dW when OC % 256 == 0, and the STRIP variant at BN 64 when
+ * N % 64 == 0.  1 = on (default; SMCONV_PAIR=0 at load time turns it off), 0 = off.  Results are
+ * identical in both modes up to summation order (parity-tested in both).  DESIGN.md §6 / §9: pairs
+ * won once the peer arrivals stopped emitting MEMBAR.ALL.GPU (ResNet-18 b4096 step 62.4 -> 59.1 ms,
+ * dW pairs -> 57.5 ms).  Returns the previous value. */
 int smconv_set_pair(int on);
 
 /* Plan the call would use, as text: "variant=.. BN=.. splits=.. tiles=.. kernels=..".
