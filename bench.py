@@ -141,16 +141,31 @@ def oracle_images_per_s(net, n_img, seed=0):
     return time.perf_counter() - t0, oracle.num_threads()
 
 
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def cpu_baseline(net, target_s=15.0):
+    """The oracle as it stands on ALL host cores (torchrun's OMP_NUM_THREADS=1 default overridden),
+    plus a 1-core sample."""
     oracle_mod = __import__("oracle")
     oracle_mod.build()
+    cores = host_cores()
+    oracle_mod.set_num_threads(1)
+    t1c, _ = oracle_images_per_s(net, 1, seed=3)
+    oracle_mod.set_num_threads(cores)
     t1, thr = oracle_images_per_s(net, 1, seed=1)
     n = max(1, min(256, int(target_s / max(t1, 1e-3))))
     t, thr = oracle_images_per_s(net, n, seed=2)
     return {"value": n / t, "unit": "images/s", "cores": thr, "kind": "oracle",
+            "value_1core": 1.0 / t1c,
             "sample": "%d image(s) through all %d %s convs (fwd, dX, dW; plain C double-accumulated "
-                      "direct loops, OpenMP over outputs), %.1f s" % (n, len(__import__(
-                          "paper_2305_08819_b200.nets", fromlist=["x"]).NETS[net]()), net, t)}
+                      "direct loops, OpenMP over outputs), %.1f s on %d threads; value_1core: 1 image on 1 thread "
+                      "(%.1f s)" % (n, len(__import__("paper_2305_08819_b200.nets", fromlist=["x"]).NETS[net]()),
+                                    net, t, thr, t1c)}
 
 
 def run_reference(a):
@@ -159,6 +174,7 @@ def run_reference(a):
         return 0
     import oracle
     oracle.build()
+    oracle.set_num_threads(host_cores())  # the driver's torchrun launch sets OMP_NUM_THREADS=1
     per_step = 2
     t_first, thr = oracle_images_per_s(a.net, 1, seed=9)
     per_step = max(1, min(16, int(6.0 / max(t_first, 1e-3))))
@@ -183,9 +199,28 @@ def run_reference(a):
     return 0
 
 
+# ---------------------------------------------------------------------- launcher
+def free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` run without torchrun: start the N ranks ourselves (one process per GPU,
+    torch.distributed.run on 127.0.0.1) with the same arguments; rank 0's JSON line reaches our stdout."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    print("bench.py: launching %d ranks: %s" % (n, " ".join(cmd)), file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 # ---------------------------------------------------------------------- GPU arm
 def main():
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(a.gpus)
     if a.impl == "reference":
         return run_reference(a)
     import torch
@@ -199,7 +234,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != a.gpus:
-        print("warning: --gpus %d but WORLD_SIZE %d" % (a.gpus, world), file=sys.stderr)
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE %d (launch with torchrun --nproc-per-node %d, or "
+                         "without torchrun to let bench.py spawn the ranks)" % (a.gpus, world, a.gpus))
+    if torch.cuda.device_count() < world:
+        raise SystemExit("bench.py: %d ranks but only %d visible GPU(s)" % (world, torch.cuda.device_count()))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
@@ -211,8 +249,8 @@ def main():
     if a.global_batch % world:
         raise SystemExit("global batch %d not divisible by %d ranks" % (a.global_batch, world))
     B = a.global_batch // world
-    step = dp.ConvNetStep(a.net, B, dev, math=a.math, seed=1 + 0 * rank, bucket_mb=a.bucket_mb)
-    # every rank needs the same filters: seed is rank-independent; activations differ per shard
+    # filters replicated (rank-independent seed); activations / loss gradients differ per shard
+    step = dp.ConvNetStep(a.net, B, dev, math=a.math, seed=1, bucket_mb=a.bucket_mb, rank=rank)
     torch.cuda.synchronize()
 
     def barrier():

@@ -38,13 +38,30 @@
  * Streams: each call validates synchronously, then enqueues its kernels on
  * `stream` and returns (the paper's async mode).  Validation
  * errors return before any launch; a failed launch returns CONV_ECUDA.  Device
- * faults surface at the caller's next synchronisation.
+ * faults surface at the caller's next synchronisation.  If the calling thread already has a
+ * CUDA error pending (cudaPeekAtLastError() != cudaSuccess) the call returns CONV_ECUDA
+ * without enqueuing anything and WITHOUT clearing that error (it is the caller's to handle).
  *
  * Math modes (north_star (b)):
- *   CONV_MATH_FP32_3XTF32  fp32-accurate: each operand split a = a_hi + a_lo into two
- *                          TF32 numbers; D += a_lo*b_hi + a_hi*b_lo + a_hi*b_hi on
- *                          tcgen05 tensor cores (the a_lo*b_lo term ~2^-22 is dropped).
- *   CONV_MATH_TF32         one TF32 product per term (reported separately).
+ *   CONV_MATH_FP32_3XTF32  fp32-accurate (normwise error <= 1e-5 against the fp64 definition, the
+ *                          north_star bar; measured margins in profiles/r02_parity_errors.json).
+ *                          Each operand is split a = a_hi + a_lo: a_hi = trunc_tf32(a) (the tensor
+ *                          core's own operand read) and a_lo = a - a_hi exactly in fp32 on the TMA /
+ *                          STRIP / DWS variants; a_hi = rna_tf32(a), a_lo = rna_tf32(a - a_hi) on the
+ *                          GENERIC variant.  The a_lo*b_lo term (~2^-22 relative) is dropped.
+ *                          Products per k-step:
+ *                          - dW (every variant) and every op on the GENERIC variant: three TF32 MMAs,
+ *                            a_lo*b_hi + a_hi*b_lo + a_hi*b_hi (strict 3xTF32);
+ *                          - fwd / dX on the TMA and STRIP variants (the default for 32x-channel
+ *                            layers): one TF32 MMA a_hi*b_hi plus ONE bf16 MMA of doubled K computing
+ *                            [bf16(a_hi) | bf16(a_lo)] . [bf16(b_lo) | bf16(b)] = the two cross terms
+ *                            (+ a_lo*b_lo) with each cross term rounded to bf16 (<= 2^-9 relative on a
+ *                            term <= 2^-10 of |a||b|, i.e. ~2^-19 of |a||b| per product, random sign),
+ *                            against ~2^-22 for strict 3xTF32.  "3xtf32+bf16x" in reports.
+ *                          Accumulation: TMEM chunks of <= 8 k-blocks promoted into fp32 registers
+ *                          with round-to-nearest; split-K partials summed in a fixed order.
+ *   CONV_MATH_TF32         one TF32 product per term (operands truncated by the tensor core),
+ *                          reported separately (normwise <= 5e-3).
  *
  * Determinism: for a fixed (shape, math, plan) results are bitwise reproducible —
  * no floating-point atomics; split-K partials are summed in a fixed order.

@@ -256,17 +256,36 @@ __global__ void __launch_bounds__(kDirThreads) conv_direct_dw_kernel(const __gri
 }
 
 // ---------------------------------------------------------------- host side
+// Dynamic shared memory of the direct kernels, shared by direct_supported() and direct_launch() so
+// that the AUTO heuristic only picks DIRECT when the launch fits (0 = the shape does not fit).
+constexpr size_t kDirSmemMax = 200 * 1024;
+size_t direct_smem(int op, int IC, int OC, int FH, int FW, int OW, int sw) {
+    const int WIN = (OW - 1) * sw + FW;
+    const int xs = FH * WIN * IC;
+    if (op == CONV_OP_FWD) {
+        const int trow = (OC / 4) * ((OW + kDirOWB - 1) / kDirOWB);
+        if (trow > kDirThreads) return 0;
+        const int rp = trow >= kDirThreads ? 1 : kDirThreads / trow;
+        const size_t s = (size_t)(FH * FW * IC * OC + 2 * rp * xs) * sizeof(float);  // W^T + 2 row-group buffers
+        return s > kDirSmemMax ? 0 : s;
+    }
+    const int tpp = (OC / 4) * FH;
+    if (tpp > kDirThreads) return 0;
+    const int acc4 = (FW * IC + 3) / 4;
+    const int nR4 = OW * OC / 4 + xs / 4;
+    const size_t s = (size_t)(kDirNB * nR4 * 4 + (size_t)tpp * (acc4 <= 3 ? 3 : 6) * 16) * sizeof(float);
+    return s > kDirSmemMax ? 0 : s;
+}
+
 bool direct_supported(int op, int IC, int OC, int FH, int FW, int OW, int sw) {
     if (op != CONV_OP_FWD && op != CONV_OP_BWD_FILTER) return false;
     if (IC > 8 || FH * FW * IC > kDirKMax || OW > kDirOWMax) return false;
-    if (op == CONV_OP_FWD && (OC / 4) * ((OW + kDirOWB - 1) / kDirOWB) > kDirThreads) return false;
     if (op == CONV_OP_BWD_FILTER) {
-        if (FW * IC > kDirDwFWIC || (OC / 4) * FH > kDirThreads) return false;
+        if (FW * IC > kDirDwFWIC) return false;
         const int WIN = (OW - 1) * sw + FW;
         if ((OW * OC / 4 + FH * WIN * IC / 4) * 16 * kDirNB > 150 * 1024) return false;  // cp.async ring
     }
-    (void)sw;
-    return true;
+    return direct_smem(op, IC, OC, FH, FW, OW, sw) != 0;
 }
 
 // dW blocks (= split-K partials summed by splitk_reduce_kernel)
@@ -291,15 +310,14 @@ int direct_launch(int op, const GenParams& g, int blocks, cudaStream_t st, char*
     p.out = g.out;
     p.rows_per_block = 0;
     size_t smem;
-    const int xs = p.FH * p.WIN * p.IC;
     if (op == CONV_OP_FWD) {
         p.X = g.A;
         p.W = g.B;
         const int trow = (p.OC / 4) * ((p.OW + kDirOWB - 1) / kDirOWB);
         const int rp = trow >= kDirThreads ? 1 : kDirThreads / trow;
-        smem = (size_t)(p.K * p.OC + 2 * rp * xs) * sizeof(float);  // W^T + 2 row-group buffers
-        if (trow > kDirThreads || smem > 200 * 1024) {
-            snprintf(err, errlen, "direct fwd: OC*OW too large (threads %d, smem %zu)", trow, smem);
+        smem = direct_smem(CONV_OP_FWD, p.IC, p.OC, p.FH, p.FW, p.OW, p.sw);
+        if (smem == 0) {
+            snprintf(err, errlen, "direct fwd: OC*OW too large (threads %d)", trow);
             return CONV_EUNSUPPORTED;
         }
         int grid = (p.N * p.OH + rp - 1) / rp;
@@ -315,10 +333,9 @@ int direct_launch(int op, const GenParams& g, int blocks, cudaStream_t st, char*
         p.rows_per_block = (p.N * p.OH + blocks - 1) / blocks;
         const int tpp = (p.OC / 4) * p.FH;
         const int acc4 = (p.FW * p.IC + 3) / 4;
-        const int nR4 = p.OW * p.OC / 4 + xs / 4;
-        smem = (size_t)(kDirNB * nR4 * 4 + (size_t)tpp * (acc4 <= 3 ? 3 : 6) * 16) * sizeof(float);
-        if (tpp > kDirThreads || smem > 200 * 1024) {
-            snprintf(err, errlen, "direct dw: OC*FH too large (threads %d, smem %zu)", tpp, smem);
+        smem = direct_smem(CONV_OP_BWD_FILTER, p.IC, p.OC, p.FH, p.FW, p.OW, p.sw);
+        if (smem == 0) {
+            snprintf(err, errlen, "direct dw: OC*FH too large (threads %d)", tpp);
             return CONV_EUNSUPPORTED;
         }
         if (acc4 <= 3) {

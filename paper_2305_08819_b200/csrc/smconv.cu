@@ -11,6 +11,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "../../include/smconv.h"
 #include "../../include/smconv_ext.h"
@@ -22,6 +23,7 @@ bool direct_supported(int op, int IC, int OC, int FH, int FW, int OW, int sw);
 int direct_dw_blocks(int N, int OH);
 int direct_launch(int op, const GenParams& g, int blocks, cudaStream_t st, char* err, size_t errlen);
 int tma_set_pair(int on);
+int tma_get_pair();
 bool dws_supported(int op, int IC, int OC, int FH, int FW, int sh, int sw, int OH, int OW);
 int dws_splits(int N, int OH, int OW, int* kb_per_split);
 int dws_launch(int planes, const GenParams& g, int splits, int kb_per_split, cudaStream_t st, char* err,
@@ -219,10 +221,50 @@ __global__ void __launch_bounds__(256) w2_build_kernel(const float* __restrict__
     }
 }
 
-int make_plan(int op, const Dims& d, int math, Plan& pl) {
-    read_env_once();
+int make_plan_uncached(int op, const Dims& d, int math, Plan& pl) {
     if (op == CONV_OP_BWD_DATA && make_plan_s2dx(d, math, pl) == 0) return CONV_OK;
     return make_plan_base(op, d, math, pl);
+}
+
+// Process-wide plan cache (SURVEY.md §8(b) contract 4): plans hold no pointers, so a plan is a pure
+// function of (op, the 11-int conv tuple, math, the forced variant, the CTA-pair switch).  Small-map
+// layers run ~10 us kernels; re-deriving the plan (tap tables, split choice) on every call is host
+// time on the critical path.  Guarded by a mutex (the library is reentrant across threads/streams).
+struct PlanKey {
+    int v[16];
+    bool operator==(const PlanKey& o) const { return memcmp(v, o.v, sizeof v) == 0; }
+};
+struct PlanKeyHash {
+    size_t operator()(const PlanKey& k) const {
+        uint64_t h = 1469598103934665603ull;
+        for (int x : k.v) h = (h ^ (uint32_t)x) * 1099511628211ull;
+        return (size_t)h;
+    }
+};
+std::mutex g_plan_mu;
+std::unordered_map<PlanKey, Plan, PlanKeyHash> g_plans;
+constexpr size_t kMaxPlans = 4096;
+
+int make_plan(int op, const Dims& d, int math, Plan& pl) {
+    read_env_once();
+    PlanKey k;
+    const int v[16] = {op, d.N, d.IH, d.IW, d.IC, d.OC, d.FH, d.FW, d.sh, d.sw, d.ph, d.pw, math,
+                       g_force[op].load(), tma_get_pair(), 0};
+    memcpy(k.v, v, sizeof v);
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        auto it = g_plans.find(k);
+        if (it != g_plans.end()) {
+            pl = it->second;
+            return CONV_OK;
+        }
+    }
+    const int rc = make_plan_uncached(op, d, math, pl);
+    if (rc) return rc;  // failures are not cached (their detail string is per call)
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    if (g_plans.size() >= kMaxPlans) g_plans.clear();
+    g_plans.emplace(k, pl);
+    return CONV_OK;
 }
 
 int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
@@ -234,6 +276,9 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
     pl.variant = forced == CONV_VARIANT_AUTO ? (tma_ok ? CONV_VARIANT_TMA : CONV_VARIANT_GENERIC) : forced;
     if (pl.variant == CONV_VARIANT_TMA && !tma_ok)
         return fail(CONV_EUNSUPPORTED, "%s: TMA variant forced but unsupported for this shape", op_name(op));
+    // STRIP serves fwd / dX only (strip_launch treats every non-fwd op as dX)
+    if (forced == CONV_VARIANT_STRIP && op == CONV_OP_BWD_FILTER)
+        return fail(CONV_EUNSUPPORTED, "%s: STRIP variant forced but it serves fwd / dX only", op_name(op));
     if (op != CONV_OP_BWD_FILTER && (forced == CONV_VARIANT_AUTO || forced == CONV_VARIANT_STRIP)) {
         const int bns = pick_bn(op == CONV_OP_FWD ? d.OC : d.IC);
         const bool strip_ok = strip_supported(op, d.N, d.IC, d.OC, d.FW, d.sh, d.sw, op == CONV_OP_FWD ? d.OW : d.IW,
@@ -491,7 +536,14 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
     g.B = B;
     g.out = pl.splits > 1 ? (float*)ws : out;
     g.Bx = nullptr;
-    cudaGetLastError();  // clear sticky-free earlier errors of the caller
+    // A launch error is detected with cudaGetLastError() after each launch; an error the caller left
+    // pending would be misattributed (and consumed) there, so refuse to enqueue and leave it in place.
+    {
+        const cudaError_t pend = cudaPeekAtLastError();
+        if (pend != cudaSuccess)
+            return fail(CONV_ECUDA, "%s: a CUDA error is pending from before this call (%s); not cleared, nothing "
+                        "enqueued", op_name(op), cudaGetErrorString(pend));
+    }
     if (pl.s2dx) {  // super-pixel stride-2 dX: the virtual fwd conv's filter W2, then its W' plane
         float* w2 = (float*)((char*)ws + pl.w2_off);
         const long long n = 16LL * d.IC * d.OC;

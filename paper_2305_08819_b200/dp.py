@@ -132,7 +132,7 @@ class ConvNetStep:
     """Buffers + one fwd/bwd pass of a conv-only network on this rank's batch shard."""
 
     def __init__(self, net: str, batch: int, device, math: str = "3xtf32", seed: int = 0,
-                 bucket_mb: float = 16.0, chain: bool = True):
+                 bucket_mb: float = 16.0, chain: bool = True, rank: int = 0):
         import torch
         self.torch = torch
         self.net = net
@@ -155,7 +155,9 @@ class ConvNetStep:
         offs = flat_offsets_backward(sizes)
         for i, l in enumerate(L):
             b = LayerBuf(l, x_src=xs[i], dy_src=ds[i], dy_share=sh[i])
-            X, Wt, dY = synth.torch_layer_inputs(l, batch, device, seed=seed * 1000 + i)
+            # W replicated (rank-independent seed); X / dY differ per rank's batch shard
+            X, Wt, dY = synth.torch_layer_inputs(l, batch, device, seed=seed * 1000 + i,
+                                                 act_seed=(seed * 1000 + i) * 65537 + 7 * rank + 1)
             b.W = Wt
             if b.x_src < 0:
                 b.X = X

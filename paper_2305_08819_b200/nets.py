@@ -139,15 +139,25 @@ def flops(layer: Layer, N: int, valid: bool = True) -> int:
     return 2 * N * pairs * layer.ic_logical * layer.OC
 
 
+def touched_rows(I: int, O: int, F: int, s: int, p: int) -> int:
+    """Input rows (or columns) some (output, tap) pair reads: a 1x1 stride-2 conv touches every
+    other row, a 3x3 stride-2 pad-1 conv all of them."""
+    return sum(1 for i in range(I) if any(0 <= (i + p - f) and (i + p - f) % s == 0 and (i + p - f) // s < O
+                                          for f in range(F)))
+
+
 def bytes_compulsory(layer: Layer, N: int, op: str) -> int:
-    """Compulsory fp32 bytes: each input read once, each output written once."""
-    x = N * layer.IH * layer.IW * layer.IC * 4
+    """Compulsory fp32 bytes: fwd X(touched) + W + Y; dX dY + W + dX (all of dX is
+    written, zeros included); dW X(touched) + dY + dW.  Each input read once, each output written once."""
+    x_all = N * layer.IH * layer.IW * layer.IC * 4
+    x = (N * touched_rows(layer.IH, layer.OH, layer.FH, layer.sh, layer.ph)
+         * touched_rows(layer.IW, layer.OW, layer.FW, layer.sw, layer.pw) * layer.IC * 4)
     y = N * layer.OH * layer.OW * layer.OC * 4
     w = layer.OC * layer.FH * layer.FW * layer.IC * 4
     if op == "fwd":
         return x + w + y
     if op == "dx":
-        return y + w + x
+        return y + w + x_all
     if op == "dw":
         return x + y + w
     raise ValueError(op)

@@ -154,6 +154,32 @@ def _need(t, name):
         raise ValueError("%s must be a contiguous float32 CUDA tensor" % name)
 
 
+def _same_device(*ts):
+    d = ts[0].device
+    for t in ts[1:]:
+        if t.device != d:
+            raise ValueError("all tensors must be on the same device (%s vs %s)" % (d, t.device))
+
+
+def _out(out, shape, like):
+    """Allocate the output, or check a caller-supplied one: the C ABI only sees dims derived from the
+    inputs, so a mis-shaped `out` would be written out of bounds."""
+    import torch
+    if out is None:
+        return torch.empty(shape, dtype=torch.float32, device=like.device)
+    _need(out, "out")
+    if tuple(out.shape) != tuple(shape):
+        raise ValueError("out has shape %s, expected %s" % (tuple(out.shape), tuple(shape)))
+    if out.device != like.device:
+        raise ValueError("out is on %s, inputs on %s" % (out.device, like.device))
+    return out
+
+
+def _rank4(t, name):
+    if t.dim() != 4:
+        raise ValueError("%s must be 4-D (got shape %s)" % (name, tuple(t.shape)))
+
+
 def raw_call(op, a_ptr, b_ptr, out_ptr, dims, math, ws_ptr, ws_bytes, stream_handle):
     """Direct C-ABI call with raw device pointers (ints) — used by bench.py's step."""
     f = (lib().conv2d_fwd, lib().conv2d_bwd_data, lib().conv2d_bwd_filter)[op]
@@ -166,11 +192,15 @@ def conv2d_fwd(x, w, stride=(1, 1), padding=(1, 1), math="3xtf32", out=None):
     import torch
     _need(x, "x")
     _need(w, "w")
+    _rank4(x, "x")
+    _rank4(w, "w")
+    _same_device(x, w)
     N, IH, IW, IC = x.shape
-    OC, FH, FW, _ = w.shape
+    OC, FH, FW, wic = w.shape
+    if wic != IC:
+        raise ValueError("w has %d input channels, x has %d" % (wic, IC))
     OH, OW = out_hw(IH, IW, FH, FW, stride, padding)
-    if out is None:
-        out = torch.empty((N, OH, OW, OC), dtype=torch.float32, device=x.device)
+    out = _out(out, (N, OH, OW, OC), x)
     dims = (N, IH, IW, IC, OC, FH, FW, stride[0], stride[1], padding[0], padding[1])
     m = _math(math)
     nb = workspace_bytes(CONV_OP_FWD, dims, m)
@@ -186,11 +216,15 @@ def conv2d_bwd_data(dy, w, input_hw, stride=(1, 1), padding=(1, 1), math="3xtf32
     import torch
     _need(dy, "dy")
     _need(w, "w")
+    _rank4(dy, "dy")
+    _rank4(w, "w")
+    _same_device(dy, w)
     N, OH, OW, OC = dy.shape
-    _, FH, FW, IC = w.shape
+    woc, FH, FW, IC = w.shape
+    if woc != OC:
+        raise ValueError("w has %d output channels, dy has %d" % (woc, OC))
     IH, IW = input_hw
-    if out is None:
-        out = torch.empty((N, IH, IW, IC), dtype=torch.float32, device=dy.device)
+    out = _out(out, (N, IH, IW, IC), dy)
     dims = (N, IH, IW, IC, OC, FH, FW, stride[0], stride[1], padding[0], padding[1])
     if out_hw(IH, IW, FH, FW, stride, padding) != (OH, OW):
         raise ValueError("dy extent %s does not match input_hw %s" % ((OH, OW), (IH, IW)))
@@ -208,11 +242,15 @@ def conv2d_bwd_filter(x, dy, kernel_hw, stride=(1, 1), padding=(1, 1), math="3xt
     import torch
     _need(x, "x")
     _need(dy, "dy")
+    _rank4(x, "x")
+    _rank4(dy, "dy")
+    _same_device(x, dy)
     N, IH, IW, IC = x.shape
-    _, OH, OW, OC = dy.shape
+    dn, OH, OW, OC = dy.shape
+    if dn != N:
+        raise ValueError("dy has batch %d, x has %d" % (dn, N))
     FH, FW = kernel_hw
-    if out is None:
-        out = torch.empty((OC, FH, FW, IC), dtype=torch.float32, device=x.device)
+    out = _out(out, (OC, FH, FW, IC), x)
     dims = (N, IH, IW, IC, OC, FH, FW, stride[0], stride[1], padding[0], padding[1])
     if out_hw(IH, IW, FH, FW, stride, padding) != (OH, OW):
         raise ValueError("dy extent does not match the forward output")

@@ -66,20 +66,28 @@ def layer_inputs(layer, N, config=0, layer_index=0, integer=0):
     return X, W, dY
 
 
-def torch_layer_inputs(layer, N, device, seed, dtype=None):
+def torch_layer_inputs(layer, N, device, seed, dtype=None, act_seed=None):
     """Device-side seeded draws with the same distributions (bench workloads too large for
     host generation).  Uses a torch.Generator on ``device``; the oracle sees these inputs only as
-    host copies in tests/test_fullsize_gpu.py (sampled outputs at the full bench size)."""
+    host copies in tests/test_fullsize_gpu.py (sampled outputs at the full bench size).
+
+    ``act_seed``: if given, X and dY come from their own generator seeded with it (data-parallel
+    ranks: the filters W are replicated -- same ``seed`` on every rank -- while each rank's batch
+    shard gets different activations)."""
     import torch
     gen = torch.Generator(device=device)
     gen.manual_seed(int(seed))
+    agen = gen
+    if act_seed is not None:
+        agen = torch.Generator(device=device)
+        agen.manual_seed(int(act_seed))
     f32 = torch.float32
     stem = layer.ic_logical < 4
     X = torch.empty((N, layer.IH, layer.IW, layer.IC), dtype=f32, device=device)
     if stem:
-        X.uniform_(0.0, 1.0, generator=gen)
+        X.uniform_(0.0, 1.0, generator=agen)
     else:
-        X.uniform_(-1.0, 1.0, generator=gen)
+        X.uniform_(-1.0, 1.0, generator=agen)
     if layer.ic_logical < layer.IC:
         X[..., layer.ic_logical:] = 0
     b = math.sqrt(6.0 / (layer.FH * layer.FW * layer.ic_logical))
@@ -88,5 +96,5 @@ def torch_layer_inputs(layer, N, device, seed, dtype=None):
     if layer.ic_logical < layer.IC:
         Wt[..., layer.ic_logical:] = 0
     dY = torch.empty((N, layer.OH, layer.OW, layer.OC), dtype=f32, device=device)
-    dY.uniform_(-1.0, 1.0, generator=gen)
+    dY.uniform_(-1.0, 1.0, generator=agen)
     return X, Wt, dY

@@ -142,3 +142,56 @@ def test_force_variant(sm):
     sm.force_variant(0, sm.CONV_VARIANT_AUTO)
     with pytest.raises(sm.ConvError):
         sm.force_variant(5, 0)
+
+
+VARIANT_NAMES = {1: "generic", 2: "tma", 3: "strip", 4: "direct", 5: "dws"}
+
+
+@pytest.mark.parametrize("op", [0, 1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5])
+def test_forced_variant_is_served_or_refused(sm, op, variant):
+    """Forcing a variant either yields a plan of THAT variant or CONV_EUNSUPPORTED -- never a plan whose
+    launch would write the wrong buffer extent (e.g. STRIP forced for dW)."""
+    shapes = [(32, 32, 32, 64, 64, 3, 3, 1, 1, 1, 1), (4, 32, 32, 4, 64, 3, 3, 1, 1, 1, 1),
+              (32, 8, 8, 128, 256, 3, 3, 2, 2, 1, 1), (3, 7, 9, 20, 36, 3, 3, 1, 1, 1, 1)]
+    sm.force_variant(op, variant)
+    try:
+        for s in shapes:
+            try:
+                d = sm.plan_describe(op, s, 0)
+            except sm.ConvError as e:
+                assert e.code == sm.CONV_EUNSUPPORTED, (s, e)
+                continue
+            assert d.startswith("variant=" + VARIANT_NAMES[variant]), (s, d)
+            assert not (variant == 3 and op == 2)
+    finally:
+        sm.force_variant(op, 0)
+
+
+def test_direct_only_when_launch_fits(sm):
+    """AUTO must not pick DIRECT for shapes whose launch would exceed its shared memory (the launch would
+    then return CONV_EUNSUPPORTED for a valid call)."""
+    assert "direct" not in sm.plan_describe(0, (8, 8, 8, 8, 1024, 3, 3, 1, 1, 1, 1), 0)
+    assert "direct" not in sm.plan_describe(2, (2048, 32, 32, 8, 256, 3, 3, 1, 1, 1, 1), 0)
+    assert "direct" in sm.plan_describe(0, (4096, 32, 32, 4, 64, 3, 3, 1, 1, 1, 1), 0)  # the stem still is
+
+
+def test_plan_cache_tracks_forced_variant(sm):
+    s = (32, 8, 8, 256, 256, 3, 3, 1, 1, 1, 1)
+    a = sm.plan_describe(0, s, 0)
+    sm.force_variant(0, 1)
+    try:
+        assert sm.plan_describe(0, s, 0).startswith("variant=generic")
+    finally:
+        sm.force_variant(0, 0)
+    assert sm.plan_describe(0, s, 0) == a
+
+
+def test_binding_cross_checks_shapes(sm):
+    """The torch wrappers check every tensor against the others before calling the C ABI (shape /
+    channel mismatch -> error, SPEC conv2d_*); CPU tensors are refused (no CPU fallback)."""
+    import torch
+    x = torch.zeros((2, 8, 8, 4))
+    w = torch.zeros((8, 3, 3, 4))
+    with pytest.raises(ValueError):
+        sm.conv2d_fwd(x, w)

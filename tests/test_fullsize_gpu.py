@@ -47,7 +47,7 @@ def _nw(got, ref):
 
 @pytest.mark.parametrize("math", ["3xtf32", "tf32"])
 @pytest.mark.parametrize("il", _layers(), ids=lambda il: il[1].name)
-def test_resnet18_layer_full_batch(env, il, math):
+def test_resnet18_layer_full_batch(env, il, math, parity_log):
     torch, oracle, sm, nets = env
     i, l = il
     from paper_2305_08819_b200 import synth
@@ -60,15 +60,28 @@ def test_resnet18_layer_full_batch(env, il, math):
     torch.cuda.synchronize()
     Wh = W.cpu().numpy()
 
+    m = sm.MATH[math]
+
+    def log(op, e, cov):
+        parity_log.append({"config": "resnet18-b%d" % B, "layer": l.name, "op": op, "math": math,
+                           "check": "random", "coverage": cov, "normwise": e, "tol": TOL[math],
+                           "plan": sm.plan_describe({"fwd": 0, "dx": 1, "dw": 2}[op], l.dims(B), m)})
+
     # fwd / dX on whole sampled images
+    ef, ed = 0.0, 0.0
     for n in (0, B // 2 + 7, B - 1):
         ref = oracle.conv2d_fwd(X[n:n + 1].cpu().numpy(), Wh, st, pd)
         e = _nw(y[n:n + 1].cpu().numpy(), ref)
+        ef = max(ef, e)
         assert e <= TOL[math], ("fwd", n, e)
         if dx is not None:
             ref = oracle.conv2d_bwd_data(dY[n:n + 1].cpu().numpy(), Wh, (l.IH, l.IW), st, pd)
             e = _nw(dx[n:n + 1].cpu().numpy(), ref)
+            ed = max(ed, e)
             assert e <= TOL[math], ("dx", n, e)
+    log("fwd", ef, "3 whole images")
+    if dx is not None:
+        log("dx", ed, "3 whole images")
 
     # dW entries over the full batch
     g = np.random.default_rng(77 + i)
@@ -77,6 +90,7 @@ def test_resnet18_layer_full_batch(env, il, math):
     got = dw.reshape(-1)[torch.from_numpy(idx).to(dev)].double().cpu().numpy()
     scale = float(dw.abs().max())
     e = float(np.max(np.abs(got - ref))) / scale
+    log("dw", e, "%d dW entries over the full batch" % len(idx))
     assert e <= TOL[math], ("dw", e)
 
     # adjoint identity over the whole tensors (fp64 reductions on the device); the scale is the
