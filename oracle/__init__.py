@@ -26,16 +26,16 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "conv_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "net_oracle.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc -O2 -fopenmp (plain C, no vectorisation tricks needed)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(f) for f in _SRCS):
         tmp = _LIB + ".tmp%d" % os.getpid()
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c99",
-                               _SRC, "-o", tmp])
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c99"] + _SRCS + ["-o", tmp])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -59,6 +59,15 @@ def _load():
         lib.oracle_out_hw.argtypes = [ctypes.c_int] * 8 + [ctypes.POINTER(ctypes.c_int)] * 2
         lib.oracle_out_hw.restype = ctypes.c_int
         lib.oracle_num_threads.restype = ctypes.c_int
+        I, LL, D = ctypes.c_int, ctypes.c_longlong, ctypes.c_double
+        lib.oracle_matmul.argtypes = [fp, fp, dp, I, I, I, I, I]
+        lib.oracle_matmul.restype = I
+        lib.oracle_channel_stats.argtypes = [dp, LL, I, dp, dp]
+        lib.oracle_channel_stats.restype = I
+        lib.oracle_leaky_relu.argtypes = [dp, dp, LL, D]
+        lib.oracle_leaky_relu.restype = I
+        lib.oracle_leaky_bwd_stats.argtypes = [dp, fp, LL, I, D, dp, dp, dp]
+        lib.oracle_leaky_bwd_stats.restype = I
         lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
         _lib = lib
     return _lib
@@ -160,3 +169,60 @@ def num_threads() -> int:
 
 def set_num_threads(n: int) -> None:
     _load().oracle_set_num_threads(int(n))
+
+
+# ---------------------------------------------------------------- net_oracle.c
+def _f64(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def matmul(A, B, ta=False, tb=False):
+    """C = op(A) . op(B) in float64 (net_oracle.c oracle_matmul).  A is [M,K] ([K,M] if ta: matMulT1),
+    B is [K,N] ([N,K] if tb: matMulT2)."""
+    A, ap = _f32(A)
+    B, bp = _f32(B)
+    M, K = (A.shape[1], A.shape[0]) if ta else A.shape
+    N, K2 = (B.shape[0], B.shape[1]) if tb else (B.shape[1], B.shape[0])
+    if K != K2:
+        raise ValueError("inner dimensions differ: %d vs %d" % (K, K2))
+    C = np.empty((M, N), np.float64)
+    if _load().oracle_matmul(ap, bp, C.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), M, N, K, int(ta), int(tb)):
+        raise ValueError("oracle_matmul: bad arguments")
+    return C
+
+
+def channel_stats(Y):
+    """(sum, sum of squares) per channel (last axis) over all other axes, float64."""
+    Y, yp = _f64(Y)
+    C = Y.shape[-1]
+    rows = Y.size // C
+    s1, s2 = np.empty(C), np.empty(C)
+    if _load().oracle_channel_stats(yp, rows, C, s1.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                    s2.ctypes.data_as(ctypes.POINTER(ctypes.c_double))):
+        raise ValueError("oracle_channel_stats: bad arguments")
+    return s1, s2
+
+
+def leaky_relu(X, k=0.01):
+    X, xp = _f64(X)
+    Y = np.empty_like(X)
+    if _load().oracle_leaky_relu(xp, Y.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), X.size, float(k)):
+        raise ValueError("oracle_leaky_relu: bad arguments")
+    return Y
+
+
+def leaky_bwd_stats(dA, A, k=0.01):
+    """(G, S1, S2): G = dA * leaky'(A) (from the output A), S1 = sum G, S2 = sum G * leaky^-1(A) per channel."""
+    dA, dap = _f64(dA)
+    A, ap = _f32(A)
+    assert dA.shape == A.shape
+    C = A.shape[-1]
+    rows = A.size // C
+    G = np.empty_like(dA)
+    s1, s2 = np.empty(C), np.empty(C)
+    dp = ctypes.POINTER(ctypes.c_double)
+    if _load().oracle_leaky_bwd_stats(dap, ap, rows, C, float(k), G.ctypes.data_as(dp), s1.ctypes.data_as(dp),
+                                      s2.ctypes.data_as(dp)):
+        raise ValueError("oracle_leaky_bwd_stats: bad arguments")
+    return G, s1, s2

@@ -15,6 +15,7 @@
 
 #include "../../include/smconv.h"
 #include "../../include/smconv_ext.h"
+#include "../../include/smgemm.h"
 #include "conv_gen.cuh"
 #include "conv_strip.cuh"
 
@@ -69,9 +70,40 @@ struct Dims {
     int N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw, OH, OW;
 };
 
+thread_local const char* g_api_name = nullptr;  // the GEMM entry points report their own name
+
 const char* op_name(int op) {
+    if (g_api_name) return g_api_name;
     return op == CONV_OP_FWD ? "conv2d_fwd" : op == CONV_OP_BWD_DATA ? "conv2d_bwd_data" : "conv2d_bwd_filter";
 }
+
+// The paper's matrix-multiply operators as 1x1 convolutions on a 1x1 map (H = W = 1; the
+// "pixels" are the matrix rows), so they run on the same tcgen05 mainloops, plans and epilogues:
+//   matMul   C[M,N] = A[M,K] . B[K,N]    = conv2d_bwd_data  (dY = A, W = B as [OC=K][IC=N])
+//   matMulT1 C[M,N] = A[K,M]^T . B[K,N]  = conv2d_bwd_filter(X = B [K][N], dY = A [K][M])
+//   matMulT2 C[M,N] = A[M,K] . B[N,K]^T  = conv2d_fwd       (X = A [M][K], W = B [OC=N][IC=K])
+struct GemmMap {
+    int op;
+    int dims[11];
+};
+GemmMap gemm_map(int g, int M, int N, int K) {
+    GemmMap m;
+    if (g == 0) {
+        m.op = CONV_OP_BWD_DATA;
+        const int d[11] = {M, 1, 1, N, K, 1, 1, 1, 1, 0, 0};
+        memcpy(m.dims, d, sizeof d);
+    } else if (g == 1) {
+        m.op = CONV_OP_BWD_FILTER;
+        const int d[11] = {K, 1, 1, N, M, 1, 1, 1, 1, 0, 0};
+        memcpy(m.dims, d, sizeof d);
+    } else {
+        m.op = CONV_OP_FWD;
+        const int d[11] = {M, 1, 1, K, N, 1, 1, 1, 1, 0, 0};
+        memcpy(m.dims, d, sizeof d);
+    }
+    return m;
+}
+const char* gemm_name(int g) { return g == 0 ? "matMul" : g == 1 ? "matMulT1" : "matMulT2"; }
 
 int check_dims(int op, Dims& d, int math) {
     const char* f = (op >= 0 && op < 3) ? op_name(op) : "conv2d";
@@ -134,6 +166,7 @@ int pick_bn(int n) {
 // Largest number of k-blocks (x32 reduction elements) one accumulator chain sums before
 // its partial is written out (split-K); bounds TMEM accumulation error.
 constexpr int kMaxKbPerChain = 256;
+constexpr int kGenMaxKbPerChain3x = 16;  // GENERIC 3xTF32 (no chunked promotion)
 constexpr int kSMs = 148;
 
 void fill_common(GenParams& g, const Dims& d) {
@@ -408,7 +441,13 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
     } else if (pl.variant == CONV_VARIANT_DWS) {
         splits = dws_splits(d.N, d.OH, d.OW, &g.kb_per_split);
     } else if (op == CONV_OP_BWD_FILTER) {
-        const int need_prec = (nkb_est + kMaxKbPerChain - 1) / kMaxKbPerChain;
+        // GENERIC accumulates its whole chain in TMEM (no chunked promotion) and tcgen05 adds by
+        // truncation, so its 3xTF32 chains are capped at 16 k-blocks (512 products): GoogLeNet b256
+        // stem dW with 111-k-block chains measured 1.77e-5 normwise (r02a); a numpy model of the
+        // truncating chain gives 1.1e-5 / 4.8e-6 / 3.1e-6 at 1024 / 512 / 256 products (K = 262144)
+        const int max_chain = (pl.variant == CONV_VARIANT_GENERIC && pl.planes == 2) ? kGenMaxKbPerChain3x
+                                                                                     : kMaxKbPerChain;
+        const int need_prec = (nkb_est + max_chain - 1) / max_chain;
         int fill = kSMs / tiles;
         if (fill < 1) fill = 1;
         splits = need_prec > fill ? need_prec : fill;
@@ -421,6 +460,13 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
         const int maxs = nkb_est / 4 > 1 ? nkb_est / 4 : 1;
         if (splits > maxs) splits = maxs;
         if (splits < 1) splits = 1;
+    }
+    if (pl.variant == CONV_VARIANT_GENERIC && pl.planes == 2 && op != CONV_OP_BWD_FILTER) {
+        // the same chain cap for GENERIC fwd / dX (worst-case tile: every tap valid)
+        const int srcC = op == CONV_OP_FWD ? d.IC : d.OC;
+        const int kb_max = (d.FH * d.FW * srcC + 31) / 32;
+        const int need = (kb_max + kGenMaxKbPerChain3x - 1) / kGenMaxKbPerChain3x;
+        if (splits < need) splits = need;
     }
     g.splits = splits;
     pl.splits = splits;
@@ -691,6 +737,69 @@ const char* conv2d_strerror(int code) {
 }
 
 const char* conv2d_last_error_detail(void) { return g_detail; }
+
+// ---------------------------------------------------------------- GEMM (include/smgemm.h)
+static int gemm_check(int g, int M, int N, int K) {
+    const char* f = gemm_name(g);
+    if (M < 1 || N < 1 || K < 1) return fail(CONV_EARG, "%s: M=%d N=%d K=%d must be >= 1", f, M, N, K);
+    const int r0 = g == 1 ? M : K;  // row lengths: matMul A[M][K], B[K][N]; T1 A[K][M]; T2 A[M][K], B[N][K]
+    if (r0 % 4 || N % 4 || (g == 2 && K % 4))
+        return fail(CONV_EALIGN, "%s: the row lengths (%s=%d, N=%d) must be multiples of 4 (PAPER.md:115)", f,
+                    g == 1 ? "M" : "K", r0, N);
+    return CONV_OK;
+}
+
+static int gemm_entry(int g, const float* A, const float* B, float* C, int M, int N, int K, int math, void* ws,
+                      size_t ws_bytes, conv_stream_t st) {
+    int rc = gemm_check(g, M, N, K);
+    if (rc) return rc;
+    g_api_name = gemm_name(g);
+    {
+        const GemmMap m = gemm_map(g, M, N, K);
+        const int* d = m.dims;
+        Dims dd = mk(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], d[8], d[9], d[10]);
+        if (m.op == CONV_OP_FWD) rc = entry(m.op, A, B, C, dd, math, ws, ws_bytes, st);
+        else if (m.op == CONV_OP_BWD_DATA) rc = entry(m.op, A, B, C, dd, math, ws, ws_bytes, st);
+        else rc = entry(m.op, B, A, C, dd, math, ws, ws_bytes, st);  // dW(X = B, dY = A)
+    }
+    g_api_name = nullptr;
+    return rc;
+}
+
+size_t gemm_workspace_bytes(int g, int M, int N, int K, int math) {
+    if (g < 0 || g > 2 || gemm_check(g, M, N, K)) return (size_t)-1;
+    const GemmMap m = gemm_map(g, M, N, K);
+    const int* d = m.dims;
+    return conv2d_workspace_bytes(m.op, d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], d[8], d[9], d[10], math);
+}
+
+int gemm_matmul(const float* A, const float* B, float* C, int M, int N, int K, int math, void* ws, size_t ws_bytes,
+                conv_stream_t st) {
+    return gemm_entry(0, A, B, C, M, N, K, math, ws, ws_bytes, st);
+}
+
+int gemm_matmul_t1(const float* A, const float* B, float* C, int M, int N, int K, int math, void* ws,
+                   size_t ws_bytes, conv_stream_t st) {
+    return gemm_entry(1, A, B, C, M, N, K, math, ws, ws_bytes, st);
+}
+
+int gemm_matmul_t2(const float* A, const float* B, float* C, int M, int N, int K, int math, void* ws,
+                   size_t ws_bytes, conv_stream_t st) {
+    return gemm_entry(2, A, B, C, M, N, K, math, ws, ws_bytes, st);
+}
+
+int gemm_plan_describe(int g, int M, int N, int K, int math, char* buf, size_t len) {
+    if (g < 0 || g > 2) return fail(CONV_EARG, "gemm_plan_describe: unknown gemm op %d", g);
+    int rc = gemm_check(g, M, N, K);
+    if (rc) return rc;
+    const GemmMap m = gemm_map(g, M, N, K);
+    const int* d = m.dims;
+    g_api_name = gemm_name(g);
+    rc = conv2d_plan_describe(m.op, d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], d[8], d[9], d[10], math, buf,
+                              len);
+    g_api_name = nullptr;
+    return rc;
+}
 
 int smconv_set_pair(int on) { return tma_set_pair(on ? 1 : 0); }
 

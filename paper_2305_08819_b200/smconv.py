@@ -23,6 +23,7 @@ MATH = {"3xtf32": CONV_MATH_FP32_3XTF32, "fp32": CONV_MATH_FP32_3XTF32, "tf32": 
 
 EXPORTS = ("conv2d_out_hw", "conv2d_workspace_bytes", "conv2d_fwd", "conv2d_bwd_data", "conv2d_bwd_filter",
            "conv2d_strerror", "conv2d_last_error_detail")
+GEMM_EXPORTS = ("gemm_workspace_bytes", "gemm_matmul", "gemm_matmul_t1", "gemm_matmul_t2", "gemm_plan_describe")
 EXT_EXPORTS = ("conv2d_force_variant", "conv2d_plan_describe", "conv2d_plan_kernels", "smconv_selftest_host",
                "smconv_probe_tf32")
 
@@ -71,6 +72,14 @@ def lib():
                 L.conv2d_plan_kernels.restype = I
                 L.smconv_selftest_host.argtypes = []
                 L.smconv_selftest_host.restype = I
+                L.gemm_workspace_bytes.argtypes = [I] * 5
+                L.gemm_workspace_bytes.restype = Z
+                for f in ("gemm_matmul", "gemm_matmul_t1", "gemm_matmul_t2"):
+                    fn = getattr(L, f)
+                    fn.argtypes = [P, P, P, I, I, I, I, P, Z, P]
+                    fn.restype = I
+                L.gemm_plan_describe.argtypes = [I] * 5 + [ctypes.c_char_p, Z]
+                L.gemm_plan_describe.restype = I
                 L.smconv_probe_tf32.argtypes = [P]
                 L.smconv_probe_tf32.restype = I
                 _lib = L
@@ -261,6 +270,72 @@ def conv2d_bwd_filter(x, dy, kernel_hw, stride=(1, 1), padding=(1, 1), math="3xt
     _check(lib().conv2d_bwd_filter(_ptr(x), _ptr(dy), _ptr(out), *dims, m, _ptr(ws) if ws is not None else None, nb,
                                    ctypes.c_void_p(st)))
     return out
+
+
+# ------------------------------------------------------------------ GEMM (include/smgemm.h)
+GEMM_MATMUL, GEMM_MATMUL_T1, GEMM_MATMUL_T2 = 0, 1, 2
+
+
+def gemm_workspace_bytes(g, M, N, K, math=CONV_MATH_FP32_3XTF32):
+    n = lib().gemm_workspace_bytes(g, M, N, K, _math(math))
+    if n == ctypes.c_size_t(-1).value:
+        raise ConvError(CONV_EARG, "gemm_workspace_bytes: invalid arguments (M=%d N=%d K=%d)" % (M, N, K))
+    return n
+
+
+def gemm_plan_describe(g, M, N, K, math=CONV_MATH_FP32_3XTF32):
+    buf = ctypes.create_string_buffer(256)
+    _check(lib().gemm_plan_describe(g, M, N, K, _math(math), buf, 256))
+    return buf.value.decode()
+
+
+def _gemm(g, a, b, M, N, K, math, out):
+    import torch
+    _same_device(a, b)
+    out = _out(out, (M, N), a)
+    m = _math(math)
+    nb = gemm_workspace_bytes(g, M, N, K, m)
+    ws = _workspace(nb, a.device)
+    st = torch.cuda.current_stream(a.device).cuda_stream
+    f = (lib().gemm_matmul, lib().gemm_matmul_t1, lib().gemm_matmul_t2)[g]
+    _check(f(_ptr(a), _ptr(b), _ptr(out), M, N, K, m, _ptr(ws) if ws is not None else None, nb, ctypes.c_void_p(st)))
+    return out
+
+
+def _mat(t, name):
+    _need(t, name)
+    if t.dim() != 2:
+        raise ValueError("%s must be 2-D (got shape %s)" % (name, tuple(t.shape)))
+
+
+def matmul(a, b, math="3xtf32", out=None):
+    """C[M,N] = A[M,K] . B[K,N]  (matMul, include/smgemm.h)."""
+    _mat(a, "a")
+    _mat(b, "b")
+    (M, K), (K2, N) = a.shape, b.shape
+    if K != K2:
+        raise ValueError("inner dimensions differ: a %s, b %s" % (tuple(a.shape), tuple(b.shape)))
+    return _gemm(GEMM_MATMUL, a, b, M, N, K, math, out)
+
+
+def matmul_t1(a, b, math="3xtf32", out=None):
+    """C[M,N] = A[K,M]^T . B[K,N]  (matMulT1, Fig. 3)."""
+    _mat(a, "a")
+    _mat(b, "b")
+    (K, M), (K2, N) = a.shape, b.shape
+    if K != K2:
+        raise ValueError("inner dimensions differ: a %s, b %s" % (tuple(a.shape), tuple(b.shape)))
+    return _gemm(GEMM_MATMUL_T1, a, b, M, N, K, math, out)
+
+
+def matmul_t2(a, b, math="3xtf32", out=None):
+    """C[M,N] = A[M,K] . B[N,K]^T  (matMulT2)."""
+    _mat(a, "a")
+    _mat(b, "b")
+    (M, K), (N, K2) = a.shape, b.shape
+    if K != K2:
+        raise ValueError("inner dimensions differ: a %s, b %s" % (tuple(a.shape), tuple(b.shape)))
+    return _gemm(GEMM_MATMUL_T2, a, b, M, N, K, math, out)
 
 
 def probe_tf32():

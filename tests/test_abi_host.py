@@ -21,7 +21,7 @@ def sm():
 
 def _declared():
     names = []
-    for h in ("smconv.h", "smconv_ext.h"):
+    for h in ("smconv.h", "smconv_ext.h", "smgemm.h"):
         src = open(os.path.join(ROOT, "include", h)).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
         names += re.findall(r"^\s*(?:const\s+)?\w+\**\s+\**(\w+)\s*\(", src, flags=re.M)
@@ -35,7 +35,7 @@ def test_exports_every_declared_symbol(sm):
     L = ctypes.CDLL(sm.LIB_PATH)
     for n in names:
         assert hasattr(L, n), n
-    assert set(sm.EXPORTS + sm.EXT_EXPORTS) <= set(names)
+    assert set(sm.EXPORTS + sm.EXT_EXPORTS + sm.GEMM_EXPORTS) <= set(names)
 
 
 def test_library_is_sm100a(sm):
@@ -195,3 +195,20 @@ def test_binding_cross_checks_shapes(sm):
     w = torch.zeros((8, 3, 3, 4))
     with pytest.raises(ValueError):
         sm.conv2d_fwd(x, w)
+
+
+def test_gemm_host_validation(sm):
+    """GEMM entry points: plans map onto the 1x1 conv variants; row lengths must be multiples of 4
+     and dims positive -- rejected on the host with the gemm name in the detail."""
+    assert "variant=" in sm.gemm_plan_describe(0, 4096, 256, 512)
+    assert "variant=" in sm.gemm_plan_describe(1, 256, 512, 4096)
+    assert "variant=" in sm.gemm_plan_describe(2, 4096, 256, 512)
+    with pytest.raises(sm.ConvError) as e:
+        sm.gemm_plan_describe(0, 8, 6, 8)  # N % 4 != 0
+    assert e.value.code == sm.CONV_EALIGN and "matMul" in e.value.detail
+    with pytest.raises(sm.ConvError) as e:
+        sm.gemm_workspace_bytes(2, 8, 8, 0)
+    assert e.value.code == sm.CONV_EARG
+    L = sm.lib()
+    rc = L.gemm_matmul_t1(None, None, None, 8, 8, 8, 0, None, 0, None)
+    assert rc == sm.CONV_EARG and b"matMulT1" in L.conv2d_last_error_detail()
