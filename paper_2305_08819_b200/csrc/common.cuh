@@ -255,6 +255,19 @@ SMCONV_DEV uint32_t cluster_ctarank() {
     return r;
 }
 
+// 16-byte load from the shared memory of CTA `cta` of this cluster at the offset of local address `la`
+SMCONV_DEV float4 ld_cluster_f4(uint32_t la, uint32_t cta) {
+    float4 v;
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %4, %5;\n\t"
+        "ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [ra];\n\t}"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "r"(la), "r"(cta)
+        : "memory");
+    return v;
+}
+
 SMCONV_DEV void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }

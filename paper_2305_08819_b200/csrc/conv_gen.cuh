@@ -64,6 +64,9 @@ struct GenParams {
     // super-pixel stride-2 dX run as a fwd conv (smconv.cu "s2dx"): output row (n, i', j') and
     // column (pi, pj, ic) go to dX[n, 2i'-2+pi, 2j'-2+pj, ic] (rows / columns i' = 0 / j' = 0 dropped)
     int s2dx, s2_IH, s2_IW, s2_IC;
+    // TMA fwd / dX: split-K inside a thread-block cluster of csk CTAs (0 = off): the partial tiles are
+    // summed through distributed shared memory instead of an HBM workspace + reduce kernel
+    int csk;
 };
 
 template <int OP, int BN, int PLANES>

@@ -78,7 +78,11 @@ int launch_t(const TmaParams& tp, const GenParams& g, dim3 grid, cudaStream_t st
         }
         attr_done.fetch_or(bit);
     }
-    if (PAIR) {  // 2-CTA clusters: one M = 256 tile per pair
+    if (PAIR || tp.csk) {  // 2-CTA clusters: one M = 256 tile per pair; csk-CTA clusters: split-K
+        if (tp.csk && !C::CSK_FITS) {
+            snprintf(err, errlen, "tma csk: partial tile does not fit the stage ring");
+            return CONV_EUNSUPPORTED;
+        }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = grid;
         cfg.blockDim = dim3(C::NTHREADS, 1, 1);
@@ -86,14 +90,14 @@ int launch_t(const TmaParams& tp, const GenParams& g, dim3 grid, cudaStream_t st
         cfg.stream = st;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.x = PAIR ? 2 : tp.csk;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
         const cudaError_t e = cudaLaunchKernelEx(&cfg, conv_tma_kernel<OP, BN, PLANES, PAIR>, tp, g);
         if (e != cudaSuccess) {
-            snprintf(err, errlen, "cudaLaunchKernelEx(tma pair): %s", cudaGetErrorString(e));
+            snprintf(err, errlen, "cudaLaunchKernelEx(tma cluster %d): %s", PAIR ? 2 : tp.csk, cudaGetErrorString(e));
             return CONV_ECUDA;
         }
         return CONV_OK;
@@ -173,7 +177,7 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
     }
     // CTA pairs (cta_group::2): fwd / dx in 3xTF32 when 256-row pair tiles (two 128-image blocks at
     // one position) tile every phase exactly; dW (not transposed) when OC is a multiple of 256
-    const int pair_mode = g_pair.load();
+    const int pair_mode = g.csk ? 0 : g_pair.load();  // cluster split-K tiles are 1-CTA MMAs
     if (op == CONV_OP_BWD_FILTER && !g.dwt && planes == 2 && pair_mode && g_dw_pair && BN == 128 && g.OC % 256 == 0 &&
         tp.m_tiles % 2 == 0) {
         tp.pair = 1;
@@ -200,6 +204,11 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
             const int pairs = tp.work < 74 ? tp.work : 74;
             grid = dim3(2 * pairs, 1, 1);
         }
+    }
+    if (g.csk && (op == CONV_OP_FWD || op == CONV_OP_BWD_DATA)) {
+        // one work item per CTA; the csk splits of a tile form one cluster (TileInfo::init)
+        tp.csk = g.csk;
+        grid = dim3(tp.work, 1, 1);
     }
     if (op == CONV_OP_FWD || op == CONV_OP_BWD_DATA) {
     } else {

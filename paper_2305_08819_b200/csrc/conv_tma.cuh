@@ -58,6 +58,8 @@ struct __align__(64) TmaParams {
                        // k-blocks whose source pixels are all padding are skipped
     int m_tiles, n_tiles;  // work decomposition (dx: m_tiles over all phases)
     int work;        // m_tiles * splits * n_tiles
+    int csk;         // fwd / dx: cluster split-K (GenParams::csk): one work item per CTA, the csk splits of a
+                     // tile are the CTAs of one cluster, partials reduced through DSMEM (csk_reduce)
 };
 
 template <int OP, int BN, int PLANES, bool PAIR = false>
@@ -96,6 +98,10 @@ struct TmaCfg {
     static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128 : ACC_COLS <= 256 ? 256 : 512;
     static constexpr int AUX_BYTES = 1024 + kMaxTaps * 16;
     static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + AUX_BYTES;
+    // cluster split-K partial [128 rows][BN + 4] fp32 in the (drained) stage ring; +4 floats per row
+    // keep a quarter-warp's 16-B row stores on distinct banks
+    static constexpr int PSTRIDE = BN + 4;
+    static constexpr bool CSK_FITS = 128 * PSTRIDE * 4 <= STAGES * STAGE_BYTES;
     static_assert(STAGES >= 2, "stage does not fit");
     static_assert(PLANES == 1 || BN <= 128, "3xTF32 promotion keeps BN/2 fp32 per epilogue thread");
     static_assert(!PAIR || (PLANES == 2 && OP != OP_DWT && BN >= 64), "CTA pairs: fwd / dx / dW, 3xTF32");
@@ -149,10 +155,16 @@ struct TileInfo {
     int vr_lo, vr_hi, vc_lo, vc_hi;  // dw single-tap tiles: output rows / cols whose source is in range
 
     SMCONV_DEV void init(const TmaParams& tp, const GenParams& p, int w, int rank = 0) {
-        const int nt = w % tp.n_tiles;
-        const int rest = w / tp.n_tiles;
+        int nt = w % tp.n_tiles;
+        int rest = w / tp.n_tiles;
         int mt;
-        if (OP == OP_DW || OP == OP_DWT) {
+        if (OP != OP_DW && OP != OP_DWT && tp.csk) {
+            // cluster split-K: the splits of one tile are consecutive CTAs (one cluster)
+            split = w % tp.csk;
+            const int tile = w / tp.csk;
+            nt = tile % tp.n_tiles;
+            mt = tile / tp.n_tiles;
+        } else if (OP == OP_DW || OP == OP_DWT) {
             // split (pixel range) outermost: all (m, n) tiles of one pixel range run together, so
             // that range's dY and X are read from HBM once and re-used from L2 by every tile
             // (m-tile-major order re-read them once per m-tile: 11.3 GB vs 2.1 GB compulsory, l1)
@@ -674,7 +686,10 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             }
             // 4 consecutive GEMM columns of this thread's row -> output
             auto st4 = [&](int col, float x, float y, float z, float w4) {
-                if (OP == OP_DWT) {  // column = oc: a warp's 32 rows are 128 contiguous bytes per column
+                if (!C::IS_DW && tp.csk) {  // cluster split-K: this CTA's partial -> own shared memory
+                    *reinterpret_cast<float4*>(tiles_ptr + ((size_t)row * C::PSTRIDE + (col - n0)) * 4) =
+                        make_float4(x, y, z, w4);
+                } else if (OP == OP_DWT) {  // column = oc: a warp's 32 rows are 128 contiguous bytes per column
                     float* o = outp + obase + (long long)col * p.M;
                     o[0] = x;
                     o[p.M] = y;
@@ -758,6 +773,43 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
 
     tc_fence_before();
     __syncthreads();
+    if (!C::IS_DW && !PAIR && tp.csk) {
+        // cluster split-K: every CTA of the cluster holds its partial of the same tile in shared memory
+        // [128 rows][PSTRIDE]; CTA r sums rows [r*128/S, (r+1)*128/S) over the S partials in rank order
+        // (fixed order: deterministic) and writes them.  One warp per row: 512-B / 1-KB row runs.
+        cluster_sync_all();  // release / acquire at cluster scope: all partials visible
+        const int S = tp.csk, crank = (int)cluster_ctarank();
+        TileInfo<OP> ti;
+        ti.init(tp, p, blockIdx.x, 0);
+        const int rows_per = 128 / S, n0 = ti.n0 * BN;
+        constexpr int NW = C::NTHREADS / 32, C4 = BN / 4;
+        for (int rr = crank * rows_per + warp; rr < (crank + 1) * rows_per; rr += NW) {
+            const RowInfo ri = row_info<OP>(p, ti.phase, ti.m0 + rr);
+            if (!ri.ok) continue;
+            float* orow = p.out + (long long)ri.orow * p.Ngemm;
+#pragma unroll
+            for (int c4 = lane; c4 < C4; c4 += 32) {
+                const int col = n0 + 4 * c4;
+                if (col >= p.Ngemm) continue;
+                const uint32_t la = tiles_addr + (uint32_t)((rr * C::PSTRIDE + 4 * c4) * 4);
+                float4 v[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    if (q < S) v[q] = ld_cluster_f4(la, (uint32_t)q);
+                float4 a = v[0];
+#pragma unroll
+                for (int q = 1; q < 16; ++q)
+                    if (q < S) {
+                        a.x += v[q].x;
+                        a.y += v[q].y;
+                        a.z += v[q].z;
+                        a.w += v[q].w;
+                    }
+                *reinterpret_cast<float4*>(orow + col) = a;
+            }
+        }
+        cluster_sync_all();  // no CTA exits while a peer still reads its shared memory
+    }
     if (PAIR) cluster_sync_all();  // the peer's MMAs / arrivals are done before TMEM is released
     if (warp == C::MMA_W) {
         tc_fence_after();

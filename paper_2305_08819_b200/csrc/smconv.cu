@@ -167,6 +167,8 @@ int pick_bn(int n) {
 // its partial is written out (split-K); bounds TMEM accumulation error.
 constexpr int kMaxKbPerChain = 256;
 constexpr int kGenMaxKbPerChain3x = 16;  // GENERIC 3xTF32 (no chunked promotion)
+// largest cluster split-K (TMA fwd / dX on small maps); SMCONV_CSK=0 turns it off (A/B experiments)
+const int g_csk_max = getenv("SMCONV_CSK") ? atoi(getenv("SMCONV_CSK")) : 8;
 constexpr int kSMs = 148;
 
 void fill_common(GenParams& g, const Dims& d) {
@@ -455,6 +457,28 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
         if (splits < 1) splits = 1;
         g.kb_per_split = (nkb_est + splits - 1) / splits;
         splits = (nkb_est + g.kb_per_split - 1) / g.kb_per_split;
+    } else if (tiles < kSMs && pl.variant == CONV_VARIANT_TMA && g_csk_max >= 2) {
+        // small maps (VGG 8x8 .. 2x2 at batch 128): split K inside a cluster and reduce the partial
+        // tiles through distributed shared memory (one launch; no HBM workspace, no reduce kernel).
+        // S = a power of two <= g_csk_max (8: two clusters per GPC), >= 2 k-blocks per split, and at
+        // most ~128 CTAs (a cluster of 8 needs 8 free SMs of one GPC).  TF32 tiles of BN = 256 leave
+        // too few tiles to fill the machine at S <= 8: use BN = 128 there.
+        if (pl.planes == 1 && pl.BN == 256 && tiles * g_csk_max < 120) {
+            pl.BN = 128;
+            n_tiles = (g.Ngemm + pl.BN - 1) / pl.BN;
+        }
+        const int t2 = m_tiles * n_tiles;
+        int S = 1;
+        for (int S2 = 2; S2 <= g_csk_max && t2 * S2 <= (S2 >= 4 ? 128 : kSMs) && 2 * S2 <= nkb_est; S2 *= 2) S = S2;
+        if (S >= 2) {
+            splits = S;
+            g.csk = S;
+        } else if (t2 < kSMs) {
+            splits = kSMs / t2;
+            const int maxs = nkb_est / 4 > 1 ? nkb_est / 4 : 1;
+            if (splits > maxs) splits = maxs;
+            if (splits < 1) splits = 1;
+        }
     } else if (tiles < kSMs) {
         splits = kSMs / tiles;
         const int maxs = nkb_est / 4 > 1 ? nkb_est / 4 : 1;
@@ -471,8 +495,9 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
     g.splits = splits;
     pl.splits = splits;
     pl.out_elems = out_elems;
-    pl.ws_bytes = splits > 1 ? (size_t)splits * out_elems * sizeof(float) : 0;
-    g.split_stride = splits > 1 ? out_elems : 0;
+    const bool ws_split = splits > 1 && !g.csk;  // cluster split-K needs no HBM partials
+    pl.ws_bytes = ws_split ? (size_t)splits * out_elems * sizeof(float) : 0;
+    g.split_stride = ws_split ? out_elems : 0;
     pl.wx_off = pl.wx_bytes = 0;
     if (pl.planes == 2 && op != CONV_OP_BWD_FILTER &&
         (pl.variant == CONV_VARIANT_TMA || pl.variant == CONV_VARIANT_STRIP)) {
@@ -580,7 +605,8 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
     GenParams g = pl.gp;
     g.A = A;
     g.B = B;
-    g.out = pl.splits > 1 ? (float*)ws : out;
+    const bool ws_split = pl.splits > 1 && !pl.gp.csk;
+    g.out = ws_split ? (float*)ws : out;
     g.Bx = nullptr;
     // A launch error is detected with cudaGetLastError() after each launch; an error the caller left
     // pending would be misattributed (and consumed) there, so refuse to enqueue and leave it in place.
@@ -634,7 +660,7 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
     if (rc) return rc;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: kernel launch failed: %s", op_name(op), cudaGetErrorString(e));
-    if (pl.splits > 1) {
+    if (ws_split) {
         const long long n4 = pl.out_elems / 4;
         int blocks = (int)((n4 + 255) / 256);
         if (blocks > kSMs * 8) blocks = kSMs * 8;
@@ -819,7 +845,7 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
     rc = make_plan(op, d, math, pl);
     if (rc) return rc;
     if (buf && len)
-        snprintf(buf, len, "variant=%s%s BN=%d planes=%d splits=%d grid=%ux%ux%u ws=%zu kernels=%d",
+        snprintf(buf, len, "variant=%s%s%s BN=%d planes=%d splits=%d grid=%ux%ux%u ws=%zu kernels=%d",
                  pl.s2dx ? "tma s2dx" :
                  pl.variant == CONV_VARIANT_DWS      ? "dws"
                  : pl.variant == CONV_VARIANT_DIRECT ? "direct"
@@ -829,9 +855,9 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
                  ((pl.variant == CONV_VARIANT_TMA && pl.tp.pair) ||
                   (pl.variant == CONV_VARIANT_STRIP && strip_pair(op, N, pl.BN, pl.planes)))
                      ? " pair=2cta"
-                     : "", pl.BN, pl.planes, pl.splits, pl.grid.x,
+                     : "", pl.gp.csk ? " csk" : "", pl.BN, pl.planes, pl.splits, pl.grid.x,
                  pl.grid.y, pl.grid.z, pl.ws_bytes,
-                 1 + (pl.splits > 1) + (pl.zero_mask != 0) + (pl.wx_bytes != 0) + (pl.s2dx != 0));
+                 1 + (pl.splits > 1 && !pl.gp.csk) + (pl.zero_mask != 0) + (pl.wx_bytes != 0) + (pl.s2dx != 0));
     return CONV_OK;
 }
 
@@ -841,7 +867,7 @@ int conv2d_plan_kernels(int op, int N, int IH, int IW, int IC, int OC, int FH, i
     if (check_dims(op, d, math)) return -1;
     Plan pl;
     if (make_plan(op, d, math, pl)) return -1;
-    return 1 + (pl.splits > 1) + (pl.zero_mask != 0) + (pl.wx_bytes != 0) + (pl.s2dx != 0);
+    return 1 + (pl.splits > 1 && !pl.gp.csk) + (pl.zero_mask != 0) + (pl.wx_bytes != 0) + (pl.s2dx != 0);
 }
 
 int smconv_selftest_host(void) {
