@@ -119,11 +119,13 @@ def test_plans_cover_network_shapes(sm):
                 for math in (0, 1):
                     d = sm.plan_describe(op, l.dims(128), math)
                     assert "variant=" in d
-                    # main kernel [+ split-K reduce] [+ zero fill of tap-less dX stride phases]
+                    # main kernel [+ split-K reduce, unless the split is reduced in-cluster (csk)]
+                    # [+ zero fill of tap-less dX stride phases]
                     # [+ the bf16 W' prep of 3xTF32 fwd / dX on the TMA and STRIP variants]
                     k = sm.plan_kernels(op, l.dims(128), math)
                     wx = math == 0 and op != 2 and ("variant=tma" in d or "variant=strip" in d)
-                    assert k == 1 + ("splits=1 " not in d) + (op == 1 and l.sh * l.sw > 1 and
+                    hbm_split = "splits=1 " not in d and " csk" not in d
+                    assert k == 1 + hbm_split + (op == 1 and l.sh * l.sw > 1 and
                                                                "variant=tma" in d and l.FH == 1) + wx + \
                         ("s2dx" in d), (l.name, op, d)
 
