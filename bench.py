@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--bucket-mb", type=float, default=16.0)
+    ap.add_argument("--epi", action="store_true",
+                    help="fused epilogues (include/smconv_epi.h): fwd emits BatchNorm statistics, dX applies the "
+                         "LeakyReLU backward and emits the BN-backward statistics (PAPER.md:52 block)")
     ap.add_argument("--graph", default="off", choices=["auto", "on", "off"],
                     help="replay the timed steps as one CUDA graph (auto: on at 1 GPU).  Measured: no gain at "
                          "batch 4096/512 or VGG b128 (the GPU, not the host, bounds the step), and per-call "
@@ -250,7 +253,7 @@ def main():
         raise SystemExit("global batch %d not divisible by %d ranks" % (a.global_batch, world))
     B = a.global_batch // world
     # filters replicated (rank-independent seed); activations / loss gradients differ per shard
-    step = dp.ConvNetStep(a.net, B, dev, math=a.math, seed=1, bucket_mb=a.bucket_mb, rank=rank)
+    step = dp.ConvNetStep(a.net, B, dev, math=a.math, seed=1, bucket_mb=a.bucket_mb, rank=rank, epi=a.epi)
     torch.cuda.synchronize()
 
     def barrier():
@@ -365,6 +368,9 @@ def main():
            "config": {"workload": "%s-cifar10 conv stack fwd+dX+dW (conv-only chain), global batch %d"
                                   % (a.net, a.global_batch),
                       "global_batch": a.global_batch, "per_gpu_batch": B, "math": a.math,
+                      "fwd_dx_cross_terms": "bf16" if a.math == "3xtf32" else None,
+                      "epilogue": ("fused: fwd + BN statistics, dX + LeakyReLU backward + BN-backward statistics"
+                                   if a.epi else "none (plain conv outputs)"),
                       "cuda_graph": graph is not None,
                       "parallelism": "dp%d" % world, "l2": "inputs larger than L2 (per-step working set "
                       "%.1f GB >> 126 MB)" % (sum(t.numel() for b in step.bufs for t in (b.X, b.Y) if t is not None)

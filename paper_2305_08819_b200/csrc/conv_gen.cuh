@@ -25,6 +25,7 @@
 // into one FP32 TMEM accumulator.  TF32 (PLANES == 1): one product of rna_tf32 operands.
 #pragma once
 #include "common.cuh"
+#include "epilogue.cuh"
 
 namespace smconv {
 
@@ -67,6 +68,9 @@ struct GenParams {
     // TMA fwd / dX: split-K inside a thread-block cluster of csk CTAs (0 = off): the partial tiles are
     // summed through distributed shared memory instead of an HBM workspace + reduce kernel
     int csk;
+    // fused epilogue (epilogue.cuh): mode EPI_NONE unless the TMA / STRIP kernel
+    // itself applies the transform and writes the statistics partial rows
+    EpiArgs epi;
 };
 
 template <int OP, int BN, int PLANES>

@@ -89,6 +89,14 @@ struct StripTile {
     }
 };
 
+// 32-row group of an epilogue warp (32 images of one output position) for the fused-epilogue
+// statistics partial rows: (image group, output row, output column); -1 past the ragged strip end
+template <int R>
+SMCONV_DEV int strip_grp(const StripParams& sp, const StripTile& t, int j, int qd) {
+    const int ocol = t.s * 4 * R + 4 * j + qd;
+    return ocol < sp.OWo ? (t.g * sp.OHo + t.orow) * sp.OWo + ocol : -1;
+}
+
 template <int OP>
 SMCONV_DEV int strip_src_row(const StripParams& sp, int orow, int fh) {
     return OP == OP_FWD ? orow + sp.row_off + fh : orow + sp.row_off - fh;
@@ -429,6 +437,25 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
                         mbar_arrive(&aux->tempty[buf]);
                     }
                 }
+                if (p.epi.mode != EPI_NONE) {  // fused epilogue (epilogue.cuh)
+#pragma unroll
+                    for (int j = 0; j < R; ++j)
+#pragma unroll
+                        for (int c0 = 0; c0 < HALF; c0 += 16) {
+                            const int col0 = n0 + half * HALF + c0;
+                            float v[16];
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) v[e] = acc[j][c0 + e];
+                            epi_apply16(p.epi, v, obase[j] >= 0 && col0 < p.Ngemm ? obase[j] + col0 : -1, col0, p.Ngemm,
+                                        strip_grp<R>(sp, t, j, qd), lane);
+                            if (obase[j] >= 0)
+#pragma unroll
+                                for (int e = 0; e < 16; e += 4)
+                                    if (col0 + e < p.Ngemm)
+                                        *reinterpret_cast<float4*>(outp + obase[j] + col0 + e) =
+                                            make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+                        }
+                } else {
 #pragma unroll
                 for (int j = 0; j < R; ++j)
                     if (obase[j] >= 0)
@@ -439,6 +466,7 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
                                 *reinterpret_cast<float4*>(outp + obase[j] + col) =
                                     make_float4(acc[j][e], acc[j][e + 1], acc[j][e + 2], acc[j][e + 3]);
                         }
+                }
             } else {
                 const int buf = c & 1;
                 if (nch > 0) {
@@ -456,6 +484,16 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
                         } else {
 #pragma unroll
                             for (int e = 0; e < 16; ++e) v[e] = 0u;
+                        }
+                        if (p.epi.mode != EPI_NONE) {  // fused epilogue (epilogue.cuh)
+                            const int col0 = n0 + half * HALF + c0;
+                            float f[16];
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
+                            epi_apply16(p.epi, f, obase[j] >= 0 && col0 < p.Ngemm ? obase[j] + col0 : -1, col0,
+                                        p.Ngemm, strip_grp<R>(sp, t, j, qd), lane);
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(f[e]);
                         }
                         if (obase[j] >= 0)
 #pragma unroll

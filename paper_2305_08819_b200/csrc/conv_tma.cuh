@@ -684,6 +684,15 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     obase = (long long)ri.orow * p.Ngemm;
                 }
             }
+            // element offset of GEMM column col of this thread's row in the output tensor (fwd / dX)
+            auto out_off = [&](int col) -> long long {
+                if (OP == OP_FWD && p.s2dx)  // column (pi, pj, ic): dX row 2i'-2+pi
+                    return col >= 2 * p.s2_IC ? obase + col + (long long)(p.s2_IW - 2) * p.s2_IC : obase + col;
+                return obase + col;
+            };
+            // fused epilogue (epilogue.cuh): 32-row group of this warp for the statistics partial rows
+            // (dX: rows of phase k start at phase_tile0[k] tiles of 128 rows, or of 256 for pair tiles)
+            const int egrp = (((OP == OP_DX ? p.phase_tile0[ti.phase] : 0) << (tp.pair ? 8 : 7)) + ti.m0 >> 5) + qd;
             // 4 consecutive GEMM columns of this thread's row -> output
             auto st4 = [&](int col, float x, float y, float z, float w4) {
                 if (!C::IS_DW && tp.csk) {  // cluster split-K: this CTA's partial -> own shared memory
@@ -696,9 +705,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     o[2 * (long long)p.M] = z;
                     o[3 * (long long)p.M] = w4;
                 } else if (OP == OP_FWD && p.s2dx) {  // column (pi, pj, ic): dX row 2i'-2+pi
-                    const long long a = col >= 2 * p.s2_IC ? obase + col + (long long)(p.s2_IW - 2) * p.s2_IC
-                                                           : obase + col;
-                    *reinterpret_cast<float4*>(outp + a) = make_float4(x, y, z, w4);
+                    *reinterpret_cast<float4*>(outp + out_off(col)) = make_float4(x, y, z, w4);
                 } else {
                     *reinterpret_cast<float4*>(outp + obase + col) = make_float4(x, y, z, w4);
                 }
@@ -728,7 +735,21 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                         mbar_arrive(&aux->tempty[buf]);
                     }
                 }
-                if (obase >= 0) {
+                if (!C::IS_DW && p.epi.mode != EPI_NONE) {
+#pragma unroll
+                    for (int c0 = 0; c0 < HALF; c0 += 16) {
+                        const int col0 = n0 + half * HALF + c0;
+                        float v[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = acc[c0 + e];
+                        epi_apply16(p.epi, v, obase >= 0 && col0 < p.Ngemm ? out_off(col0) : -1, col0, p.Ngemm, egrp,
+                                    lane);
+                        if (obase >= 0)
+#pragma unroll
+                            for (int e = 0; e < 16; e += 4)
+                                if (col0 + e < p.Ngemm) st4(col0 + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+                    }
+                } else if (obase >= 0) {
 #pragma unroll
                     for (int e = 0; e < HALF; e += 4) {
                         const int col = n0 + half * HALF + e;
@@ -751,6 +772,16 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     } else {
 #pragma unroll
                         for (int e = 0; e < 16; ++e) v[e] = 0u;
+                    }
+                    if (!C::IS_DW && p.epi.mode != EPI_NONE) {
+                        const int col0 = n0 + half * HALF + c0;
+                        float f[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
+                        epi_apply16(p.epi, f, obase >= 0 && col0 < p.Ngemm ? out_off(col0) : -1, col0, p.Ngemm, egrp,
+                                    lane);
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(f[e]);
                     }
                     if (obase >= 0) {
 #pragma unroll

@@ -15,6 +15,7 @@
 
 #include "../../include/smconv.h"
 #include "../../include/smconv_ext.h"
+#include "../../include/smconv_epi.h"
 #include "../../include/smgemm.h"
 #include "conv_gen.cuh"
 #include "conv_strip.cuh"
@@ -154,6 +155,14 @@ struct Plan {
     TmaParams tp;
     int s2dx;                 // stride-2 3x3 dX as a super-pixel fwd conv (make_plan_s2dx)
     size_t w2_off, w2_bytes;  // its 2x2 filter W2 [(pi, pj, ic)][2][2][OC] in the workspace
+    // fused epilogue (smconv_epi.h, csrc/epilogue.cuh)
+    int epi;                  // CONV_EPI_*
+    int epi_fused;            // 1: in the main kernel's epilogue warps; 0: epi_pass_kernel over the output
+    int epi_C, epi_ncols, epi_ngroups, epi_nchunks;
+    long long epi_rows;       // pass: output rows (N * H * W)
+    size_t epi_part_off, epi_part2_off;  // stats: fp32 partial rows, double chunk sums (workspace)
+    size_t epi_stage_off;     // pass form of the LEAKY_BWD modes: the conv output is staged here (so that
+                              // A may be the output buffer itself: in-place G over A)
 };
 
 int pick_bn(int n) {
@@ -256,9 +265,57 @@ __global__ void __launch_bounds__(256) w2_build_kernel(const float* __restrict__
     }
 }
 
-int make_plan_uncached(int op, const Dims& d, int math, Plan& pl) {
-    if (op == CONV_OP_BWD_DATA && make_plan_s2dx(d, math, pl) == 0) return CONV_OK;
-    return make_plan_base(op, d, math, pl);
+// Fused epilogue (smconv_epi.h): in the conv kernel's epilogue where that kernel writes the final
+// values (TMA / STRIP without split-K), else one pass over the output; statistics partial rows of 32
+// output rows, summed in fixed order by two small kernels.
+void plan_epi(int op, const Dims& d, int epi, Plan& pl) {
+    pl.epi = epi;
+    if (!epi) return;
+    const bool ws_split = pl.splits > 1 && !pl.gp.csk;
+    const int C = op == CONV_OP_FWD ? d.OC : d.IC;
+    const int oh = op == CONV_OP_FWD ? d.OH : d.IH, ow = op == CONV_OP_FWD ? d.OW : d.IW;
+    pl.epi_C = C;
+    pl.epi_rows = (long long)d.N * oh * ow;
+    pl.epi_fused = (pl.variant == CONV_VARIANT_TMA || pl.variant == CONV_VARIANT_STRIP) && !ws_split && !pl.gp.csk;
+    if (pl.epi_fused) {
+        if (pl.variant == CONV_VARIANT_STRIP) pl.epi_ngroups = (d.N + 31) / 32 * oh * ow;
+        else if (op == CONV_OP_BWD_DATA && !pl.s2dx)  // phase tiles of 128 rows (256 rows for CTA pairs)
+            pl.epi_ngroups = pl.gp.phase_tile0[pl.gp.nphase] * (pl.tp.pair ? 8 : 4);
+        else pl.epi_ngroups = (pl.gp.M + 127) / 128 * 4;  // fwd, and the super-pixel dX's virtual fwd rows
+        pl.epi_ncols = pl.gp.Ngemm;                        // = C, or 4 IC for the super-pixel dX
+    } else {
+        pl.epi_ngroups = (int)((pl.epi_rows + 31) / 32);
+        pl.epi_ncols = C;
+        if (epi_reads_a(epi)) {
+            pl.epi_stage_off = (pl.ws_bytes + 255) & ~(size_t)255;
+            pl.ws_bytes = pl.epi_stage_off + (size_t)pl.epi_rows * C * sizeof(float);
+        }
+    }
+    if (epi_has_stats(epi)) {
+        long long nch = 65536 / (2 * pl.epi_ncols);
+        if (nch < 1) nch = 1;
+        if (nch > pl.epi_ngroups) nch = pl.epi_ngroups;
+        pl.epi_nchunks = (int)nch;
+        pl.epi_part_off = (pl.ws_bytes + 255) & ~(size_t)255;
+        pl.ws_bytes = pl.epi_part_off + (size_t)2 * pl.epi_ngroups * pl.epi_ncols * sizeof(float);
+        pl.epi_part2_off = (pl.ws_bytes + 255) & ~(size_t)255;
+        pl.ws_bytes = pl.epi_part2_off + (size_t)2 * pl.epi_nchunks * pl.epi_ncols * sizeof(double);
+    }
+}
+
+int plan_kernel_count(const Plan& pl) {
+    return 1 + (pl.splits > 1 && !pl.gp.csk) + (pl.zero_mask != 0) + (pl.wx_bytes != 0) + (pl.s2dx != 0) +
+           (pl.epi && !pl.epi_fused) + 2 * epi_has_stats(pl.epi);
+}
+
+int make_plan_uncached(int op, const Dims& d, int math, Plan& pl, int epi) {
+    if (op == CONV_OP_BWD_DATA && make_plan_s2dx(d, math, pl) == 0) {
+        plan_epi(op, d, epi, pl);
+        return CONV_OK;
+    }
+    const int rc = make_plan_base(op, d, math, pl);
+    if (rc == CONV_OK) plan_epi(op, d, epi, pl);
+    return rc;
 }
 
 // Process-wide plan cache (SURVEY.md §8(b) contract 4): plans hold no pointers, so a plan is a pure
@@ -280,11 +337,11 @@ std::mutex g_plan_mu;
 std::unordered_map<PlanKey, Plan, PlanKeyHash> g_plans;
 constexpr size_t kMaxPlans = 4096;
 
-int make_plan(int op, const Dims& d, int math, Plan& pl) {
+int make_plan(int op, const Dims& d, int math, Plan& pl, int epi = CONV_EPI_NONE) {
     read_env_once();
     PlanKey k;
     const int v[16] = {op, d.N, d.IH, d.IW, d.IC, d.OC, d.FH, d.FW, d.sh, d.sw, d.ph, d.pw, math,
-                       g_force[op].load(), tma_get_pair(), 0};
+                       g_force[op].load(), tma_get_pair(), epi};
     memcpy(k.v, v, sizeof v);
     {
         std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -294,7 +351,7 @@ int make_plan(int op, const Dims& d, int math, Plan& pl) {
             return CONV_OK;
         }
     }
-    const int rc = make_plan_uncached(op, d, math, pl);
+    const int rc = make_plan_uncached(op, d, math, pl, epi);
     if (rc) return rc;  // failures are not cached (their detail string is per call)
     std::lock_guard<std::mutex> lk(g_plan_mu);
     if (g_plans.size() >= kMaxPlans) g_plans.clear();
@@ -592,11 +649,49 @@ __global__ void __launch_bounds__(256) wx_prep_kernel(const float* __restrict__ 
     }
 }
 
+struct EpiCall {
+    int mode;
+    float k;
+    const float* A;  // LEAKY_BWD*: activation
+    double* stats;   // stats modes: [2][C]
+};
+
+// after the main kernel (and split-K reduce / zero fill): the pass form of the epilogue, then the
+// fixed-order statistics reduction.  `conv_out` is where the conv wrote (the staging buffer in the pass
+// form of the LEAKY_BWD modes), `out` the caller's output.
+int finish_epi(int op, const Plan& pl, const float* conv_out, float* out, void* ws, const EpiCall& ec,
+               cudaStream_t st) {
+    if (!pl.epi) return CONV_OK;
+    EpiArgs ea;
+    ea.mode = pl.epi;
+    ea.k = ec.k;
+    ea.A = ec.A;
+    ea.part = epi_has_stats(pl.epi) ? (float*)((char*)ws + pl.epi_part_off) : nullptr;
+    ea.ngroups = pl.epi_ngroups;
+    ea.ncols = pl.epi_ncols;
+    if (!pl.epi_fused) {
+        const long long items = (long long)pl.epi_ngroups * ((pl.epi_C + 15) / 16);
+        const int blocks = (int)((items + 7) / 8 < kSMs * 8 ? (items + 7) / 8 : kSMs * 8);
+        epi_pass_kernel<0><<<blocks, 256, 0, st>>>(conv_out, out, pl.epi_rows, pl.epi_C, ea);
+    }
+    if (epi_has_stats(pl.epi)) {
+        double* part2 = (double*)((char*)ws + pl.epi_part2_off);
+        const long long n1 = 2LL * pl.epi_nchunks * pl.epi_ncols;
+        const int b1 = (int)((n1 + 255) / 256 < kSMs * 8 ? (n1 + 255) / 256 : kSMs * 8);
+        epi_stats_stage1<0><<<b1, 256, 0, st>>>(ea.part, part2, pl.epi_ngroups, pl.epi_ncols, pl.epi_nchunks);
+        const int b2 = (2 * pl.epi_C + 255) / 256;
+        epi_stats_stage2<0><<<b2, 256, 0, st>>>(part2, ec.stats, pl.epi_ncols, pl.epi_nchunks, pl.epi_C);
+    }
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: epilogue launch failed: %s", op_name(op), cudaGetErrorString(e));
+    return CONV_OK;
+}
+
 int run(int op, const float* A, const float* B, float* out, const Dims& d, int math, void* ws, size_t ws_bytes,
-        conv_stream_t stream_) {
+        conv_stream_t stream_, const EpiCall& ec) {
     cudaStream_t st = (cudaStream_t)stream_;
     Plan pl;
-    int rc = make_plan(op, d, math, pl);
+    int rc = make_plan(op, d, math, pl, ec.mode);
     if (rc) return rc;
     if (pl.ws_bytes > 0 && (ws == nullptr || ws_bytes < pl.ws_bytes))
         return fail(CONV_EWORKSPACE, "%s: workspace %zu bytes at %p, need %zu (conv2d_workspace_bytes)", op_name(op),
@@ -608,6 +703,18 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
     const bool ws_split = pl.splits > 1 && !pl.gp.csk;
     g.out = ws_split ? (float*)ws : out;
     g.Bx = nullptr;
+    // pass form of the LEAKY_BWD modes: the conv (and its reduce / zero fill) write the staging buffer
+    float* conv_out = (pl.epi && !pl.epi_fused && epi_reads_a(pl.epi)) ? (float*)((char*)ws + pl.epi_stage_off) : out;
+    if (!ws_split) g.out = conv_out;
+    memset(&g.epi, 0, sizeof g.epi);
+    if (pl.epi && pl.epi_fused) {
+        g.epi.mode = pl.epi;
+        g.epi.k = ec.k;
+        g.epi.A = ec.A;
+        g.epi.part = epi_has_stats(pl.epi) ? (float*)((char*)ws + pl.epi_part_off) : nullptr;
+        g.epi.ngroups = pl.epi_ngroups;
+        g.epi.ncols = pl.epi_ncols;
+    }
     // A launch error is detected with cudaGetLastError() after each launch; an error the caller left
     // pending would be misattributed (and consumed) there, so refuse to enqueue and leave it in place.
     {
@@ -633,6 +740,9 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
         if (rc) return rc;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: s2dx launch failed: %s", op_name(op), cudaGetErrorString(e));
+        rc = finish_epi(op, pl, conv_out, out, ws, ec, st);
+        if (rc) return rc;
+        g_detail[0] = 0;
         return CONV_OK;
     }
     if (pl.wx_bytes) {
@@ -664,24 +774,26 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
         const long long n4 = pl.out_elems / 4;
         int blocks = (int)((n4 + 255) / 256);
         if (blocks > kSMs * 8) blocks = kSMs * 8;
-        splitk_reduce_kernel<0><<<blocks, 256, 0, st>>>((const float4*)ws, (float4*)out, n4, pl.splits, n4);
+        splitk_reduce_kernel<0><<<blocks, 256, 0, st>>>((const float4*)ws, (float4*)conv_out, n4, pl.splits, n4);
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: reduce launch failed: %s", op_name(op), cudaGetErrorString(e));
     }
     if (pl.zero_mask) {  // after the reduce: its workspace never held the empty phases
         const long long rows = (long long)d.N * d.IH;
         const int blocks = (int)(rows < kSMs * 8 ? rows : kSMs * 8);
-        zero_phases_kernel<0><<<blocks, 256, 0, st>>>((float4*)out, (long long)d.N * d.IH, d.IC / 4, d.IH, d.IW, d.sh, d.sw,
+        zero_phases_kernel<0><<<blocks, 256, 0, st>>>((float4*)conv_out, (long long)d.N * d.IH, d.IC / 4, d.IH, d.IW, d.sh, d.sw,
                                                       pl.zero_mask);
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: zero-fill launch failed: %s", op_name(op), cudaGetErrorString(e));
     }
+    rc = finish_epi(op, pl, conv_out, out, ws, ec, st);
+    if (rc) return rc;
     g_detail[0] = 0;
     return CONV_OK;
 }
 
 int entry(int op, const float* in0, const float* in1, float* out, Dims d, int math, void* ws, size_t ws_bytes,
-          conv_stream_t st) {
+          conv_stream_t st, const EpiCall& ec = EpiCall{0, 0.f, nullptr, nullptr}) {
     int rc = check_dims(op, d, math);
     if (rc) return rc;
     const char* f = op_name(op);
@@ -698,9 +810,32 @@ int entry(int op, const float* in0, const float* in1, float* out, Dims d, int ma
         return fail(CONV_EALIAS, "%s: output buffer overlaps an input buffer", f);
     if (ws && (overlap(ws, ws_bytes, in0, b0) || overlap(ws, ws_bytes, in1, b1) || overlap(ws, ws_bytes, out, bo)))
         return fail(CONV_EALIAS, "%s: workspace overlaps a tensor", f);
-    if (op == CONV_OP_FWD) return run(op, in0, in1, out, d, math, ws, ws_bytes, st);
-    if (op == CONV_OP_BWD_DATA) return run(op, in0, in1, out, d, math, ws, ws_bytes, st);
-    return run(op, in1, in0, out, d, math, ws, ws_bytes, st);  // dW: A = dY, B = X
+    if (ec.mode) {  // fused-epilogue arguments (smconv_epi.h)
+        const bool fwd_ok = op == CONV_OP_FWD && (ec.mode == CONV_EPI_BN_STATS || ec.mode == CONV_EPI_LEAKY);
+        const bool dx_ok = op == CONV_OP_BWD_DATA && (ec.mode == CONV_EPI_LEAKY_BWD || ec.mode == CONV_EPI_LEAKY_BWD_STATS);
+        if (!fwd_ok && !dx_ok) return fail(CONV_EARG, "%s: epilogue %d is not defined for this op", f, ec.mode);
+        if ((ec.mode == CONV_EPI_LEAKY || epi_reads_a(ec.mode)) && !(ec.k > 0.f && ec.k < 3.0e38f))
+            return fail(CONV_EARG, "%s: LeakyReLU slope k=%g must be finite and > 0", f, (double)ec.k);
+        const int C = op == CONV_OP_FWD ? d.OC : d.IC;
+        if (epi_has_stats(ec.mode)) {
+            if (!ec.stats) return fail(CONV_EARG, "%s: NULL stats pointer", f);
+            if ((uintptr_t)ec.stats & 7) return fail(CONV_EALIGN, "%s: stats must be 8-byte aligned", f);
+            const size_t bs = (size_t)2 * C * sizeof(double);
+            if (overlap(ec.stats, bs, in0, b0) || overlap(ec.stats, bs, in1, b1) || overlap(ec.stats, bs, out, bo) ||
+                (ws && overlap(ec.stats, bs, ws, ws_bytes)) || (ec.A && overlap(ec.stats, bs, ec.A, bo)))
+                return fail(CONV_EALIAS, "%s: stats overlaps a tensor or the workspace", f);
+        }
+        if (epi_reads_a(ec.mode)) {
+            if (!ec.A) return fail(CONV_EARG, "%s: NULL activation pointer A", f);
+            if ((uintptr_t)ec.A & 15) return fail(CONV_EALIGN, "%s: A must be 16-byte aligned", f);
+            if ((ec.A != out && overlap(ec.A, bo, out, bo)) || overlap(ec.A, bo, in0, b0) || overlap(ec.A, bo, in1, b1) ||
+                (ws && overlap(ec.A, bo, ws, ws_bytes)))
+                return fail(CONV_EALIAS, "%s: A overlaps dY, W, the workspace, or dX other than exactly", f);
+        }
+    }
+    if (op == CONV_OP_FWD) return run(op, in0, in1, out, d, math, ws, ws_bytes, st, ec);
+    if (op == CONV_OP_BWD_DATA) return run(op, in0, in1, out, d, math, ws, ws_bytes, st, ec);
+    return run(op, in1, in0, out, d, math, ws, ws_bytes, st, ec);  // dW: A = dY, B = X
 }
 
 Dims mk(int N, int IH, int IW, int IC, int OC, int FH, int FW, int sh, int sw, int ph, int pw) {
@@ -827,6 +962,55 @@ int gemm_plan_describe(int g, int M, int N, int K, int math, char* buf, size_t l
     return rc;
 }
 
+// ---------------------------------------------------------------- fused epilogues (include/smconv_epi.h)
+size_t conv2d_epi_workspace_bytes(int op, int N, int IH, int IW, int IC, int OC, int FH, int FW, int sh, int sw,
+                                  int ph, int pw, int math, int epi) {
+    Dims d = mk(N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw);
+    if (check_dims(op, d, math) || epi < CONV_EPI_NONE || epi > CONV_EPI_LEAKY_BWD_STATS) return (size_t)-1;
+    if (epi && !(op == CONV_OP_FWD ? (epi == CONV_EPI_BN_STATS || epi == CONV_EPI_LEAKY)
+                                   : op == CONV_OP_BWD_DATA && epi_reads_a(epi)))
+        return (size_t)-1;
+    Plan pl;
+    if (make_plan(op, d, math, pl, epi)) return (size_t)-1;
+    return pl.ws_bytes;
+}
+
+int conv2d_fwd_epi(const float* X, const float* W, float* Y, double* stats, int N, int IH, int IW, int IC, int OC,
+                   int FH, int FW, int sh, int sw, int ph, int pw, int math, int epi, float k, void* ws,
+                   size_t ws_bytes, conv_stream_t st) {
+    if (epi == CONV_EPI_LEAKY_BWD || epi == CONV_EPI_LEAKY_BWD_STATS || epi < 0 || epi > CONV_EPI_LEAKY_BWD_STATS)
+        return fail(CONV_EARG, "conv2d_fwd_epi: epilogue %d is not a forward epilogue", epi);
+    return entry(CONV_OP_FWD, X, W, Y, mk(N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw), math, ws, ws_bytes, st,
+                 EpiCall{epi, k, nullptr, stats});
+}
+
+int conv2d_bwd_data_epi(const float* dY, const float* W, const float* A, float* dX, double* stats, int N, int IH,
+                        int IW, int IC, int OC, int FH, int FW, int sh, int sw, int ph, int pw, int math, int epi,
+                        float k, void* ws, size_t ws_bytes, conv_stream_t st) {
+    if (epi == CONV_EPI_BN_STATS || epi == CONV_EPI_LEAKY || epi < 0 || epi > CONV_EPI_LEAKY_BWD_STATS)
+        return fail(CONV_EARG, "conv2d_bwd_data_epi: epilogue %d is not a deconvolution epilogue", epi);
+    return entry(CONV_OP_BWD_DATA, dY, W, dX, mk(N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw), math, ws, ws_bytes, st,
+                 EpiCall{epi, k, A, stats});
+}
+
+int conv2d_epi_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, int FW, int sh, int sw, int ph,
+                             int pw, int math, int epi, char* buf, size_t len) {
+    Dims d = mk(N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw);
+    int rc = check_dims(op, d, math);
+    if (rc) return rc;
+    if (epi < CONV_EPI_NONE || epi > CONV_EPI_LEAKY_BWD_STATS) return fail(CONV_EARG, "conv2d_epi_plan_describe: epi");
+    Plan pl;
+    rc = make_plan(op, d, math, pl, epi);
+    if (rc) return rc;
+    char base[256];
+    rc = conv2d_plan_describe(op, N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw, math, base, sizeof base);
+    if (rc) return rc;
+    if (buf && len)
+        snprintf(buf, len, "%s epi=%s groups=%d ws_epi=%zu kernels_epi=%d", base,
+                 !epi ? "none" : pl.epi_fused ? "fused" : "pass", pl.epi_ngroups, pl.ws_bytes, plan_kernel_count(pl));
+    return CONV_OK;
+}
+
 int smconv_set_pair(int on) { return tma_set_pair(on ? 1 : 0); }
 
 int conv2d_force_variant(int op, int variant) {
@@ -856,8 +1040,7 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
                   (pl.variant == CONV_VARIANT_STRIP && strip_pair(op, N, pl.BN, pl.planes)))
                      ? " pair=2cta"
                      : "", pl.gp.csk ? " csk" : "", pl.BN, pl.planes, pl.splits, pl.grid.x,
-                 pl.grid.y, pl.grid.z, pl.ws_bytes,
-                 1 + (pl.splits > 1 && !pl.gp.csk) + (pl.zero_mask != 0) + (pl.wx_bytes != 0) + (pl.s2dx != 0));
+                 pl.grid.y, pl.grid.z, pl.ws_bytes, plan_kernel_count(pl));
     return CONV_OK;
 }
 
@@ -867,7 +1050,7 @@ int conv2d_plan_kernels(int op, int N, int IH, int IW, int IC, int OC, int FH, i
     if (check_dims(op, d, math)) return -1;
     Plan pl;
     if (make_plan(op, d, math, pl)) return -1;
-    return 1 + (pl.splits > 1 && !pl.gp.csk) + (pl.zero_mask != 0) + (pl.wx_bytes != 0) + (pl.s2dx != 0);
+    return plan_kernel_count(pl);
 }
 
 int smconv_selftest_host(void) {

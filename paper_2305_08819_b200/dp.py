@@ -132,7 +132,8 @@ class ConvNetStep:
     """Buffers + one fwd/bwd pass of a conv-only network on this rank's batch shard."""
 
     def __init__(self, net: str, batch: int, device, math: str = "3xtf32", seed: int = 0,
-                 bucket_mb: float = 16.0, chain: bool = True, rank: int = 0):
+                 bucket_mb: float = 16.0, chain: bool = True, rank: int = 0, epi: bool = False,
+                 leaky_k: float = 0.01):
         import torch
         self.torch = torch
         self.net = net
@@ -140,6 +141,11 @@ class ConvNetStep:
         self.batch = batch
         self.device = device
         self.math = sm.MATH[math]
+        # fused epilogues (include/smconv_epi.h): every fwd also emits its BatchNorm statistics, every dX
+        # applies the LeakyReLU backward (slope read from the layer's forward input A = X) and emits the
+        # BN-backward statistics — the paper's leakyRelu(bn(conv(X))) block
+        self.epi = epi
+        self.leaky_k = leaky_k
         L = self.layers
         if chain and net == "resnet18":
             xs, ds, sh = _chain_resnet(L)
@@ -183,20 +189,40 @@ class ConvNetStep:
         # one split-K workspace shared by every call (they are stream-ordered), sized by the library
         for b in self.bufs:
             b.ws_bytes = [sm.workspace_bytes(op, b.layer.dims(batch), self.math) for op in range(3)]
+            if epi:
+                b.ws_bytes[0] = sm.epi_workspace_bytes(0, b.layer.dims(batch), self.math, "bn_stats")
+                b.ws_bytes[1] = sm.epi_workspace_bytes(1, b.layer.dims(batch), self.math, "leaky_bwd_stats")
+                b.stats_fwd = torch.zeros((2, b.layer.OC), dtype=torch.float64, device=device)
+                b.stats_dx = torch.zeros((2, b.layer.IC), dtype=torch.float64, device=device)
         mx = max(max(b.ws_bytes) for b in self.bufs)
         ws = torch.empty(max(mx, 16), dtype=torch.uint8, device=device) if mx else None
         for b in self.bufs:
             b.ws = ws
         # buckets over the backward-ordered flat buffer
         self.buckets = plan_buckets(sizes, int(bucket_mb * (1 << 20) / 4))
-        self.kernels_per_step = sum(
-            sm.plan_kernels(0, b.layer.dims(batch), self.math) + sm.plan_kernels(2, b.layer.dims(batch), self.math)
-            + (sm.plan_kernels(1, b.layer.dims(batch), self.math) if k > 0 else 0)
-            for k, b in enumerate(self.bufs))
+        if epi:
+            self.kernels_per_step = sum(
+                sm.epi_plan_kernels(0, b.layer.dims(batch), self.math, "bn_stats")
+                + sm.plan_kernels(2, b.layer.dims(batch), self.math)
+                + (sm.epi_plan_kernels(1, b.layer.dims(batch), self.math, "leaky_bwd_stats") if k > 0 else 0)
+                for k, b in enumerate(self.bufs))
+        else:
+            self.kernels_per_step = sum(
+                sm.plan_kernels(0, b.layer.dims(batch), self.math) + sm.plan_kernels(2, b.layer.dims(batch), self.math)
+                + (sm.plan_kernels(1, b.layer.dims(batch), self.math) if k > 0 else 0)
+                for k, b in enumerate(self.bufs))
 
     # ---------------------------------------------------------------- one step
     def _call(self, op, b: LayerBuf, a, bb, out, stream):
         ws = b.ws
+        if self.epi and op != 2:
+            ep = sm.EPI["bn_stats"] if op == 0 else sm.EPI["leaky_bwd_stats"]
+            st = b.stats_fwd if op == 0 else b.stats_dx
+            sm.raw_call_epi(op, a.data_ptr(), bb.data_ptr(), b.X.data_ptr(), out.data_ptr(), st.data_ptr(),
+                            b.layer.dims(self.batch), self.math, ep, self.leaky_k,
+                            ws.data_ptr() if (ws is not None and b.ws_bytes[op]) else 0,
+                            b.ws_bytes[op] if ws is not None else 0, stream)
+            return
         sm.raw_call(op, a.data_ptr(), bb.data_ptr(), out.data_ptr(), b.layer.dims(self.batch), self.math,
                     ws.data_ptr() if (ws is not None and b.ws_bytes[op]) else 0,
                     b.ws_bytes[op] if ws is not None else 0, stream)

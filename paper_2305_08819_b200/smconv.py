@@ -23,6 +23,7 @@ MATH = {"3xtf32": CONV_MATH_FP32_3XTF32, "fp32": CONV_MATH_FP32_3XTF32, "tf32": 
 
 EXPORTS = ("conv2d_out_hw", "conv2d_workspace_bytes", "conv2d_fwd", "conv2d_bwd_data", "conv2d_bwd_filter",
            "conv2d_strerror", "conv2d_last_error_detail")
+EPI_EXPORTS = ("conv2d_epi_workspace_bytes", "conv2d_fwd_epi", "conv2d_bwd_data_epi", "conv2d_epi_plan_describe")
 GEMM_EXPORTS = ("gemm_workspace_bytes", "gemm_matmul", "gemm_matmul_t1", "gemm_matmul_t2", "gemm_plan_describe")
 EXT_EXPORTS = ("conv2d_force_variant", "conv2d_plan_describe", "conv2d_plan_kernels", "smconv_selftest_host",
                "smconv_probe_tf32")
@@ -80,6 +81,15 @@ def lib():
                     fn.restype = I
                 L.gemm_plan_describe.argtypes = [I] * 5 + [ctypes.c_char_p, Z]
                 L.gemm_plan_describe.restype = I
+                F = ctypes.c_float
+                L.conv2d_epi_workspace_bytes.argtypes = [I] * 14
+                L.conv2d_epi_workspace_bytes.restype = Z
+                L.conv2d_fwd_epi.argtypes = [P, P, P, P] + [I] * 11 + [I, I, F, P, Z, P]
+                L.conv2d_fwd_epi.restype = I
+                L.conv2d_bwd_data_epi.argtypes = [P, P, P, P, P] + [I] * 11 + [I, I, F, P, Z, P]
+                L.conv2d_bwd_data_epi.restype = I
+                L.conv2d_epi_plan_describe.argtypes = [I] * 14 + [ctypes.c_char_p, Z]
+                L.conv2d_epi_plan_describe.restype = I
                 L.smconv_probe_tf32.argtypes = [P]
                 L.smconv_probe_tf32.restype = I
                 _lib = L
@@ -196,6 +206,18 @@ def raw_call(op, a_ptr, b_ptr, out_ptr, dims, math, ws_ptr, ws_bytes, stream_han
              ctypes.c_void_p(ws_ptr or 0), ws_bytes, ctypes.c_void_p(stream_handle)))
 
 
+def raw_call_epi(op, a_ptr, b_ptr, act_ptr, out_ptr, stats_ptr, dims, math, epi, k, ws_ptr, ws_bytes, stream_handle):
+    """Direct C-ABI call of conv2d_fwd_epi (op 0) / conv2d_bwd_data_epi (op 1) with raw device pointers."""
+    P = ctypes.c_void_p
+    if op == CONV_OP_FWD:
+        rc = lib().conv2d_fwd_epi(P(a_ptr), P(b_ptr), P(out_ptr), P(stats_ptr or 0), *dims, math, epi, float(k),
+                                  P(ws_ptr or 0), ws_bytes, P(stream_handle))
+    else:
+        rc = lib().conv2d_bwd_data_epi(P(a_ptr), P(b_ptr), P(act_ptr), P(out_ptr), P(stats_ptr or 0), *dims, math, epi,
+                                       float(k), P(ws_ptr or 0), ws_bytes, P(stream_handle))
+    _check(rc)
+
+
 def conv2d_fwd(x, w, stride=(1, 1), padding=(1, 1), math="3xtf32", out=None):
     """Y[N,OH,OW,OC] = X[N,IH,IW,IC] (*) W[OC,FH,FW,IC] (include/smconv.h conv2d_fwd)."""
     import torch
@@ -270,6 +292,93 @@ def conv2d_bwd_filter(x, dy, kernel_hw, stride=(1, 1), padding=(1, 1), math="3xt
     _check(lib().conv2d_bwd_filter(_ptr(x), _ptr(dy), _ptr(out), *dims, m, _ptr(ws) if ws is not None else None, nb,
                                    ctypes.c_void_p(st)))
     return out
+
+
+# ------------------------------------------------------------------ fused epilogues (include/smconv_epi.h)
+EPI = {"none": 0, "bn_stats": 1, "leaky": 2, "leaky_bwd": 3, "leaky_bwd_stats": 4}
+
+
+def _epi(e):
+    return EPI[e] if isinstance(e, str) else int(e)
+
+
+def epi_workspace_bytes(op, dims, math, epi):
+    n = lib().conv2d_epi_workspace_bytes(op, *dims, _math(math), _epi(epi))
+    if n == ctypes.c_size_t(-1).value:
+        raise ConvError(CONV_EARG, lib().conv2d_last_error_detail().decode())
+    return n
+
+
+def epi_plan_describe(op, dims, math, epi):
+    buf = ctypes.create_string_buffer(384)
+    _check(lib().conv2d_epi_plan_describe(op, *dims, _math(math), _epi(epi), buf, 384))
+    return buf.value.decode()
+
+
+def epi_plan_kernels(op, dims, math, epi):
+    """Kernels one fused-epilogue call enqueues (main + split-K / zero fill / W' + epilogue pass + stats)."""
+    return int(epi_plan_describe(op, dims, math, epi).rsplit("kernels_epi=", 1)[1])
+
+
+def conv2d_fwd_epi(x, w, stride=(1, 1), padding=(1, 1), math="3xtf32", epi="bn_stats", k=0.01, out=None):
+    """Y = conv(X, W) with a fused epilogue (include/smconv_epi.h conv2d_fwd_epi):
+    epi="bn_stats" -> (Y, stats[2, OC] float64: per-channel sum y, sum y^2);  epi="leaky" -> (leaky_k(Y), None)."""
+    import torch
+    _need(x, "x")
+    _need(w, "w")
+    _rank4(x, "x")
+    _rank4(w, "w")
+    _same_device(x, w)
+    N, IH, IW, IC = x.shape
+    OC, FH, FW, wic = w.shape
+    if wic != IC:
+        raise ValueError("w has %d input channels, x has %d" % (wic, IC))
+    OH, OW = out_hw(IH, IW, FH, FW, stride, padding)
+    out = _out(out, (N, OH, OW, OC), x)
+    e = _epi(epi)
+    stats = torch.empty((2, OC), dtype=torch.float64, device=x.device) if e == EPI["bn_stats"] else None
+    dims = (N, IH, IW, IC, OC, FH, FW, stride[0], stride[1], padding[0], padding[1])
+    m = _math(math)
+    nb = epi_workspace_bytes(CONV_OP_FWD, dims, m, e)
+    ws = _workspace(nb, x.device)
+    st = torch.cuda.current_stream(x.device).cuda_stream
+    _check(lib().conv2d_fwd_epi(_ptr(x), _ptr(w), _ptr(out), _ptr(stats) if stats is not None else None, *dims, m, e,
+                                float(k), _ptr(ws) if ws is not None else None, nb, ctypes.c_void_p(st)))
+    return out, stats
+
+
+def conv2d_bwd_data_epi(dy, w, a, input_hw, stride=(1, 1), padding=(1, 1), math="3xtf32", epi="leaky_bwd_stats",
+                        k=0.01, out=None):
+    """G = deconv(dY, W) * slope_k(A) with a fused epilogue (include/smconv_epi.h conv2d_bwd_data_epi);
+    epi="leaky_bwd_stats" also returns stats[2, IC] float64 (sum G, sum G*z).  `out` may be `a` (in place)."""
+    import torch
+    _need(dy, "dy")
+    _need(w, "w")
+    _need(a, "a")
+    _rank4(dy, "dy")
+    _rank4(w, "w")
+    _same_device(dy, w, a)
+    N, OH, OW, OC = dy.shape
+    woc, FH, FW, IC = w.shape
+    if woc != OC:
+        raise ValueError("w has %d output channels, dy has %d" % (woc, OC))
+    IH, IW = input_hw
+    if tuple(a.shape) != (N, IH, IW, IC):
+        raise ValueError("a has shape %s, expected %s" % (tuple(a.shape), (N, IH, IW, IC)))
+    out = _out(out, (N, IH, IW, IC), dy)
+    dims = (N, IH, IW, IC, OC, FH, FW, stride[0], stride[1], padding[0], padding[1])
+    if out_hw(IH, IW, FH, FW, stride, padding) != (OH, OW):
+        raise ValueError("dy extent %s does not match input_hw %s" % ((OH, OW), (IH, IW)))
+    e = _epi(epi)
+    stats = torch.empty((2, IC), dtype=torch.float64, device=dy.device) if e == EPI["leaky_bwd_stats"] else None
+    m = _math(math)
+    nb = epi_workspace_bytes(CONV_OP_BWD_DATA, dims, m, e)
+    ws = _workspace(nb, dy.device)
+    st = torch.cuda.current_stream(dy.device).cuda_stream
+    _check(lib().conv2d_bwd_data_epi(_ptr(dy), _ptr(w), _ptr(a), _ptr(out), _ptr(stats) if stats is not None else None,
+                                     *dims, m, e, float(k), _ptr(ws) if ws is not None else None, nb,
+                                     ctypes.c_void_p(st)))
+    return out, stats
 
 
 # ------------------------------------------------------------------ GEMM (include/smgemm.h)

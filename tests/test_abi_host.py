@@ -21,7 +21,9 @@ def sm():
 
 def _declared():
     names = []
-    for h in ("smconv.h", "smconv_ext.h", "smgemm.h"):
+    for h in sorted(os.listdir(os.path.join(ROOT, "include"))):
+        if not h.endswith(".h"):
+            continue
         src = open(os.path.join(ROOT, "include", h)).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
         names += re.findall(r"^\s*(?:const\s+)?\w+\**\s+\**(\w+)\s*\(", src, flags=re.M)
@@ -35,7 +37,7 @@ def test_exports_every_declared_symbol(sm):
     L = ctypes.CDLL(sm.LIB_PATH)
     for n in names:
         assert hasattr(L, n), n
-    assert set(sm.EXPORTS + sm.EXT_EXPORTS + sm.GEMM_EXPORTS) <= set(names)
+    assert set(sm.EXPORTS + sm.EXT_EXPORTS + sm.GEMM_EXPORTS + sm.EPI_EXPORTS) <= set(names)
 
 
 def test_library_is_sm100a(sm):
@@ -214,3 +216,42 @@ def test_gemm_host_validation(sm):
     L = sm.lib()
     rc = L.gemm_matmul_t1(None, None, None, 8, 8, 8, 0, None, 0, None)
     assert rc == sm.CONV_EARG and b"matMulT1" in L.conv2d_last_error_detail()
+
+
+def test_epi_argument_errors_on_host(sm):
+    """Fused-epilogue argument checks (include/smconv_epi.h) return before anything is enqueued."""
+    import ctypes as C
+    L = sm.lib()
+    P = C.c_void_p
+    d = (32, 8, 8, 32, 32, 3, 3, 1, 1, 1, 1)
+    x, w, y, st = P(0x100000), P(0x200000), P(0x300000), P(0x400000)
+    call = lambda epi, k, stats: L.conv2d_fwd_epi(x, w, y, stats, *d, 0, epi, k, P(0), 0, P(0))
+    assert call(3, 0.1, st) == sm.CONV_EARG          # a dX epilogue on fwd
+    assert call(9, 0.1, st) == sm.CONV_EARG          # unknown
+    assert call(2, 0.0, st) == sm.CONV_EARG          # leaky slope must be > 0
+    assert call(2, float("nan"), st) == sm.CONV_EARG
+    assert call(1, 0.1, P(0)) == sm.CONV_EARG        # stats required
+    assert call(1, 0.1, P(0x400004)) == sm.CONV_EALIGN
+    assert call(1, 0.1, P(0x300000 + 64)) == sm.CONV_EALIAS  # stats inside Y
+    dx = lambda epi, a: L.conv2d_bwd_data_epi(y, w, a, x, st, *d, 0, epi, C.c_float(0.1), P(0), 0, P(0))
+    assert dx(1, P(0x500000)) == sm.CONV_EARG       # a fwd epilogue on dX
+    assert dx(3, P(0)) == sm.CONV_EARG               # A required
+    assert dx(3, P(0x500008)) == sm.CONV_EALIGN
+    assert dx(3, P(0x300000)) == sm.CONV_EALIAS      # A overlapping dY
+    assert dx(3, P(0x100000 + 4096)) == sm.CONV_EALIAS  # A partially overlapping dX
+    assert sm.lib().conv2d_epi_workspace_bytes(2, *d, 0, 1) == C.c_size_t(-1).value  # no dW epilogue
+    assert sm.epi_workspace_bytes(0, d, 0, "bn_stats") >= sm.workspace_bytes(0, d, 0)
+
+
+def test_epi_plans(sm):
+    """Fused where the conv kernel writes final values (TMA / STRIP without split-K), else a pass;
+    statistics add two fixed-order reduction kernels."""
+    d_strip = (128, 32, 32, 64, 64, 3, 3, 1, 1, 1, 1)
+    d_csk = (128, 2, 2, 512, 512, 3, 3, 1, 1, 1, 1)
+    d_stem = (512, 32, 32, 4, 64, 3, 3, 1, 1, 1, 1)
+    assert "epi=fused" in sm.epi_plan_describe(0, d_strip, 1, "bn_stats")
+    assert "epi=pass" in sm.epi_plan_describe(0, d_csk, 1, "bn_stats")
+    assert "epi=pass" in sm.epi_plan_describe(0, d_stem, 0, "leaky")
+    assert sm.epi_plan_kernels(0, d_strip, 1, "bn_stats") == sm.plan_kernels(0, d_strip, 1) + 2
+    assert sm.epi_plan_kernels(0, d_csk, 1, "bn_stats") == sm.plan_kernels(0, d_csk, 1) + 3
+    assert sm.epi_plan_kernels(1, d_strip, 1, "leaky_bwd") == sm.plan_kernels(1, d_strip, 1)
