@@ -52,6 +52,12 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
 int conv2d_plan_kernels(int op, int N, int IH, int IW, int IC, int OC, int FH, int FW,
                         int sh, int sw, int ph, int pw, int math);
 
+/* EXPERIMENT hook: when device_buf != NULL (>= 16 * grid u64, device memory), the TMA-variant kernels
+ * write per-CTA phase timestamps (clock64; slot 15 = globaltimer at entry) into it: 0 entry, 1 setup
+ * done, 2 first TMA issue, 4 first MMA issue, 5 last MMA commit, 6 accumulator ready (epilogue),
+ * 7 epilogue done, 8 CTA barrier, 9/10 cluster split-K reduce start/end, 11 exit.  NULL (default) = off. */
+int smconv_set_trace(void* device_buf);
+
 /* Host-only self test of the library's index arithmetic (fast division); 0 = pass. */
 int smconv_selftest_host(void);
 

@@ -38,6 +38,38 @@ SMCONV_HD uint32_t umulhi32(uint32_t a, uint32_t b) {
 
 SMCONV_HD uint32_t fdiv(uint32_t n, const FastDiv& f) { return (umulhi32(n, f.mul) + n) >> f.shift; }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// (launch.cuh): let the next kernel of the stream be scheduled now / wait until the previous kernels
+// have completed and their writes are visible.  Every kernel calls pdl_wait() before its first
+// global-memory access; both are no-ops for a kernel launched without the PDL attribute.
+SMCONV_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+SMCONV_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// ------------------------------------------------------------------ kernel-parameter cache warm-up
+// The kernels read their (~2.5 KB) parameter blocks through the constant cache, and every role's
+// per-tile bookkeeping (tap tables, fast divisors, dynamically indexed) walked the parameter lines one
+// cache miss at a time: TileInfo::init took ~4400 cycles and the TMA producer issued its first load
+// ~7400 cycles after the CTA started (smconv_set_trace, r02i/r02j: VGG conv11 at batch 128 is a ~2 us
+// memory-bound kernel).  Thread t < lines loads the word at byte 64 t of the block with ld.param on a
+// register address (cvta.to.param; SASS LDC c[0x0][R]), so all lines miss at once, in the shadow of the
+// barrier / TMEM set-up.  The value goes to a shared-memory sink so ptxas keeps the load.
+template <class T>
+SMCONV_DEV void param_warm(const T& prm, int t, volatile int* sink) {
+    constexpr int NL = (int)((sizeof(T) + 63) / 64);
+    if (t >= 0 && t < NL) {
+        int v;
+        const unsigned long long g = reinterpret_cast<unsigned long long>(reinterpret_cast<const char*>(&prm) + 64 * t);
+        asm volatile("{\n\t.reg .u64 pa;\n\tcvta.to.param.u64 pa, %1;\n\tld.param.u32 %0, [pa];\n\t}"
+                     : "=r"(v)
+                     : "l"(g));
+        *sink = v;
+    }
+}
+template <class T>
+constexpr int param_lines() {
+    return (int)((sizeof(T) + 63) / 64);
+}
+
 // ------------------------------------------------------------------ shared-memory helpers
 SMCONV_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -256,6 +288,16 @@ SMCONV_DEV uint32_t cluster_ctarank() {
 }
 
 // 16-byte load from the shared memory of CTA `cta` of this cluster at the offset of local address `la`
+// 16-B store into the shared memory of CTA `cta` of the cluster at local offset-address `la`
+SMCONV_DEV void st_cluster_f4(uint32_t la, uint32_t cta, float4 v) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "st.shared::cluster.v4.f32 [ra], {%2, %3, %4, %5};\n\t}" ::"r"(la),
+        "r"(cta), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+        : "memory");
+}
+
 SMCONV_DEV float4 ld_cluster_f4(uint32_t la, uint32_t cta) {
     float4 v;
     asm volatile(
@@ -266,6 +308,10 @@ SMCONV_DEV float4 ld_cluster_f4(uint32_t la, uint32_t cta) {
         : "r"(la), "r"(cta)
         : "memory");
     return v;
+}
+
+SMCONV_DEV void cluster_arrive_wait() {  // same as cluster_sync_all, for one role's threads at a time
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 SMCONV_DEV void cluster_sync_all() {

@@ -11,6 +11,7 @@
 #include <cstdlib>
 
 #include "../../include/smconv.h"
+#include "launch.cuh"
 #include "conv_gen.cuh"
 
 namespace smconv {
@@ -76,6 +77,8 @@ SMCONV_DEV void direct_load_rows(const DirectParams& p, float* Xs, int n, int oh
 template <int TFH, int TFW, int TIC4, int TSW, bool RAG>
 __global__ void __launch_bounds__(kDirThreads) conv_direct_fwd_kernel(const __grid_constant__ DirectParams p) {
     extern __shared__ float4 sm4[];
+    pdl_trigger();
+    pdl_wait();  // launch.cuh
     float* Ws = reinterpret_cast<float*>(sm4);  // [K][OC]
     const int FH = TFH ? TFH : p.FH, FW = TFW ? TFW : p.FW, SW = TSW ? TSW : p.sw;
     const int OC4 = p.OC >> 2, IC4 = TIC4 ? TIC4 : p.IC >> 2;
@@ -164,6 +167,8 @@ __global__ void __launch_bounds__(kDirThreads) conv_direct_fwd_kernel(const __gr
 template <int ACC4>  // accumulator float4 columns per thread = ceil(FW*IC / 4)
 __global__ void __launch_bounds__(kDirThreads) conv_direct_dw_kernel(const __grid_constant__ DirectParams p) {
     extern __shared__ float4 sm4[];
+    pdl_trigger();
+    pdl_wait();  // launch.cuh
     const int OC4 = p.OC >> 2, IC4 = p.IC >> 2;
     const int nD4 = p.OW * OC4, nX4 = p.FH * p.WIN * IC4, nR4 = nD4 + nX4;  // float4 per row
     float* Red = reinterpret_cast<float*>(sm4 + kDirNB * nR4);
@@ -326,7 +331,7 @@ int direct_launch(int op, const GenParams& g, int blocks, cudaStream_t st, char*
         if (p.FH == 3 && p.FW == 3 && p.IC == 4 && p.sw == 1 && p.OW % kDirOWB == 0)
             kern = conv_direct_fwd_kernel<3, 3, 1, 1, false>;  // the RGB stems
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, kDirThreads, smem, st>>>(p);
+        launch_k(kern, dim3(grid), dim3(kDirThreads), smem, st, 1, p);
     } else {
         p.dY = g.A;  // run(): dW gets A = dY, B = X
         p.X = g.B;
@@ -341,11 +346,11 @@ int direct_launch(int op, const GenParams& g, int blocks, cudaStream_t st, char*
         if (acc4 <= 3) {
             if (smem > 48 * 1024)
                 cudaFuncSetAttribute(conv_direct_dw_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            conv_direct_dw_kernel<3><<<blocks, kDirThreads, smem, st>>>(p);
+            launch_k(conv_direct_dw_kernel<3>, dim3(blocks), dim3(kDirThreads), smem, st, 1, p);
         } else {
             if (smem > 48 * 1024)
                 cudaFuncSetAttribute(conv_direct_dw_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            conv_direct_dw_kernel<6><<<blocks, kDirThreads, smem, st>>>(p);
+            launch_k(conv_direct_dw_kernel<6>, dim3(blocks), dim3(kDirThreads), smem, st, 1, p);
         }
     }
     return CONV_OK;

@@ -33,6 +33,7 @@
 
 #include "../../include/smconv.h"
 #include "conv_tma.cuh"
+#include "launch.cuh"
 
 namespace smconv {
 
@@ -82,6 +83,7 @@ struct DwsAux {
     uint64_t conv[16], tfree[8];
     uint64_t tfull, tempty;
     uint32_t tmem_base;
+    int sink;  // param_warm
 };
 
 struct DwsItem {
@@ -108,6 +110,8 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
     DwsAux* aux = reinterpret_cast<DwsAux*>(tiles_ptr + C::SS * C::STAGE_BYTES);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int CHK = PLANES == 2 ? dp.chunk_kb : (1 << 30);
+    param_warm(p, tid, &aux->sink);
+    param_warm(dp, tid - param_lines<GenParams>(), &aux->sink);
 
     if (tid == 0) {
         for (int s = 0; s < C::SS; ++s) {
@@ -135,6 +139,8 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = aux->tmem_base;
+    pdl_trigger();
+    pdl_wait();  // launch.cuh
 
     if (warp == C::TMA_W) {
         // ======================= TMA producer: per k-block one dY box + one activation slab box
@@ -394,7 +400,11 @@ int launch_t(const DwsParams& dp, const GenParams& g, cudaStream_t st, char* err
         attr_done.fetch_or(bit);
     }
     const int grid = dp.work < 148 ? dp.work : 148;
-    conv_dws_kernel<PLANES, OW><<<grid, C::NTHREADS, C::SMEM_BYTES, st>>>(dp, g);
+    const cudaError_t e = launch_k(conv_dws_kernel<PLANES, OW>, dim3(grid), dim3(C::NTHREADS), C::SMEM_BYTES, st, 1, dp, g);
+    if (e != cudaSuccess) {
+        snprintf(err, errlen, "cudaLaunchKernelEx(dws): %s", cudaGetErrorString(e));
+        return CONV_ECUDA;
+    }
     return CONV_OK;
 }
 

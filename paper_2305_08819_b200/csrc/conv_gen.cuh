@@ -71,7 +71,22 @@ struct GenParams {
     // fused epilogue (epilogue.cuh): mode EPI_NONE unless the TMA / STRIP kernel
     // itself applies the transform and writes the statistics partial rows
     EpiArgs epi;
+    // TMA dW with IC % 32 != 0: the GEMM columns are (tap, ic) with ic padded to dw_icp = roundup(IC, 32)
+    // (a 32-column block never straddles a tap); the epilogue drops ic >= IC and stores at tap * IC + ic
+    int dw_icp;
+    FastDiv fd_icp;
+    // TEST/EXPERIMENT hook (smconv_set_trace): per-CTA phase timestamps, NULL in normal operation
+    unsigned long long* trace;
 };
+
+// trace slot e of this CTA: clock64 (SM cycles; slot 15 = globaltimer at entry, ns)
+SMCONV_DEV void trace_mark(unsigned long long* t, int e) {
+    if (t) {
+        unsigned long long c;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+        t[blockIdx.x * 16 + e] = c;
+    }
+}
 
 template <int OP, int BN, int PLANES>
 struct GenCfg {
@@ -99,6 +114,7 @@ struct GenAux {
     uint64_t done;
     uint32_t tmem_base;
     int ntaps;
+    int sink;  // param_warm
     int4 taps[kMaxTaps];  // {dh, dw, tapfull, 0}
 };
 
@@ -205,6 +221,7 @@ __global__ void __launch_bounds__(GenCfg<OP, BN, PLANES>::NTHREADS, 1)
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
+    param_warm(p, tid, &aux->sink);
 
     // ---------------- tile coordinates
     int phase = 0, mt = blockIdx.x;
@@ -235,6 +252,8 @@ __global__ void __launch_bounds__(GenCfg<OP, BN, PLANES>::NTHREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = aux->tmem_base;
+    pdl_trigger();
+    pdl_wait();  // launch.cuh
 
     // K extent of this tile / split
     int kb_begin, kb_end, Ktot;
@@ -465,6 +484,8 @@ __global__ void __launch_bounds__(GenCfg<OP, BN, PLANES>::NTHREADS, 1)
 template <int UNUSED = 0>
 __global__ void __launch_bounds__(256) zero_phases_kernel(float4* __restrict__ dx, long long rows, int IC4, int IH, int IW,
                                                           int sh, int sw, uint32_t empty_mask) {
+    pdl_trigger();
+    pdl_wait();
     // one (n, ih) row per block iteration, 32-bit index math (a 64-bit division per element made
     // this kernel 3x slower than the HBM write it does); rows whose phases are all empty are a
     // contiguous memset
@@ -489,6 +510,8 @@ __global__ void __launch_bounds__(256) zero_phases_kernel(float4* __restrict__ d
 template <int UNUSED = 0>
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ out,
                                                             long long n4, int splits, long long stride4) {
+    pdl_trigger();
+    pdl_wait();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
         // fixed summation order s = 0, 1, ..., splits-1 (deterministic); loads are batched 8 deep so
         // a thread keeps 8 independent requests in flight (one at a time: 137 us for l1 dW's 512 splits)

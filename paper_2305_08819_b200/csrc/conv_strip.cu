@@ -8,6 +8,7 @@
 
 #include "../../include/smconv.h"
 #include "conv_strip.cuh"
+#include "launch.cuh"
 
 namespace smconv {
 
@@ -38,19 +39,8 @@ int launch_t(const StripParams& sp, const GenParams& g, cudaStream_t st, char* e
     }
     if (PAIR) {  // 2-CTA clusters: one M = 256 tile (two 32-image strips) per pair
         const int pairs = sp.work < 74 ? sp.work : 74;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(2 * pairs, 1, 1);
-        cfg.blockDim = dim3(C::NTHREADS, 1, 1);
-        cfg.dynamicSmemBytes = C::SMEM_BYTES;
-        cfg.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 2;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        const cudaError_t e = cudaLaunchKernelEx(&cfg, conv_strip_kernel<OP, BN, PLANES, R, PAIR>, sp, g);
+        const cudaError_t e = launch_k(conv_strip_kernel<OP, BN, PLANES, R, PAIR>, dim3(2 * pairs), dim3(C::NTHREADS),
+                                       C::SMEM_BYTES, st, 2, sp, g);
         if (e != cudaSuccess) {
             snprintf(err, errlen, "cudaLaunchKernelEx(strip pair): %s", cudaGetErrorString(e));
             return CONV_ECUDA;
@@ -58,7 +48,12 @@ int launch_t(const StripParams& sp, const GenParams& g, cudaStream_t st, char* e
         return CONV_OK;
     }
     const int grid = sp.work < 148 ? sp.work : 148;
-    conv_strip_kernel<OP, BN, PLANES, R, PAIR><<<grid, C::NTHREADS, C::SMEM_BYTES, st>>>(sp, g);
+    const cudaError_t e = launch_k(conv_strip_kernel<OP, BN, PLANES, R, PAIR>, dim3(grid), dim3(C::NTHREADS),
+                                   C::SMEM_BYTES, st, 1, sp, g);
+    if (e != cudaSuccess) {
+        snprintf(err, errlen, "cudaLaunchKernelEx(strip): %s", cudaGetErrorString(e));
+        return CONV_ECUDA;
+    }
     return CONV_OK;
 }
 
@@ -113,6 +108,9 @@ int strip_launch(int op, int BN, int planes, const GenParams& g, cudaStream_t st
     sp.SW = (int)W;
     sp.strips = (sp.OWo + 4 * R - 1) / (4 * R);
     sp.n_tiles = (g.Ngemm + BN - 1) / BN;
+    sp.fd_ntiles = make_fastdiv(sp.n_tiles);
+    sp.fd_strips = make_fastdiv(sp.strips);
+    sp.fd_OHo = make_fastdiv(sp.OHo);
     sp.pair = strip_pair(op, g.N, BN, planes) ? 1 : 0;
     sp.work = (sp.pair ? sp.NG / 2 : sp.NG) * sp.OHo * sp.strips * sp.n_tiles;
     const int BNC = sp.pair ? BN / 2 : BN;  // B columns staged per CTA

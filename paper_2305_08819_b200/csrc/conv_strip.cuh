@@ -40,6 +40,7 @@ struct __align__(64) StripParams {
     int row_off;       // source row = out row + row_off + (fwd: fh | dX: -fh)   (fwd: -ph, dX: +ph)
     int col_off;       // first slab column = strip origin + col_off (fwd: -pw, dX: pw - (FW-1))
     int pair;          // work items are pair tiles (two 32-image groups), kernel template PAIR
+    FastDiv fd_ntiles, fd_strips, fd_OHo;
 };
 
 template <int OP, int BN, int PLANES, int R, bool PAIR = false>
@@ -79,12 +80,13 @@ struct StripCfg {
 struct StripTile {
     int g, orow, s, nt;
     SMCONV_DEV void init(const StripParams& sp, int w, int rank = 0) {
-        nt = w % sp.n_tiles;
-        int r = w / sp.n_tiles;
-        s = r % sp.strips;
-        r /= sp.strips;
-        orow = r % sp.OHo;
-        g = r / sp.OHo;
+        // fast divisors (host-built): generic divisions are ~150-cycle dependent chains
+        int r = (int)fdiv((uint32_t)w, sp.fd_ntiles);
+        nt = w - r * sp.n_tiles;
+        const int r2 = (int)fdiv((uint32_t)r, sp.fd_strips);
+        s = r - r2 * sp.strips;
+        g = (int)fdiv((uint32_t)r2, sp.fd_OHo);
+        orow = r2 - g * sp.OHo;
         if (sp.pair) g = 2 * g + rank;  // pair tile: image groups 2g' (CTA 0) and 2g'+1 (CTA 1)
     }
 };
@@ -126,6 +128,8 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
     const int rank = PAIR ? (int)cluster_ctarank() : 0;
     const int wfirst = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
     const int wstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    param_warm(p, tid, &aux->sink);
+    param_warm(sp, tid - param_lines<GenParams>(), &aux->sink);
 
     if (tid == 0) {
         for (int t = 0; t < C::NT; ++t) mbar_init(&aux->tfree[t], 1);
@@ -157,6 +161,8 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
     if (PAIR) cluster_sync_all();  // the peer's barriers exist before any remote arrival
     tc_fence_after();
     const uint32_t tmem = aux->tmem_base;
+    pdl_trigger();
+    pdl_wait();  // launch.cuh
 
     if (warp == C::TMA_W) {
         // ======================= TMA producer: 2 boxes per stage (slab row, FW filter taps)

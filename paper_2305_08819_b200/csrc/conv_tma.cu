@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 
 #include "conv_tma.cuh"
+#include "launch.cuh"
 
 namespace smconv {
 
@@ -83,26 +84,20 @@ int launch_t(const TmaParams& tp, const GenParams& g, dim3 grid, cudaStream_t st
             snprintf(err, errlen, "tma csk: partial tile does not fit the stage ring");
             return CONV_EUNSUPPORTED;
         }
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = grid;
-        cfg.blockDim = dim3(C::NTHREADS, 1, 1);
-        cfg.dynamicSmemBytes = C::SMEM_BYTES;
-        cfg.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = PAIR ? 2 : tp.csk;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        const cudaError_t e = cudaLaunchKernelEx(&cfg, conv_tma_kernel<OP, BN, PLANES, PAIR>, tp, g);
+        const cudaError_t e = launch_k(conv_tma_kernel<OP, BN, PLANES, PAIR>, grid, dim3(C::NTHREADS), C::SMEM_BYTES, st,
+                                       PAIR ? 2 : tp.csk, tp, g);
         if (e != cudaSuccess) {
             snprintf(err, errlen, "cudaLaunchKernelEx(tma cluster %d): %s", PAIR ? 2 : tp.csk, cudaGetErrorString(e));
             return CONV_ECUDA;
         }
         return CONV_OK;
     }
-    conv_tma_kernel<OP, BN, PLANES, PAIR><<<grid, C::NTHREADS, C::SMEM_BYTES, st>>>(tp, g);
+    const cudaError_t e = launch_k(conv_tma_kernel<OP, BN, PLANES, PAIR>, grid, dim3(C::NTHREADS), C::SMEM_BYTES, st, 1,
+                                   tp, g);
+    if (e != cudaSuccess) {
+        snprintf(err, errlen, "cudaLaunchKernelEx(tma): %s", cudaGetErrorString(e));
+        return CONV_ECUDA;
+    }
     return CONV_OK;
 }
 
@@ -142,7 +137,7 @@ bool tma_encode_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* 
 // the bf16 W' plane (wx_prep_kernel): rows (tap, n, cb) of 64 bf16, box (64, 1, BNC, 1) -> BNC
 // K-major 128-B rows in shared memory, 128B swizzle (the UMMA SWIZZLE_128B K-major layout)
 bool tma_encode_wx(CUtensorMap* m, const void* base, int Nn, int Kc, int T, int BNC) {
-    const uint64_t CB = Kc / 32;
+    const uint64_t CB = (Kc + 31) / 32;
     uint64_t d[4] = {64, CB, (uint64_t)Nn, (uint64_t)T}, s[3] = {128, CB * 128, (uint64_t)Nn * CB * 128};
     uint32_t b[4] = {64, 1, (uint32_t)BNC, 1};
     return encode(m, base, 4, d, s, b, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
@@ -152,8 +147,15 @@ bool tma_supported(int op, int N, int IC, int OC, int FH, int FW, int sh, int sw
     (void)sh; (void)sw;
     if (N % 32) return false;
     if (FH > kMaxTF || FW > kMaxTF) return false;  // per-phase tap tables (GenParams::tf_*)
-    if (op == CONV_OP_FWD) return IC % 32 == 0;
-    return IC % 32 == 0 && OC % 32 == 0;
+    // the REDUCTION channels of fwd (IC) and dX (OC) need only the ABI's multiple of 4: their last
+    // 32-channel block is completed by the TMA's out-of-bounds zero fill (A and B alike; the W' plane is
+    // zero-padded by wx_prep_kernel).  The GEMM-column channels of dX (IC, an MN-major 32-channel view)
+    // and both channel extents of dW still need multiples of 32.
+    if (op == CONV_OP_FWD) return true;
+    // ragged GEMM-column channels are padded to 32: below 16 channels (the RGB stems) that wastes >= 2x
+    // of every MMA and B box, so those stay on the GENERIC / DIRECT variants
+    if (op == CONV_OP_BWD_DATA) return IC % 32 == 0 || IC >= 16;  // IC % 32 != 0: TmaParams::dx_ragged
+    return (IC % 32 == 0 || IC >= 16) && (OC % 32 == 0 || OC >= 16);  // dW: dw_a_ragged / dw_b_ragged, dw_icp
 }
 
 int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3& grid, char* err, size_t errlen) {
@@ -171,9 +173,9 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
         return CONV_EUNSUPPORTED;
     }
     if (op == CONV_OP_FWD) {
-        tp.CB = g.IC / 32;
+        tp.CB = (g.IC + 31) / 32;
     } else if (op == CONV_OP_BWD_DATA) {
-        tp.CB = g.OC / 32;
+        tp.CB = (g.OC + 31) / 32;
     }
     // CTA pairs (cta_group::2): fwd / dx in 3xTF32 when 256-row pair tiles (two 128-image blocks at
     // one position) tile every phase exactly; dW (not transposed) when OC is a multiple of 256
@@ -210,6 +212,17 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
         tp.csk = g.csk;
         grid = dim3(tp.work, 1, 1);
     }
+    // fast divisors for TileInfo::init (after every m_tiles / n_tiles / phase_tile0 adjustment above)
+    tp.fd_ntiles = make_fastdiv(tp.n_tiles > 0 ? tp.n_tiles : 1);
+    tp.fd_csk = make_fastdiv(tp.csk > 0 ? tp.csk : 1);
+    tp.fd_splits = make_fastdiv(g.splits > 0 ? g.splits : 1);
+    tp.fd_mtiles = make_fastdiv(tp.m_tiles > 0 ? tp.m_tiles : 1);
+    tp.fd_CB = make_fastdiv(tp.CB > 0 ? tp.CB : 1);
+    for (int k = 0; k < kMaxPhases; ++k) {
+        int P = g.OH * g.OW;
+        if (op == CONV_OP_BWD_DATA && k < g.nphase) P = g.phase_IHp[k] * g.phase_IWp[k];
+        tp.fd_P[k] = make_fastdiv(P > 0 ? P : 1);
+    }
     if (op == CONV_OP_FWD || op == CONV_OP_BWD_DATA) {
     } else {
         tp.NB32 = g.N / 32;
@@ -227,11 +240,13 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
             tp.a_boxes = 128 / tp.a_box_cols;
         } else {
             const int bnc = tp.pair ? BN / 2 : BN;  // B columns staged per CTA
-            tp.b_box_cols = gcd(bnc, g.IC);
+            const int cpt = g.dw_icp ? g.dw_icp : g.IC;  // GEMM columns per tap
+            tp.b_box_cols = g.dw_icp ? 32 : gcd(bnc, g.IC);
             tp.b_boxes = bnc / tp.b_box_cols;
-            if (g.IC % BN == 0) tp.dw_tap_tiles = g.IC / BN;  // n-tiles never straddle a tap
+            if (cpt % BN == 0) tp.dw_tap_tiles = cpt / BN;  // n-tiles never straddle a tap
         }
     }
+    tp.fd_dwtap = make_fastdiv(tp.dw_tap_tiles > 0 ? tp.dw_tap_tiles : 1);
     return CONV_OK;
 }
 
@@ -254,9 +269,16 @@ int tma_launch(int op, int BN, int planes, const GenParams& g, TmaParams& tp, di
         uint64_t da[4] = {OC, OW, OH, N}, sa[3] = {OC * 4, OW * OC * 4, OH * OW * OC * 4};
         uint32_t ba[4] = {32, 1, 1, (uint32_t)tp.G};
         ok &= encode(&tp.mapA, g.A, 4, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B);
-        uint64_t db[4] = {32, OC, IC / 32, T}, sb[3] = {T * IC * 4, 128, IC * 4};
-        uint32_t bb[4] = {32, 32, (uint32_t)((tp.pair ? BN / 2 : BN) / 32), 1};
-        ok &= encode(&tp.mapB, g.B, 4, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+        if (IC % 32 == 0) {
+            uint64_t db[4] = {32, OC, IC / 32, T}, sb[3] = {T * IC * 4, 128, IC * 4};
+            uint32_t bb[4] = {32, 32, (uint32_t)((tp.pair ? BN / 2 : BN) / 32), 1};
+            ok &= encode(&tp.mapB, g.B, 4, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+        } else {  // ragged IC: W viewed (IC, OC, T), box (32 ic, 32 oc, 1) per 32-column block
+            tp.dx_ragged = 1;
+            uint64_t db[3] = {IC, OC, T}, sb[2] = {T * IC * 4, IC * 4};
+            uint32_t bb[3] = {32, 32, 1};
+            ok &= encode(&tp.mapB, g.B, 3, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+        }
         if (planes == 2) ok &= g.Bx && tma_encode_wx(&tp.mapBx, g.Bx, (int)IC, (int)OC, (int)T, tp.pair ? BN / 2 : BN);
     } else if (g.dwt) {
         // transposed dW: A = X viewed (32 ic, N, IC/32, IW, IH), B = dY viewed (32 oc, N, OC/32, OH*OW)
@@ -267,13 +289,29 @@ int tma_launch(int op, int BN, int planes, const GenParams& g, TmaParams& tp, di
         uint32_t bb[4] = {32, 32, (uint32_t)(BN / 32), 1};
         ok &= encode(&tp.mapB, g.A, 4, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     } else {
-        // A = dY viewed (32 oc, N, OC/32, OH*OW), MN-major; B = X viewed (32 ic, N, IC/32, IW, IH), MN-major
-        uint64_t da[4] = {32, N, OC / 32, OH * OW}, sa[3] = {OH * OW * OC * 4, 128, OC * 4};
-        uint32_t ba[4] = {32, 32, 4, 1};
-        ok &= encode(&tp.mapA, g.A, 4, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-        uint64_t db[5] = {32, N, IC / 32, IW, IH}, sb[4] = {IH * IW * IC * 4, 128, IC * 4, IW * IC * 4};
-        uint32_t bb[5] = {32, 32, (uint32_t)(tp.b_box_cols / 32), 1, 1};
-        ok &= encode(&tp.mapB, g.B, 5, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+        // A = dY viewed (32 oc, N, OC/32, OH*OW), MN-major; B = X viewed (32 ic, N, IC/32, IW, IH), MN-major.
+        // Ragged channel extents: views with the whole channel extent innermost, one 32-channel box at
+        // a time (the TMA zero-fills channels past the extent)
+        if (OC % 32 == 0) {
+            uint64_t da[4] = {32, N, OC / 32, OH * OW}, sa[3] = {OH * OW * OC * 4, 128, OC * 4};
+            uint32_t ba[4] = {32, 32, 4, 1};
+            ok &= encode(&tp.mapA, g.A, 4, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+        } else {
+            tp.dw_a_ragged = 1;
+            uint64_t da[3] = {OC, N, OH * OW}, sa[2] = {OH * OW * OC * 4, OC * 4};
+            uint32_t ba[3] = {32, 32, 1};
+            ok &= encode(&tp.mapA, g.A, 3, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+        }
+        if (IC % 32 == 0) {
+            uint64_t db[5] = {32, N, IC / 32, IW, IH}, sb[4] = {IH * IW * IC * 4, 128, IC * 4, IW * IC * 4};
+            uint32_t bb[5] = {32, 32, (uint32_t)(tp.b_box_cols / 32), 1, 1};
+            ok &= encode(&tp.mapB, g.B, 5, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+        } else {
+            tp.dw_b_ragged = 1;
+            uint64_t db[4] = {IC, N, IW, IH}, sb[3] = {IH * IW * IC * 4, IC * 4, IW * IC * 4};
+            uint32_t bb[4] = {32, 32, 1, 1};
+            ok &= encode(&tp.mapB, g.B, 4, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+        }
     }
     if (!ok) {
         snprintf(err, errlen, "cuTensorMapEncodeTiled failed (op %d)", op);

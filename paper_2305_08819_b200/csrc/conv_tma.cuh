@@ -60,6 +60,15 @@ struct __align__(64) TmaParams {
     int work;        // m_tiles * splits * n_tiles
     int csk;         // fwd / dx: cluster split-K (GenParams::csk): one work item per CTA, the csk splits of a
                      // tile are the CTAs of one cluster, partials reduced through DSMEM (csk_reduce)
+    // host-built fast divisors for TileInfo::init: a generic 32-bit division is a ~150-cycle dependent
+    // I2F / MUFU.RCP / F2I chain, and the ~10 of them per work item kept every role ~3800 cycles in its
+    // first TileInfo::init (smconv_set_trace, r02j) -- the TMA producer's first load waited on it
+    FastDiv fd_ntiles, fd_csk, fd_splits, fd_mtiles, fd_CB, fd_dwtap;
+    FastDiv fd_P[kMaxPhases];  // positions per (phase) map: fwd / dW OH*OW, dX phase IHp*IWp
+    int dx_ragged;  // dX with IC % 32 != 0: B = W viewed (IC, OC, T), one (32 ic, 32 oc) box per 32-column
+                    // block (the TMA zero-fills ic >= IC) instead of one 4-D box of BNC / 32 blocks
+    int dw_a_ragged;  // dW with OC % 32 != 0: A = dY viewed (OC, N, P), 4 boxes (32 oc, 32 n, 1) per k-block
+    int dw_b_ragged;  // dW with IC % 32 != 0: B = X viewed (IC, N, IW, IH), boxes (32 ic, 32 n, 1, 1)
 };
 
 template <int OP, int BN, int PLANES, bool PAIR = false>
@@ -111,6 +120,7 @@ struct TmaAux {
     uint64_t full[8], conv[8], empty[8], tfree[8];
     uint64_t tfull[2], tempty[2];
     uint32_t tmem_base;
+    int sink;              // param_warm
     int4 ptaps[kMaxTaps];  // producer-private per-tile tap list / X-box geometry
 };
 
@@ -155,24 +165,25 @@ struct TileInfo {
     int vr_lo, vr_hi, vc_lo, vc_hi;  // dw single-tap tiles: output rows / cols whose source is in range
 
     SMCONV_DEV void init(const TmaParams& tp, const GenParams& p, int w, int rank = 0) {
-        int nt = w % tp.n_tiles;
-        int rest = w / tp.n_tiles;
+        auto dv = [](int a, const FastDiv& f) { return (int)fdiv((uint32_t)a, f); };
+        int rest = dv(w, tp.fd_ntiles);
+        int nt = w - rest * tp.n_tiles;
         int mt;
         if (OP != OP_DW && OP != OP_DWT && tp.csk) {
             // cluster split-K: the splits of one tile are consecutive CTAs (one cluster)
-            split = w % tp.csk;
-            const int tile = w / tp.csk;
-            nt = tile % tp.n_tiles;
-            mt = tile / tp.n_tiles;
+            const int tile = dv(w, tp.fd_csk);
+            split = w - tile * tp.csk;
+            mt = dv(tile, tp.fd_ntiles);
+            nt = tile - mt * tp.n_tiles;
         } else if (OP == OP_DW || OP == OP_DWT) {
             // split (pixel range) outermost: all (m, n) tiles of one pixel range run together, so
             // that range's dY and X are read from HBM once and re-used from L2 by every tile
             // (m-tile-major order re-read them once per m-tile: 11.3 GB vs 2.1 GB compulsory, l1)
-            mt = rest % tp.m_tiles;
-            split = rest / tp.m_tiles;
+            split = dv(rest, tp.fd_mtiles);
+            mt = rest - split * tp.m_tiles;
         } else {
-            split = rest % p.splits;
-            mt = rest / p.splits;
+            mt = dv(rest, tp.fd_splits);
+            split = rest - mt * p.splits;
         }
         phase = 0;
         if (OP == OP_DX) {
@@ -191,7 +202,7 @@ struct TileInfo {
             // neighbouring positions of the same images, so the 3x3 taps' source rows are reused
             // from L2 instead of re-read from HBM (a position-major walk thrashed L2: 3x X reads)
             const int P = OP == OP_DX ? p.phase_IHp[phase] * p.phase_IWp[phase] : p.OH * p.OW;
-            const int ib = mt / P, pos = mt - ib * P;
+            const int ib = dv(mt, tp.fd_P[OP == OP_DX ? phase : 0]), pos = mt - ib * P;
             // pair tiles: the two CTAs take image blocks 2*ib and 2*ib+1 at the same position, so
             // both halves of the M = 256 tile have the same taps (one shared k-loop)
             m0 = tp.pair ? pos * p.N + (2 * ib + rank) * 128 : pos * p.N + ib * 128;
@@ -200,7 +211,7 @@ struct TileInfo {
         ngrp = 0;
         if (!DWK) {
             const int Mrows = OP == OP_DX ? p.phase_IHp[phase] * p.phase_IWp[phase] * p.N : p.M;
-            ngrp = 128 / tp.G;
+            ngrp = tp.G == 128 ? 1 : 4;  // G is 128 or 32
 #pragma unroll
             for (int g = 0; g < 4; ++g) {  // static indexing keeps grp[] in registers
                 if (g >= ngrp) break;
@@ -219,7 +230,7 @@ struct TileInfo {
             kb_end = min(nkb, kb_begin + p.kb_per_split);
         } else {
             nkb = ntaps(p) * tp.CB;
-            const int per = (nkb + p.splits - 1) / p.splits;
+            const int per = dv(nkb + p.splits - 1, tp.fd_splits);
             kb_begin = split * per;
             kb_end = min(nkb, kb_begin + per);
         }
@@ -229,7 +240,7 @@ struct TileInfo {
         if (OP == OP_DW && tp.dw_tap_tiles > 0 && nkb_eff > 0) {
             // a single-tap tile gets only zeros from the positions whose source pixel is padding
             // (4x4 maps: 7 of 16 positions for a corner tap): those k-blocks are not issued at all
-            const int tap = n0 / tp.dw_tap_tiles, fh = tap / p.FW, fw = tap - fh * p.FW;
+            const int tap = dv(n0, tp.fd_dwtap), fh = dv(tap, p.fd_FW), fw = tap - fh * p.FW;
             auto fdiv = [](int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
             vr_lo = max(0, -fdiv(fh - p.ph, p.sh));  // ceil((ph - fh) / sh)
             vr_hi = min(p.OH, fdiv(p.IH - 1 + p.ph - fh, p.sh) + 1);
@@ -239,7 +250,7 @@ struct TileInfo {
             if (vc_hi < vc_lo) vc_hi = vc_lo;
             const int P = p.OH * p.OW, nvw = vc_hi - vc_lo, V = (vr_hi - vr_lo) * nvw;
             auto cnt = [&](int k) {  // valid k-blocks below k (k-block = image block x position)
-                const int nb = k / P, pp = k - nb * P, r = pp / p.OW, c = pp - r * p.OW;
+                const int nb = dv(k, tp.fd_P[0]), pp = k - nb * P, r = dv(pp, p.fd_OW), c = pp - r * p.OW;
                 const int rb = min(max(r, vr_lo), vr_hi) - vr_lo;
                 const int cb = (r >= vr_lo && r < vr_hi) ? min(max(c, vc_lo), vc_hi) - vc_lo : 0;
                 return nb * V + rb * nvw + cb;
@@ -284,6 +295,54 @@ struct TileInfo {
     }
 };
 
+// In-cluster split-K reduction: CTA `crank` of the S-CTA cluster sums rows [crank*128/S, (crank+1)*128/S)
+// of the tile over the S partials held in the cluster's shared memories ([128][PSTRIDE] fp32 each), in
+// rank order (fixed: deterministic), and stores them.  Item = (row, 4 columns); consecutive threads take
+// consecutive column quads of a row (coalesced 16-B stores).  16 / S items per thread are loaded before
+// any is summed: 16 DSMEM loads in flight per thread (one item at a time left the reduce latency-bound,
+// ~900 cycles per round trip: 11.6k of the 46k cycles of VGG conv6, trace r02i -> 6.5k, r02k).  Pushing
+// the partial rows to their owners with remote stores from the epilogue instead was slower (15k cycles
+// of remote stores per CTA, r02m/r02n: a lane holds a row, so a warp's stores scatter over 32 rows).
+template <int OP, int BN, int PSTRIDE, int S>
+SMCONV_DEV void csk_reduce(const TmaParams& tp, const GenParams& p, uint32_t tiles_addr, int crank, int tid,
+                           int nthreads) {
+    TileInfo<OP> ti;
+    ti.init(tp, p, blockIdx.x, 0);
+    constexpr int ROWS = 128 / S, C4 = BN / 4, ITEMS = ROWS * C4, UNR = 16 / S;
+    const int n0 = ti.n0 * BN;
+    for (int base = tid; base < ITEMS; base += nthreads * UNR) {
+        float4 v[UNR][S];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int it = base + u * nthreads;
+            if (it < ITEMS) {
+                const int rr = crank * ROWS + it / C4, c4 = it % C4;
+                const uint32_t la = tiles_addr + (uint32_t)((rr * PSTRIDE + 4 * c4) * 4);
+#pragma unroll
+                for (int q = 0; q < S; ++q) v[u][q] = ld_cluster_f4(la, (uint32_t)q);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int it = base + u * nthreads;
+            if (it >= ITEMS) break;
+            const int rr = crank * ROWS + it / C4, c4 = it % C4;
+            const int col = n0 + 4 * c4;
+            const RowInfo ri = row_info<OP>(p, ti.phase, ti.m0 + rr);
+            if (!ri.ok || col >= p.Ngemm) continue;
+            float4 a = v[u][0];
+#pragma unroll
+            for (int q = 1; q < S; ++q) {
+                a.x += v[u][q].x;
+                a.y += v[u][q].y;
+                a.z += v[u][q].z;
+                a.w += v[u][q].w;
+            }
+            *reinterpret_cast<float4*>(p.out + (long long)ri.orow * p.Ngemm + col) = a;
+        }
+    }
+}
+
 template <int OP, int BN, int PLANES, bool PAIR = false>
 __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
     conv_tma_kernel(const __grid_constant__ TmaParams tp, const __grid_constant__ GenParams p) {
@@ -301,6 +360,16 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
     const int rank = PAIR ? (int)cluster_ctarank() : 0;
     const int wfirst = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
     const int wstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    const uint32_t csk_rank = (!C::IS_DW && !PAIR && tp.csk) ? cluster_ctarank() : 0u;
+    param_warm(p, tid, &aux->sink);
+    param_warm(tp, tid - param_lines<GenParams>(), &aux->sink);
+    unsigned long long* const trc = p.trace;
+    if (trc && tid == 0) {
+        trace_mark(trc, 0);
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        trc[blockIdx.x * 16 + 15] = gt;
+    }
 
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
@@ -331,6 +400,9 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
     if (PAIR) cluster_sync_all();  // the peer's barriers exist before any remote arrival
     tc_fence_after();
     const uint32_t tmem = aux->tmem_base;
+    if (tid == 0) trace_mark(trc, 1);
+    pdl_trigger();
+    pdl_wait();  // launch.cuh: no global-memory access before the previous kernels completed
 
     if (warp == C::TMA_W) {
         // ======================= TMA producer
@@ -344,6 +416,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             for (int w = wfirst; w < tp.work; w += wstep) {
                 TileInfo<OP> ti;
                 ti.init(tp, p, w, rank);
+                if (trc && lane == 0 && w == wfirst) trace_mark(trc, 3);
                 const int n0 = ti.n0 * BN;
                 const int nkb = ti.kb_end - ti.kb_begin;
                 if (ti.nkb_eff <= 0) continue;
@@ -354,7 +427,8 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                         for (int kw = 0; kw < p.tf_n[ph_][1]; ++kw)
                             if (ti.tap_valid(p, kh, kw, &taps[nt])) ++nt;  // same value from every lane
                     __syncwarp();
-                    int j = ti.kb_begin / tp.CB, cb = ti.kb_begin - j * tp.CB;
+                    if (trc && lane == 0 && w == wfirst) trace_mark(trc, 12);
+                    int j = (int)fdiv((uint32_t)ti.kb_begin, tp.fd_CB), cb = ti.kb_begin - j * tp.CB;
                     int4 tap = taps[j];
                     for (int it = 0; it < nkb; ++it) {
                         if (r > 0) {
@@ -363,6 +437,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                         }
                         const uint32_t sA = tiles_addr + s * C::STAGE_BYTES;
                         const uint32_t sB = sA + C::B_OFF;
+                        if (trc && lane == 0 && r == 0 && s == 0) trace_mark(trc, 2);
                         if (elect_one()) {
                             mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + (C::HYB ? 2 : 1) * C::B_BYTES);
 #pragma unroll
@@ -370,8 +445,15 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                                 if (g < ti.ngrp) tma_load_4d(sA + g * tp.G * 128, &tp.mapA, &aux->full[s], cb * 32,
                                             ti.grp[g].y + tap.y, ti.grp[g].x + tap.x, ti.grp[g].z);
                             const int nb0 = n0 + rank * C::BNC;  // this CTA's half of B (pairs)
-                            if (OP == OP_FWD) tma_load_3d(sB, &tp.mapB, &aux->full[s], cb * 32, tap.z, nb0);
-                            else tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, cb * 32, nb0 / 32, tap.z);
+                            if (OP == OP_FWD) {
+                                tma_load_3d(sB, &tp.mapB, &aux->full[s], cb * 32, tap.z, nb0);
+                            } else if (tp.dx_ragged) {
+#pragma unroll 1
+                                for (int j = 0; j < C::BNC / 32; ++j)
+                                    tma_load_3d(sB + j * 4096, &tp.mapB, &aux->full[s], nb0 + 32 * j, cb * 32, tap.z);
+                            } else {
+                                tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, cb * 32, nb0 / 32, tap.z);
+                            }
                             if (C::HYB) tma_load_4d(sB + C::B_BYTES, &tp.mapBx, &aux->full[s], 0, cb, nb0, tap.z);
                         }
                         __syncwarp();
@@ -387,8 +469,8 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                 } else {
                     // image-block-major reduction order (k-block = 32 images at one position)
                     const int P = p.OH * p.OW;
-                    int nb = ti.kb_begin / P, pos = ti.kb_begin - nb * P;
-                    int oh = pos / p.OW, ow = pos - oh * p.OW;
+                    int nb = (int)fdiv((uint32_t)ti.kb_begin, tp.fd_P[0]), pos = ti.kb_begin - nb * P;
+                    int oh = (int)fdiv((uint32_t)pos, p.fd_OW), ow = pos - oh * p.OW;
                     // X boxes of this tile (dw: B side; dwT: A side): tap offsets and channel block
                     const int nboxes = OP == OP_DWT ? tp.a_boxes : tp.b_boxes;
                     const int bcols = OP == OP_DWT ? tp.a_box_cols : tp.b_box_cols;
@@ -398,7 +480,8 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     for (int b = 0; b < nboxes; ++b) {
                         const int c0 = base + b * bcols;
                         if (c0 >= lim) break;
-                        const int tp_ = c0 / p.IC, icb = (c0 - tp_ * p.IC) / 32;
+                        const int cpt = (OP == OP_DW && p.dw_icp) ? p.dw_icp : p.IC;  // GEMM columns per tap
+                        const int tp_ = c0 / cpt, icb = (c0 - tp_ * cpt) / 32;
                         const int fh_ = tp_ / p.FW, fw_ = tp_ - fh_ * p.FW;
                         taps[b] = make_int4(fw_ - p.pw, fh_ - p.ph, icb, 0);  // same value from every lane
                         ++nbox;
@@ -430,11 +513,23 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                         const int iw0 = ow * p.sw, ih0 = oh * p.sh;
                         if (elect_one()) {
                             mbar_arrive_expect_tx(&aux->full[s], tx);
-                            for (int b = 0; b < nbox; ++b)
-                                tma_load_5d(sX + b * bcols * 128, OP == OP_DWT ? &tp.mapA : &tp.mapB, &aux->full[s],
-                                            0, nb * 32, taps[b].z, iw0 + taps[b].x, ih0 + taps[b].y);
-                            if (OP == OP_DWT) tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, nb * 32, n0 / 32, pos);
-                            else tma_load_4d(sA, &tp.mapA, &aux->full[s], 0, nb * 32, ti.m0 / 32, pos);
+                            for (int b = 0; b < nbox; ++b) {
+                                if (OP == OP_DW && tp.dw_b_ragged)  // (32 ic, 32 n, 1, 1); ic >= IC zero-filled
+                                    tma_load_4d(sX + b * bcols * 128, &tp.mapB, &aux->full[s], taps[b].z * 32, nb * 32,
+                                                iw0 + taps[b].x, ih0 + taps[b].y);
+                                else
+                                    tma_load_5d(sX + b * bcols * 128, OP == OP_DWT ? &tp.mapA : &tp.mapB, &aux->full[s],
+                                                0, nb * 32, taps[b].z, iw0 + taps[b].x, ih0 + taps[b].y);
+                            }
+                            if (OP == OP_DWT) {
+                                tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, nb * 32, n0 / 32, pos);
+                            } else if (tp.dw_a_ragged) {  // 4 x (32 oc, 32 n, 1); oc >= OC zero-filled
+#pragma unroll 1
+                                for (int j = 0; j < 4; ++j)
+                                    tma_load_3d(sA + j * 4096, &tp.mapA, &aux->full[s], ti.m0 + 32 * j, nb * 32, pos);
+                            } else {
+                                tma_load_4d(sA, &tp.mapA, &aux->full[s], 0, nb * 32, ti.m0 / 32, pos);
+                            }
                         }
                         __syncwarp();
                         if (++ow == p.OW) {
@@ -491,6 +586,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     const uint32_t d = tmem + (uint32_t)(buf * BN);
                     const uint64_t so = (uint64_t)(s * C::STAGE_BYTES) >> 4;
                     const bool last = (in_chunk + 1 == CHK || it == nkb - 1);
+                    if (trc && lane == 0 && q == 0) trace_mark(trc, 4);
                     if (elect_one()) {
 #pragma unroll
                         for (int g = 0; g < C::BK / 8; ++g) {
@@ -522,6 +618,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                                 else mma_bf16_ts(d, ax, bx0 + so + j * 2, IDESC_X, 1u);
                             }
                         }
+                        if (trc && last) trace_mark(trc, 5);
                         if (PAIR) {
                             mma2_commit_both(&aux->empty[s]);
                             mma2_commit_both(&aux->tfree[t]);
@@ -668,7 +765,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             long long obase = -1;
             if (OP == OP_DW) {
                 const int oc = ti.m0 + row;
-                if (oc < p.OC) obase = (long long)oc * p.Ngemm;
+                if (oc < p.OC) obase = (long long)oc * (p.dw_icp ? p.FH * p.FW * p.IC : p.Ngemm);
             } else if (OP == OP_DWT) {
                 const int m = ti.m0 + row;  // (tap, ic) index; dW[oc][m] at oc * M + m
                 if (m < p.M) obase = m;
@@ -706,6 +803,10 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     o[3 * (long long)p.M] = w4;
                 } else if (OP == OP_FWD && p.s2dx) {  // column (pi, pj, ic): dX row 2i'-2+pi
                     *reinterpret_cast<float4*>(outp + out_off(col)) = make_float4(x, y, z, w4);
+                } else if (OP == OP_DW && p.dw_icp) {  // padded (tap, ic) column: drop ic >= IC
+                    const int tap = (int)fdiv((uint32_t)col, p.fd_icp), ic = col - tap * p.dw_icp;
+                    if (ic < p.IC)
+                        *reinterpret_cast<float4*>(outp + obase + tap * p.IC + ic) = make_float4(x, y, z, w4);
                 } else {
                     *reinterpret_cast<float4*>(outp + obase + col) = make_float4(x, y, z, w4);
                 }
@@ -719,6 +820,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     if (PAIR) mbar_wait_cluster(&aux->tfull[buf], (c >> 1) & 1);
                     else mbar_wait(&aux->tfull[buf], (c >> 1) & 1);
                     tc_fence_after();
+                    if (trc && tid == 0) trace_mark(trc, 6);
 #pragma unroll
                     for (int c0 = 0; c0 < HALF; c0 += 16) {
                         uint32_t v[16];
@@ -763,33 +865,43 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     else mbar_wait(&aux->tfull[buf], (c >> 1) & 1);
                     tc_fence_after();
                 }
+                if (trc && tid == 0) trace_mark(trc, 6);
+                // up to 64 columns per TMEM round trip: 4 tcgen05.ld in flight, one wait (one load + wait
+                // per 16 columns made the epilogue of a 128 x 256 tile ~4k cycles of TMEM latency, r02k)
+                constexpr int CH = HALF < 64 ? HALF : 64;
 #pragma unroll 1
-                for (int c0 = 0; c0 < HALF; c0 += 16) {
-                    uint32_t v[16];
+                for (int c0 = 0; c0 < HALF; c0 += CH) {
+                    uint32_t v[CH];
                     if (nch > 0) {
-                        tmem_ld_32x32b_x16(tmem + lane_addr + (uint32_t)(buf * BN + half * HALF + c0), v);
+#pragma unroll
+                        for (int q = 0; q < CH / 16; ++q)
+                            tmem_ld_32x32b_x16(tmem + lane_addr + (uint32_t)(buf * BN + half * HALF + c0 + 16 * q),
+                                               *reinterpret_cast<uint32_t(*)[16]>(&v[16 * q]));
                         tmem_ld_wait();
                     } else {
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) v[e] = 0u;
+                        for (int e = 0; e < CH; ++e) v[e] = 0u;
                     }
-                    if (!C::IS_DW && p.epi.mode != EPI_NONE) {
-                        const int col0 = n0 + half * HALF + c0;
-                        float f[16];
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
-                        epi_apply16(p.epi, f, obase >= 0 && col0 < p.Ngemm ? out_off(col0) : -1, col0, p.Ngemm, egrp,
-                                    lane);
+                    for (int q = 0; q < CH / 16; ++q) {
+                        const int col0 = n0 + half * HALF + c0 + 16 * q;
+                        if (!C::IS_DW && p.epi.mode != EPI_NONE) {
+                            float f[16];
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(f[e]);
-                    }
-                    if (obase >= 0) {
+                            for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[16 * q + e]);
+                            epi_apply16(p.epi, f, obase >= 0 && col0 < p.Ngemm ? out_off(col0) : -1, col0, p.Ngemm,
+                                        egrp, lane);
 #pragma unroll
-                        for (int e = 0; e < 16; e += 4) {
-                            const int col = n0 + half * HALF + c0 + e;
-                            if (col < p.Ngemm)
-                                st4(col, __uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
-                                    __uint_as_float(v[e + 3]));
+                            for (int e = 0; e < 16; ++e) v[16 * q + e] = __float_as_uint(f[e]);
+                        }
+                        if (obase >= 0) {
+#pragma unroll
+                            for (int e = 0; e < 16; e += 4) {
+                                const int col = col0 + e;
+                                if (col < p.Ngemm)
+                                    st4(col, __uint_as_float(v[16 * q + e]), __uint_as_float(v[16 * q + e + 1]),
+                                        __uint_as_float(v[16 * q + e + 2]), __uint_as_float(v[16 * q + e + 3]));
+                            }
                         }
                     }
                 }
@@ -802,43 +914,22 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
         }
     }
 
+    if (trc && tid == 0) trace_mark(trc, 7);
     tc_fence_before();
     __syncthreads();
+    if (tid == 0) trace_mark(trc, 8);
     if (!C::IS_DW && !PAIR && tp.csk) {
         // cluster split-K: every CTA of the cluster holds its partial of the same tile in shared memory
-        // [128 rows][PSTRIDE]; CTA r sums rows [r*128/S, (r+1)*128/S) over the S partials in rank order
-        // (fixed order: deterministic) and writes them.  One warp per row: 512-B / 1-KB row runs.
+        // [128 rows][PSTRIDE]; CTA r sums rows [r*128/S, (r+1)*128/S) over the S partials (csk_reduce)
         cluster_sync_all();  // release / acquire at cluster scope: all partials visible
-        const int S = tp.csk, crank = (int)cluster_ctarank();
-        TileInfo<OP> ti;
-        ti.init(tp, p, blockIdx.x, 0);
-        const int rows_per = 128 / S, n0 = ti.n0 * BN;
-        constexpr int NW = C::NTHREADS / 32, C4 = BN / 4;
-        for (int rr = crank * rows_per + warp; rr < (crank + 1) * rows_per; rr += NW) {
-            const RowInfo ri = row_info<OP>(p, ti.phase, ti.m0 + rr);
-            if (!ri.ok) continue;
-            float* orow = p.out + (long long)ri.orow * p.Ngemm;
-#pragma unroll
-            for (int c4 = lane; c4 < C4; c4 += 32) {
-                const int col = n0 + 4 * c4;
-                if (col >= p.Ngemm) continue;
-                const uint32_t la = tiles_addr + (uint32_t)((rr * C::PSTRIDE + 4 * c4) * 4);
-                float4 v[16];
-#pragma unroll
-                for (int q = 0; q < 16; ++q)
-                    if (q < S) v[q] = ld_cluster_f4(la, (uint32_t)q);
-                float4 a = v[0];
-#pragma unroll
-                for (int q = 1; q < 16; ++q)
-                    if (q < S) {
-                        a.x += v[q].x;
-                        a.y += v[q].y;
-                        a.z += v[q].z;
-                        a.w += v[q].w;
-                    }
-                *reinterpret_cast<float4*>(orow + col) = a;
-            }
+        if (tid == 0) trace_mark(trc, 9);
+        switch (tp.csk) {
+            case 2: csk_reduce<OP, BN, C::PSTRIDE, 2>(tp, p, tiles_addr, (int)csk_rank, tid, C::NTHREADS); break;
+            case 4: csk_reduce<OP, BN, C::PSTRIDE, 4>(tp, p, tiles_addr, (int)csk_rank, tid, C::NTHREADS); break;
+            case 8: csk_reduce<OP, BN, C::PSTRIDE, 8>(tp, p, tiles_addr, (int)csk_rank, tid, C::NTHREADS); break;
+            default: csk_reduce<OP, BN, C::PSTRIDE, 16>(tp, p, tiles_addr, (int)csk_rank, tid, C::NTHREADS); break;
         }
+        if (tid == 0) trace_mark(trc, 10);
         cluster_sync_all();  // no CTA exits while a peer still reads its shared memory
     }
     if (PAIR) cluster_sync_all();  // the peer's MMAs / arrivals are done before TMEM is released
@@ -847,6 +938,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
         if (PAIR) tmem_dealloc2(tmem, C::TMEM_COLS);
         else tmem_dealloc(tmem, C::TMEM_COLS);
     }
+    if (tid == 0) trace_mark(trc, 11);
 }
 
 // ------------------------------------------------------------------ host side

@@ -115,6 +115,8 @@ SMCONV_DEV void epi_apply16(const EpiArgs& e, float (&v)[16], long long addr, in
 template <int UNUSED = 0>
 __global__ void __launch_bounds__(256) epi_pass_kernel(const float* src, float* out, long long rows, int C,
                                                        EpiArgs e) {
+    pdl_trigger();
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
     const int chunks = (C + 15) / 16;
@@ -150,6 +152,8 @@ __global__ void __launch_bounds__(256) epi_pass_kernel(const float* src, float* 
 template <int UNUSED = 0>
 __global__ void __launch_bounds__(256) epi_stats_stage1(const float* __restrict__ part, double* __restrict__ part2,
                                                         int ngroups, int ncols, int nchunks) {
+    pdl_trigger();
+    pdl_wait();
     const int per = (ngroups + nchunks - 1) / nchunks;
     const long long n = 2LL * nchunks * ncols;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -176,6 +180,8 @@ __global__ void __launch_bounds__(256) epi_stats_stage1(const float* __restrict_
 template <int UNUSED = 0>
 __global__ void __launch_bounds__(256) epi_stats_stage2(const double* __restrict__ part2, double* __restrict__ stats,
                                                         int ncols, int nchunks, int C) {
+    pdl_trigger();
+    pdl_wait();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * C; i += gridDim.x * blockDim.x) {
         const int s = i / C, ch = i - s * C;
         double acc = 0.0;

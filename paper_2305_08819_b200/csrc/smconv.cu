@@ -19,6 +19,7 @@
 #include "../../include/smgemm.h"
 #include "conv_gen.cuh"
 #include "conv_strip.cuh"
+#include "launch.cuh"
 
 namespace smconv {  // conv_direct.cu
 bool direct_supported(int op, int IC, int OC, int FH, int FW, int OW, int sw);
@@ -46,6 +47,7 @@ int fail(int code, const char* fmt, ...) {
     return code;
 }
 
+std::atomic<unsigned long long*> g_trace{nullptr};  // smconv_set_trace (experiments)
 std::atomic<int> g_force[3] = {{CONV_VARIANT_AUTO}, {CONV_VARIANT_AUTO}, {CONV_VARIANT_AUTO}};
 std::once_flag g_env_once;
 
@@ -251,6 +253,8 @@ int make_plan_s2dx(const Dims& d, int math, Plan& pl) {
 // W2[(pi, pj, ic)][a][b][oc] = W[oc][fh(pi, a)][fw(pj, b)][ic], 0 where the phase has no such tap
 __global__ void __launch_bounds__(256) w2_build_kernel(const float* __restrict__ W, float* __restrict__ W2, int IC,
                                                        int OC) {
+    pdl_trigger();
+    pdl_wait();
     const long long n = 16LL * IC * OC;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
         const int oc = (int)(e % OC);
@@ -444,7 +448,8 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
         out_elems = (long long)d.N * d.IH * d.IW * d.IC;
         const int taps_per_phase = (est_taps(d) + d.sh * d.sw - 1) / (d.sh * d.sw) * 1;
         nkb_est = ((taps_per_phase < 1 ? 1 : taps_per_phase) * d.OC + 31) / 32;
-    } else if (pl.variant == CONV_VARIANT_TMA && d.OC <= 64 && d.FH * d.FW * d.IC >= 128) {
+    } else if (pl.variant == CONV_VARIANT_TMA && d.OC <= 64 && d.FH * d.FW * d.IC >= 128 && d.IC % 32 == 0 &&
+               d.OC % 32 == 0) {
         // OC <= 64 would leave half of every 128-row MMA empty: transpose the dW GEMM to
         // (tap, IC) rows x OC columns (TMA variant only)
         g.dwt = 1;
@@ -459,6 +464,11 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
     } else {
         g.M = d.OC;
         g.Ngemm = d.FH * d.FW * d.IC;
+        if (pl.variant == CONV_VARIANT_TMA && d.IC % 32) {  // (tap, ic) columns with ic padded to 32
+            g.dw_icp = (d.IC + 31) / 32 * 32;
+            g.fd_icp = make_fastdiv(g.dw_icp);
+            g.Ngemm = d.FH * d.FW * g.dw_icp;
+        }
         g.P = d.N * d.OH * d.OW;
         m_tiles = (d.OC + 127) / 128;
         pl.BN = bn_for(g.Ngemm);
@@ -525,8 +535,13 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
             n_tiles = (g.Ngemm + pl.BN - 1) / pl.BN;
         }
         const int t2 = m_tiles * n_tiles;
+        // co-resident clusters of S CTAs (1 CTA per SM, ~200 KB smem): 8 GPCs of ~18 SMs hold 15 clusters
+        // of 8 (ncu launch__cluster_max_active, r02d); a grid of 16 clusters ran in two waves (VGG conv11
+        // 23.4 us at S = 8 vs 13.8 us at S = 4, r02h), so S is capped to keep one wave
+        auto max_clusters = [](int S2) { return S2 <= 2 ? 74 : S2 <= 4 ? 32 : S2 <= 8 ? 15 : 7; };
         int S = 1;
-        for (int S2 = 2; S2 <= g_csk_max && t2 * S2 <= (S2 >= 4 ? 128 : kSMs) && 2 * S2 <= nkb_est; S2 *= 2) S = S2;
+        for (int S2 = 2; S2 <= g_csk_max && t2 * S2 <= kSMs && t2 <= max_clusters(S2) && 2 * S2 <= nkb_est; S2 *= 2)
+            S = S2;
         if (S >= 2) {
             splits = S;
             g.csk = S;
@@ -560,7 +575,8 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
         (pl.variant == CONV_VARIANT_TMA || pl.variant == CONV_VARIANT_STRIP)) {
         // W' = [bf16(w_lo) | bf16(w)] per (tap, GEMM column, 32-k block): 4 bytes per weight
         pl.wx_off = (pl.ws_bytes + 1023) & ~(size_t)1023;
-        pl.wx_bytes = (size_t)d.FH * d.FW * d.IC * d.OC * 4;
+        const int Kp = ((op == CONV_OP_FWD ? d.IC : d.OC) + 31) / 32 * 32;  // reduction channels padded to 32
+        pl.wx_bytes = (size_t)d.FH * d.FW * (op == CONV_OP_FWD ? d.OC : d.IC) * Kp * 4;
         pl.ws_bytes = pl.wx_off + pl.wx_bytes;
     }
     pl.grid = dim3(m_tiles, n_tiles, splits);
@@ -586,7 +602,8 @@ int launch_gen_t(const GenParams& g, dim3 grid, cudaStream_t st) {
                         cudaGetErrorString(cudaGetLastError()));
         attr_done.fetch_or(bit);
     }
-    conv_gen_kernel<OP, BN, PLANES><<<grid, C::NTHREADS, C::SMEM_BYTES, st>>>(g);
+    if (launch_k(conv_gen_kernel<OP, BN, PLANES>, grid, dim3(C::NTHREADS), C::SMEM_BYTES, st, 1, g) != cudaSuccess)
+        return fail(CONV_ECUDA, "cudaLaunchKernelEx(generic): %s", cudaGetErrorString(cudaGetLastError()));
     return CONV_OK;
 }
 
@@ -610,7 +627,11 @@ int launch_gen_op(const Plan& pl, const GenParams& g, cudaStream_t st) {
 // column n / reduction index k are (oc, ic) for fwd and (ic, oc) for dX.  One thread per row.
 __global__ void __launch_bounds__(256) wx_prep_kernel(const float* __restrict__ W, uint4* __restrict__ Wx, int OC,
                                                       int IC, int T, int dx) {
-    const int Nn = dx ? IC : OC, Kc = dx ? OC : IC, CB = Kc / 32;
+    pdl_trigger();
+    pdl_wait();
+    // Kc need not be a multiple of 32 (GoogLeNet 16/24/48/112/...-channel layers): the last block's
+    // k >= Kc entries are zero, like the TMA's out-of-bounds fill of the matching A columns
+    const int Nn = dx ? IC : OC, Kc = dx ? OC : IC, CB = (Kc + 31) / 32;
     const long long rows = (long long)T * Nn * CB;
     for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows; r += (long long)gridDim.x * blockDim.x) {
         int tap, n, cb;
@@ -628,14 +649,17 @@ __global__ void __launch_bounds__(256) wx_prep_kernel(const float* __restrict__ 
         uint32_t lo[16], hi[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            float w0, w1;
-            if (dx) {
-                w0 = W[((size_t)(32 * cb + 2 * i) * T + tap) * IC + n];
-                w1 = W[((size_t)(32 * cb + 2 * i + 1) * T + tap) * IC + n];
-            } else {
-                const float2 v = *reinterpret_cast<const float2*>(W + ((size_t)n * T + tap) * IC + 32 * cb + 2 * i);
-                w0 = v.x;
-                w1 = v.y;
+            float w0 = 0.f, w1 = 0.f;
+            const int k = 32 * cb + 2 * i;  // Kc % 4 == 0: k and k + 1 are both in range or both out
+            if (k < Kc) {
+                if (dx) {
+                    w0 = W[((size_t)k * T + tap) * IC + n];
+                    w1 = W[((size_t)(k + 1) * T + tap) * IC + n];
+                } else {
+                    const float2 v = *reinterpret_cast<const float2*>(W + ((size_t)n * T + tap) * IC + k);
+                    w0 = v.x;
+                    w1 = v.y;
+                }
             }
             lo[i] = pack_bf16x2(w0 - __uint_as_float(__float_as_uint(w0) & 0xFFFFE000u),
                                 w1 - __uint_as_float(__float_as_uint(w1) & 0xFFFFE000u));
@@ -672,15 +696,17 @@ int finish_epi(int op, const Plan& pl, const float* conv_out, float* out, void* 
     if (!pl.epi_fused) {
         const long long items = (long long)pl.epi_ngroups * ((pl.epi_C + 15) / 16);
         const int blocks = (int)((items + 7) / 8 < kSMs * 8 ? (items + 7) / 8 : kSMs * 8);
-        epi_pass_kernel<0><<<blocks, 256, 0, st>>>(conv_out, out, pl.epi_rows, pl.epi_C, ea);
+        launch_k(epi_pass_kernel<0>, dim3(blocks), dim3(256), 0, st, 1, conv_out, out, pl.epi_rows, pl.epi_C, ea);
     }
     if (epi_has_stats(pl.epi)) {
         double* part2 = (double*)((char*)ws + pl.epi_part2_off);
         const long long n1 = 2LL * pl.epi_nchunks * pl.epi_ncols;
         const int b1 = (int)((n1 + 255) / 256 < kSMs * 8 ? (n1 + 255) / 256 : kSMs * 8);
-        epi_stats_stage1<0><<<b1, 256, 0, st>>>(ea.part, part2, pl.epi_ngroups, pl.epi_ncols, pl.epi_nchunks);
+        launch_k(epi_stats_stage1<0>, dim3(b1), dim3(256), 0, st, 1, (const float*)ea.part, part2, pl.epi_ngroups,
+                 pl.epi_ncols, pl.epi_nchunks);
         const int b2 = (2 * pl.epi_C + 255) / 256;
-        epi_stats_stage2<0><<<b2, 256, 0, st>>>(part2, ec.stats, pl.epi_ncols, pl.epi_nchunks, pl.epi_C);
+        launch_k(epi_stats_stage2<0>, dim3(b2), dim3(256), 0, st, 1, (const double*)part2, ec.stats, pl.epi_ncols,
+                 pl.epi_nchunks, pl.epi_C);
     }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: epilogue launch failed: %s", op_name(op), cudaGetErrorString(e));
@@ -703,6 +729,7 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
     const bool ws_split = pl.splits > 1 && !pl.gp.csk;
     g.out = ws_split ? (float*)ws : out;
     g.Bx = nullptr;
+    g.trace = g_trace.load();
     // pass form of the LEAKY_BWD modes: the conv (and its reduce / zero fill) write the staging buffer
     float* conv_out = (pl.epi && !pl.epi_fused && epi_reads_a(pl.epi)) ? (float*)((char*)ws + pl.epi_stage_off) : out;
     if (!ws_split) g.out = conv_out;
@@ -727,13 +754,13 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
         float* w2 = (float*)((char*)ws + pl.w2_off);
         const long long n = 16LL * d.IC * d.OC;
         const int blocks = (int)((n + 255) / 256 < kSMs * 8 ? (n + 255) / 256 : kSMs * 8);
-        w2_build_kernel<<<blocks, 256, 0, st>>>(B, w2, d.IC, d.OC);
+        launch_k(w2_build_kernel, dim3(blocks), dim3(256), 0, st, 1, B, w2, d.IC, d.OC);
         g.B = w2;
         if (pl.wx_bytes) {
             g.Bx = (char*)ws + pl.wx_off;
             const long long rows = 4LL * d.OC * 4 * d.IC / 32;
             const int bl = (int)((rows + 255) / 256 < kSMs * 4 ? (rows + 255) / 256 : kSMs * 4);
-            wx_prep_kernel<<<bl, 256, 0, st>>>(w2, (uint4*)g.Bx, 4 * d.IC, d.OC, 4, 0);
+            launch_k(wx_prep_kernel, dim3(bl), dim3(256), 0, st, 1, (const float*)w2, (uint4*)g.Bx, 4 * d.IC, d.OC, 4, 0);
         }
         TmaParams tp = pl.tp;
         rc = tma_launch(CONV_OP_FWD, pl.BN, pl.planes, g, tp, pl.grid, st, g_detail, sizeof g_detail);
@@ -747,9 +774,10 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
     }
     if (pl.wx_bytes) {
         g.Bx = (char*)ws + pl.wx_off;
-        const long long rows = (long long)d.FH * d.FW * d.IC * d.OC / 32;
+        const long long rows = (long long)pl.wx_bytes / 128;  // one 64-bf16 row per (tap, column, 32-k block)
         const int blocks = (int)((rows + 255) / 256 < kSMs * 4 ? (rows + 255) / 256 : kSMs * 4);
-        wx_prep_kernel<<<blocks, 256, 0, st>>>(B, (uint4*)g.Bx, d.OC, d.IC, d.FH * d.FW, op == CONV_OP_BWD_DATA);
+        launch_k(wx_prep_kernel, dim3(blocks), dim3(256), 0, st, 1, B, (uint4*)g.Bx, d.OC, d.IC, d.FH * d.FW,
+                 (int)(op == CONV_OP_BWD_DATA));
     }
     if (pl.variant == CONV_VARIANT_DIRECT) {
         rc = direct_launch(op, g, pl.splits, st, g_detail, sizeof g_detail);
@@ -774,14 +802,16 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
         const long long n4 = pl.out_elems / 4;
         int blocks = (int)((n4 + 255) / 256);
         if (blocks > kSMs * 8) blocks = kSMs * 8;
-        splitk_reduce_kernel<0><<<blocks, 256, 0, st>>>((const float4*)ws, (float4*)conv_out, n4, pl.splits, n4);
+        launch_k(splitk_reduce_kernel<0>, dim3(blocks), dim3(256), 0, st, 1, (const float4*)ws, (float4*)conv_out, n4,
+                 pl.splits, n4);
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: reduce launch failed: %s", op_name(op), cudaGetErrorString(e));
     }
     if (pl.zero_mask) {  // after the reduce: its workspace never held the empty phases
         const long long rows = (long long)d.N * d.IH;
         const int blocks = (int)(rows < kSMs * 8 ? rows : kSMs * 8);
-        zero_phases_kernel<0><<<blocks, 256, 0, st>>>((float4*)conv_out, (long long)d.N * d.IH, d.IC / 4, d.IH, d.IW, d.sh, d.sw,
+        launch_k(zero_phases_kernel<0>, dim3(blocks), dim3(256), 0, st, 1, (float4*)conv_out, (long long)d.N * d.IH,
+                 d.IC / 4, d.IH, d.IW, d.sh, d.sw,
                                                       pl.zero_mask);
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: zero-fill launch failed: %s", op_name(op), cudaGetErrorString(e));
@@ -1012,6 +1042,11 @@ int conv2d_epi_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int 
 }
 
 int smconv_set_pair(int on) { return tma_set_pair(on ? 1 : 0); }
+
+int smconv_set_trace(void* device_buf) {
+    g_trace.store((unsigned long long*)device_buf);
+    return CONV_OK;
+}
 
 int conv2d_force_variant(int op, int variant) {
     if (op < 0 || op > 2 || variant < 0 || variant > 5) return fail(CONV_EARG, "conv2d_force_variant: bad op/variant");

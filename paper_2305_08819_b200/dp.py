@@ -227,7 +227,7 @@ class ConvNetStep:
                     ws.data_ptr() if (ws is not None and b.ws_bytes[op]) else 0,
                     b.ws_bytes[op] if ws is not None else 0, stream)
 
-    def step(self, pg=None, events: Optional[list] = None, external_events: bool = False):
+    def step(self, pg=None, events: Optional[list] = None, external_events: bool = False, only=None):
         """Enqueue fwd for all layers, then dX/dW in reverse with bucketed async all-reduce.
         external_events: timing events that stay valid inside CUDA-graph capture."""
         torch = self.torch
@@ -235,7 +235,9 @@ class ConvNetStep:
         rec = events is not None
 
         def mark(key):
-            if rec:
+            # only: record just these (op, layer) calls (a CUDA event between two kernels also stops the
+            # second one from being scheduled early: programmatic dependent launch, csrc/launch.cuh)
+            if rec and (only is None or key[:2] in only):
                 e = torch.cuda.Event(enable_timing=True, external=True) if external_events else \
                     torch.cuda.Event(enable_timing=True)
                 e.record()

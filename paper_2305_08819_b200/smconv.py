@@ -26,7 +26,7 @@ EXPORTS = ("conv2d_out_hw", "conv2d_workspace_bytes", "conv2d_fwd", "conv2d_bwd_
 EPI_EXPORTS = ("conv2d_epi_workspace_bytes", "conv2d_fwd_epi", "conv2d_bwd_data_epi", "conv2d_epi_plan_describe")
 GEMM_EXPORTS = ("gemm_workspace_bytes", "gemm_matmul", "gemm_matmul_t1", "gemm_matmul_t2", "gemm_plan_describe")
 EXT_EXPORTS = ("conv2d_force_variant", "conv2d_plan_describe", "conv2d_plan_kernels", "smconv_selftest_host",
-               "smconv_probe_tf32")
+               "smconv_probe_tf32", "smconv_set_trace")
 
 
 class ConvError(RuntimeError):
@@ -90,6 +90,8 @@ def lib():
                 L.conv2d_bwd_data_epi.restype = I
                 L.conv2d_epi_plan_describe.argtypes = [I] * 14 + [ctypes.c_char_p, Z]
                 L.conv2d_epi_plan_describe.restype = I
+                L.smconv_set_trace.argtypes = [P]
+                L.smconv_set_trace.restype = I
                 L.smconv_probe_tf32.argtypes = [P]
                 L.smconv_probe_tf32.restype = I
                 _lib = L

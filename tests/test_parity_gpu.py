@@ -92,6 +92,13 @@ SWEEP = [
     (2, 13, 13, 4, 64, 11, 11, 4, 4, 5, 5),    # AlexNet conv1 11x11 s4
     (1, 3, 3, 8, 8, 3, 3, 1, 1, 4, 4),         # pad >= FH: many outputs only see padding
     (130, 2, 2, 32, 36, 3, 3, 1, 1, 1, 1),     # N = 130: tiles straddle positions
+    # channels that are not multiples of 32 on the TMA variant (TMA out-of-bounds fill pads the reduction
+    # channels; ragged GEMM-column channels: per-32-block boxes, padded dW columns)
+    (32, 7, 9, 20, 36, 3, 3, 1, 1, 1, 1),      # ragged everything, N % 32 == 0
+    (64, 6, 6, 48, 112, 5, 5, 1, 1, 2, 2),     # GoogLeNet-style 5x5
+    (32, 8, 8, 24, 16, 1, 1, 1, 1, 0, 0),      # 1x1 with 16 / 24 channels (GoogLeNet 5x5 reduce)
+    (256, 4, 4, 112, 208, 3, 3, 1, 1, 1, 1),   # CTA pairs with ragged channels
+    (32, 8, 8, 144, 48, 3, 3, 2, 2, 1, 1),     # stride-2 phases, ragged channels
 ]
 
 
