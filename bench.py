@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--bucket-mb", type=float, default=16.0)
+    ap.add_argument("--fused-allreduce", action="store_true",
+                    help="dW all-reduce inside the dW kernels through an NVLink multicast object "
+                         "(include/smconv_mcast.h; torch symmetric memory) instead of bucketed NCCL all-reduces")
     ap.add_argument("--epi", action="store_true",
                     help="fused epilogues (include/smconv_epi.h): fwd emits BatchNorm statistics, dX applies the "
                          "LeakyReLU backward and emits the BN-backward statistics (PAPER.md:52 block)")
@@ -51,7 +54,8 @@ def parse():
     ap.add_argument("--layers-out", default=os.path.join(ROOT, "gpurun_out", "bench_layers.json"))
     a = ap.parse_args()
     if a.global_batch is None:
-        a.global_batch = {"resnet18": 4096, "vgg16": 128, "googlenet": 256, "alexnet": 256}.get(a.net, 512)
+        a.global_batch = {"resnet18": 4096, "vgg16": 128, "googlenet": 256, "alexnet": 256, "resnet18@64": 1024,
+                          "resnet18@128": 256, "resnet18@224": 64}.get(a.net, 512)
     return a
 
 
@@ -219,6 +223,16 @@ def spawn_ranks(n):
     return subprocess.call(cmd)
 
 
+def _world1_group(dev):
+    """A world-size-1 NCCL group for --fused-allreduce on one GPU (the multicast object then spans this GPU)."""
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(free_port()))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    return dist.group.WORLD
+
+
 # ---------------------------------------------------------------------- GPU arm
 def main():
     a = parse()
@@ -253,7 +267,8 @@ def main():
         raise SystemExit("global batch %d not divisible by %d ranks" % (a.global_batch, world))
     B = a.global_batch // world
     # filters replicated (rank-independent seed); activations / loss gradients differ per shard
-    step = dp.ConvNetStep(a.net, B, dev, math=a.math, seed=1, bucket_mb=a.bucket_mb, rank=rank, epi=a.epi)
+    step = dp.ConvNetStep(a.net, B, dev, math=a.math, seed=1, bucket_mb=a.bucket_mb, rank=rank, epi=a.epi,
+                          mcast_group=(pg if pg is not None else _world1_group(dev)) if a.fused_allreduce else None)
     torch.cuda.synchronize()
 
     def barrier():
@@ -393,7 +408,9 @@ def main():
                       "epilogue": ("fused: fwd + BN statistics, dX + LeakyReLU backward + BN-backward statistics"
                                    if a.epi else "none (plain conv outputs)"),
                       "cuda_graph": graph is not None,
-                      "parallelism": "dp%d" % world, "l2": "inputs larger than L2 (per-step working set "
+                      "parallelism": "dp%d" % world,
+                      "dw_allreduce": ("fused in the dW kernels (NVLink multicast multimem.red)" if a.fused_allreduce
+                                       else "NCCL all_reduce SUM, bucketed, async" if world > 1 else "none (1 GPU)"), "l2": "inputs larger than L2 (per-step working set "
                       "%.1f GB >> 126 MB)" % (sum(t.numel() for b in step.bufs for t in (b.X, b.Y) if t is not None)
                                               * 4 / 1e9),
                       "conv_tflops_valid": step.flops(True) * world / (ms_max / a.steps / 1000) / 1e12,

@@ -45,6 +45,8 @@ struct __align__(64) DwsParams {
     CUtensorMap mapXB;  // the same view, box RB rows: [RB][XW][64 ch]
     CUtensorMap mapY;  // dY viewed (32 oc, OW, OH, N, OC/32), 128B/32B-atom swizzle: MN-major B
     int OW, RB, XW, ohb;  // k-block = RB output rows x OW (RB * OW == 32); XW = OW + 2; ohb = OH / RB
+    int cbs;              // wide maps (OW = 64, 128, 224, ...: kernel geometry of OW = 32): column blocks of 32
+                          // per output row; k-block = (image, column block, output row), rows innermost
     int kb_total, kb_per_split, splits, work, chunk_kb;
     int ph, pw;
 };
@@ -83,7 +85,6 @@ struct DwsAux {
     uint64_t conv[16], tfree[8];
     uint64_t tfull, tempty;
     uint32_t tmem_base;
-    int sink;  // param_warm
 };
 
 struct DwsItem {
@@ -110,8 +111,6 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
     DwsAux* aux = reinterpret_cast<DwsAux*>(tiles_ptr + C::SS * C::STAGE_BYTES);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int CHK = PLANES == 2 ? dp.chunk_kb : (1 << 30);
-    param_warm(p, tid, &aux->sink);
-    param_warm(dp, tid - param_lines<GenParams>(), &aux->sink);
 
     if (tid == 0) {
         for (int s = 0; s < C::SS; ++s) {
@@ -151,7 +150,8 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
             it.init(dp, w);
             for (int kb = it.kb0; kb < it.kb1; ++kb) {
                 if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
-                const int n = kb / dp.ohb, oh0 = (kb - n * dp.ohb) * dp.RB;
+                const int ncb = kb / dp.ohb, oh0 = (kb - ncb * dp.ohb) * dp.RB;
+                const int n = ncb / dp.cbs, cb = ncb - n * dp.cbs, ow0 = cb * 32;  // cbs == 1: ow0 = 0
                 // slab rows: ih0 + 0 .. ih0 + RB.  Row 0 equals the previous k-block's last row when that
                 // k-block is the previous output rows of the same image: then only rows 1..RB are loaded
                 // and the converters read row 0 from the previous stage (1 of 2 rows saved at OW = 32).
@@ -160,9 +160,9 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
                 const uint32_t sY = tiles_addr + s * C::STAGE_BYTES;
                 if (elect_one()) {
                     mbar_arrive_expect_tx(&aux->full[s], C::Y_BYTES + C::XB_BYTES + (fresh ? C::XA_BYTES : 0));
-                    tma_load_5d(sY, &dp.mapY, &aux->full[s], 0, 0, oh0, n, 0);
-                    tma_load_4d(sY + C::XB_OFF, &dp.mapXB, &aux->full[s], 0, -dp.pw, ih0 + 1, n);
-                    if (fresh) tma_load_4d(sY + C::XA_OFF, &dp.mapXA, &aux->full[s], 0, -dp.pw, ih0, n);
+                    tma_load_5d(sY, &dp.mapY, &aux->full[s], 0, ow0, oh0, n, 0);
+                    tma_load_4d(sY + C::XB_OFF, &dp.mapXB, &aux->full[s], 0, ow0 - dp.pw, ih0 + 1, n);
+                    if (fresh) tma_load_4d(sY + C::XA_OFF, &dp.mapXA, &aux->full[s], 0, ow0 - dp.pw, ih0, n);
                 }
                 __syncwarp();
                 if (++s == C::SS) {
@@ -413,16 +413,16 @@ int launch_t(const DwsParams& dp, const GenParams& g, cudaStream_t st, char* err
 bool dws_supported(int op, int IC, int OC, int FH, int FW, int sh, int sw, int OH, int OW) {
     if (op != CONV_OP_BWD_FILTER) return false;
     if (IC != 64 || OC != 64 || FH != 3 || FW != 3 || sh != 1 || sw != 1) return false;
-    if (OW != 32 && OW != 16 && OW != 8) return false;
-    return OH % (32 / OW) == 0;
+    if (OW != 32 && OW != 16 && OW != 8 && (OW % 32 != 0 || OW > 4096)) return false;  // wide maps: OW % 32
+    return OW >= 32 || OH % (32 / OW) == 0;
 }
 
 // Split choice: chains of <= 256 k-blocks (the precision bound shared with the TMA variant), and a
 // number of work items (3 groups per split) that fills whole rounds of the 148-CTA persistent grid,
 // at least 4 rounds: with 300 items (2.03 rounds) two thirds of the CTAs idled through the last one.
 int dws_splits(int N, int OH, int OW, int* kb_per_split) {
-    const int RB = 32 / OW;
-    const long long kb_total = (long long)N * (OH / RB);
+    const int RB = OW >= 32 ? 1 : 32 / OW;
+    const long long kb_total = (long long)N * (OH / RB) * (OW >= 32 ? OW / 32 : 1);
     const long long need = (kb_total + 255) / 256;
     long long rounds = (3 * need + 147) / 148;
     if (rounds < 4) rounds = 4;
@@ -438,11 +438,13 @@ int dws_launch(int planes, const GenParams& g, int splits, int kb_per_split, cud
                size_t errlen) {
     DwsParams dp;
     memset(&dp, 0, sizeof dp);
-    dp.OW = g.OW;
-    dp.RB = 32 / g.OW;
-    dp.XW = g.OW + 2;
+    const int wow = g.OW >= 32 ? 32 : g.OW;  // geometry width (wide maps: 32-column blocks)
+    dp.OW = wow;
+    dp.cbs = g.OW >= 32 ? g.OW / 32 : 1;
+    dp.RB = 32 / wow;
+    dp.XW = wow + 2;
     dp.ohb = g.OH / dp.RB;
-    dp.kb_total = g.N * dp.ohb;
+    dp.kb_total = g.N * dp.ohb * dp.cbs;
     dp.kb_per_split = kb_per_split;
     dp.splits = splits;
     dp.work = splits * kDwsGroups;
@@ -457,18 +459,18 @@ int dws_launch(int planes, const GenParams& g, int splits, int kb_per_split, cud
     bool ok = tma_encode_f32(&dp.mapXA, g.B, 4, dx, sx, bxa, CU_TENSOR_MAP_SWIZZLE_NONE);
     ok &= tma_encode_f32(&dp.mapXB, g.B, 4, dx, sx, bxb, CU_TENSOR_MAP_SWIZZLE_NONE);
     uint64_t dy[5] = {32, OW, OH, N, OC / 32}, sy[4] = {OC * 4, OW * OC * 4, OH * OW * OC * 4, 128};
-    uint32_t by[5] = {32, (uint32_t)OW, (uint32_t)dp.RB, 1, (uint32_t)(OC / 32)};
+    uint32_t by[5] = {32, (uint32_t)wow, (uint32_t)dp.RB, 1, (uint32_t)(OC / 32)};
     ok &= tma_encode_f32(&dp.mapY, g.A, 5, dy, sy, by, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     if (!ok) {
         snprintf(err, errlen, "dws: cuTensorMapEncodeTiled failed");
         return CONV_ECUDA;
     }
     if (planes == 2) {
-        if (g.OW == 32) return launch_t<2, 32>(dp, g, st, err, errlen);
+        if (g.OW >= 32) return launch_t<2, 32>(dp, g, st, err, errlen);
         if (g.OW == 16) return launch_t<2, 16>(dp, g, st, err, errlen);
         return launch_t<2, 8>(dp, g, st, err, errlen);
     }
-    if (g.OW == 32) return launch_t<1, 32>(dp, g, st, err, errlen);
+    if (g.OW >= 32) return launch_t<1, 32>(dp, g, st, err, errlen);
     if (g.OW == 16) return launch_t<1, 16>(dp, g, st, err, errlen);
     return launch_t<1, 8>(dp, g, st, err, errlen);
 }

@@ -75,6 +75,9 @@ struct GenParams {
     // (a 32-column block never straddles a tap); the epilogue drops ic >= IC and stores at tap * IC + ic
     int dw_icp;
     FastDiv fd_icp;
+    // fused dW all-reduce (smconv_mcast.h): the TMA dW epilogue adds its tile into this multicast address
+    // (multimem.red) instead of storing it; NULL otherwise
+    float* mc_out;
     // TEST/EXPERIMENT hook (smconv_set_trace): per-CTA phase timestamps, NULL in normal operation
     unsigned long long* trace;
 };
@@ -114,7 +117,6 @@ struct GenAux {
     uint64_t done;
     uint32_t tmem_base;
     int ntaps;
-    int sink;  // param_warm
     int4 taps[kMaxTaps];  // {dh, dw, tapfull, 0}
 };
 
@@ -221,7 +223,6 @@ __global__ void __launch_bounds__(GenCfg<OP, BN, PLANES>::NTHREADS, 1)
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
-    param_warm(p, tid, &aux->sink);
 
     // ---------------- tile coordinates
     int phase = 0, mt = blockIdx.x;
@@ -507,9 +508,12 @@ __global__ void __launch_bounds__(256) zero_phases_kernel(float4* __restrict__ d
 }
 
 // Deterministic split-K reduction: out[i] = sum_{s=0..S-1} ws[s*stride + i] in fixed order.
+// mc != NULL (smconv_mcast.h): the fixed-order sum is added into the multicast address (multimem.red:
+// every rank's copy receives it) instead of being stored to out.
 template <int UNUSED = 0>
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ out,
-                                                            long long n4, int splits, long long stride4) {
+                                                            long long n4, int splits, long long stride4,
+                                                            float* mc = nullptr) {
     pdl_trigger();
     pdl_wait();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
@@ -536,7 +540,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __rest
             a.z += b.z;
             a.w += b.w;
         }
-        out[i] = a;
+        if (mc) mc_red_add_f4(mc + 4 * i, a);
+        else out[i] = a;
     }
 }
 

@@ -128,8 +128,6 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
     const int rank = PAIR ? (int)cluster_ctarank() : 0;
     const int wfirst = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
     const int wstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-    param_warm(p, tid, &aux->sink);
-    param_warm(sp, tid - param_lines<GenParams>(), &aux->sink);
 
     if (tid == 0) {
         for (int t = 0; t < C::NT; ++t) mbar_init(&aux->tfree[t], 1);

@@ -120,7 +120,6 @@ struct TmaAux {
     uint64_t full[8], conv[8], empty[8], tfree[8];
     uint64_t tfull[2], tempty[2];
     uint32_t tmem_base;
-    int sink;              // param_warm
     int4 ptaps[kMaxTaps];  // producer-private per-tile tap list / X-box geometry
 };
 
@@ -361,8 +360,6 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
     const int wfirst = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
     const int wstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     const uint32_t csk_rank = (!C::IS_DW && !PAIR && tp.csk) ? cluster_ctarank() : 0u;
-    param_warm(p, tid, &aux->sink);
-    param_warm(tp, tid - param_lines<GenParams>(), &aux->sink);
     unsigned long long* const trc = p.trace;
     if (trc && tid == 0) {
         trace_mark(trc, 0);
@@ -795,6 +792,21 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                 if (!C::IS_DW && tp.csk) {  // cluster split-K: this CTA's partial -> own shared memory
                     *reinterpret_cast<float4*>(tiles_ptr + ((size_t)row * C::PSTRIDE + (col - n0)) * 4) =
                         make_float4(x, y, z, w4);
+                } else if (C::IS_DW && p.mc_out) {  // fused dW all-reduce: add into every rank's copy
+                    if (OP == OP_DWT) {
+                        float* o = p.mc_out + obase + (long long)col * p.M;  // 4 output channels, one element each
+                        asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(o), "f"(x) : "memory");
+                        asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(o + p.M), "f"(y) : "memory");
+                        asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(o + 2 * (long long)p.M),
+                                     "f"(z) : "memory");
+                        asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(o + 3 * (long long)p.M),
+                                     "f"(w4) : "memory");
+                    } else if (p.dw_icp) {
+                        const int tap = (int)fdiv((uint32_t)col, p.fd_icp), ic = col - tap * p.dw_icp;
+                        if (ic < p.IC) mc_red_add_f4(p.mc_out + obase + tap * p.IC + ic, make_float4(x, y, z, w4));
+                    } else {
+                        mc_red_add_f4(p.mc_out + obase + col, make_float4(x, y, z, w4));
+                    }
                 } else if (OP == OP_DWT) {  // column = oc: a warp's 32 rows are 128 contiguous bytes per column
                     float* o = outp + obase + (long long)col * p.M;
                     o[0] = x;

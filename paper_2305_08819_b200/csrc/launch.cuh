@@ -19,10 +19,20 @@
 
 namespace smconv {
 
-inline bool pdl_enabled() {
-    static const int on = getenv("SMCONV_PDL") ? atoi(getenv("SMCONV_PDL")) : 1;
-    return on != 0;
+// SMCONV_PDL: 0 = never, 1 = auto (default): calls whose plan runs plain TF32 MMAs, 2 = always.
+// Measured on VGG-16 b128 (r02p, 2 runs each): TF32 step 1.080 -> 0.991 ms with PDL, but 3xTF32
+// 1.628 -> 1.697 ms and ResNet-18 b4096 3xTF32 57.5 -> 58.7 ms, so "auto" leaves 3xTF32 calls without.
+inline int pdl_mode() {
+    static const int m = getenv("SMCONV_PDL") ? atoi(getenv("SMCONV_PDL")) : 1;
+    return m;
 }
+// set by the C-ABI entry for the kernels of the current call (thread-local: calls on other host threads
+// are independent)
+inline bool& pdl_this_call() {
+    static thread_local bool on = false;
+    return on;
+}
+inline bool pdl_enabled() { return pdl_this_call(); }
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,

@@ -16,6 +16,7 @@
 #include "../../include/smconv.h"
 #include "../../include/smconv_ext.h"
 #include "../../include/smconv_epi.h"
+#include "../../include/smconv_mcast.h"
 #include "../../include/smgemm.h"
 #include "conv_gen.cuh"
 #include "conv_strip.cuh"
@@ -163,6 +164,8 @@ struct Plan {
     int epi_C, epi_ncols, epi_ngroups, epi_nchunks;
     long long epi_rows;       // pass: output rows (N * H * W)
     size_t epi_part_off, epi_part2_off;  // stats: fp32 partial rows, double chunk sums (workspace)
+    int mc_direct;            // fused dW all-reduce: the TMA dW epilogue adds into the multicast address
+    int mc_reduce;            //   ... or the split-K reduce kernel does (every other dW plan)
     size_t epi_stage_off;     // pass form of the LEAKY_BWD modes: the conv output is staged here (so that
                               // A may be the output buffer itself: in-place G over A)
 };
@@ -307,8 +310,23 @@ void plan_epi(int op, const Dims& d, int epi, Plan& pl) {
     }
 }
 
+// kMcastEpi: plan-cache key of a conv2d_bwd_filter_mcast plan (fused dW + in-switch all-reduce)
+constexpr int kMcastEpi = 100;
+
+void plan_mcast(Plan& pl) {
+    if (pl.variant == CONV_VARIANT_TMA && pl.splits == 1) {
+        pl.mc_direct = 1;
+        return;
+    }
+    pl.mc_reduce = 1;
+    if (!(pl.splits > 1 && !pl.gp.csk)) {  // single split: stage the tile in the workspace, reduce kernel adds it
+        pl.ws_bytes = (size_t)pl.out_elems * sizeof(float);
+        pl.gp.split_stride = pl.out_elems;
+    }
+}
+
 int plan_kernel_count(const Plan& pl) {
-    return 1 + (pl.splits > 1 && !pl.gp.csk) + (pl.zero_mask != 0) + (pl.wx_bytes != 0) + (pl.s2dx != 0) +
+    return 1 + ((pl.splits > 1 && !pl.gp.csk) || pl.mc_reduce) + (pl.zero_mask != 0) + (pl.wx_bytes != 0) + (pl.s2dx != 0) +
            (pl.epi && !pl.epi_fused) + 2 * epi_has_stats(pl.epi);
 }
 
@@ -318,7 +336,8 @@ int make_plan_uncached(int op, const Dims& d, int math, Plan& pl, int epi) {
         return CONV_OK;
     }
     const int rc = make_plan_base(op, d, math, pl);
-    if (rc == CONV_OK) plan_epi(op, d, epi, pl);
+    if (rc == CONV_OK && epi == kMcastEpi) plan_mcast(pl);
+    else if (rc == CONV_OK) plan_epi(op, d, epi, pl);
     return rc;
 }
 
@@ -679,6 +698,7 @@ struct EpiCall {
     const float* A;  // LEAKY_BWD*: activation
     double* stats;   // stats modes: [2][C]
 };
+constexpr EpiCall kMcastCall{kMcastEpi, 0.f, nullptr, nullptr};
 
 // after the main kernel (and split-K reduce / zero fill): the pass form of the epilogue, then the
 // fixed-order statistics reduction.  `conv_out` is where the conv wrote (the staging buffer in the pass
@@ -723,12 +743,14 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
         return fail(CONV_EWORKSPACE, "%s: workspace %zu bytes at %p, need %zu (conv2d_workspace_bytes)", op_name(op),
                     ws_bytes, ws, pl.ws_bytes);
     if (pl.ws_bytes > 0 && ((uintptr_t)ws & 15)) return fail(CONV_EALIGN, "%s: workspace not 16-B aligned", op_name(op));
+    pdl_this_call() = pdl_mode() == 2 || (pdl_mode() == 1 && pl.planes == 1);  // launch.cuh
     GenParams g = pl.gp;
     g.A = A;
     g.B = B;
-    const bool ws_split = pl.splits > 1 && !pl.gp.csk;
+    const bool ws_split = (pl.splits > 1 && !pl.gp.csk) || pl.mc_reduce;
     g.out = ws_split ? (float*)ws : out;
     g.Bx = nullptr;
+    g.mc_out = pl.mc_direct ? out : nullptr;  // `out` is the multicast address in the mcast plans
     g.trace = g_trace.load();
     // pass form of the LEAKY_BWD modes: the conv (and its reduce / zero fill) write the staging buffer
     float* conv_out = (pl.epi && !pl.epi_fused && epi_reads_a(pl.epi)) ? (float*)((char*)ws + pl.epi_stage_off) : out;
@@ -803,7 +825,7 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
         int blocks = (int)((n4 + 255) / 256);
         if (blocks > kSMs * 8) blocks = kSMs * 8;
         launch_k(splitk_reduce_kernel<0>, dim3(blocks), dim3(256), 0, st, 1, (const float4*)ws, (float4*)conv_out, n4,
-                 pl.splits, n4);
+                 pl.splits, n4, pl.mc_reduce ? out : (float*)nullptr);
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: reduce launch failed: %s", op_name(op), cudaGetErrorString(e));
     }
@@ -840,7 +862,7 @@ int entry(int op, const float* in0, const float* in1, float* out, Dims d, int ma
         return fail(CONV_EALIAS, "%s: output buffer overlaps an input buffer", f);
     if (ws && (overlap(ws, ws_bytes, in0, b0) || overlap(ws, ws_bytes, in1, b1) || overlap(ws, ws_bytes, out, bo)))
         return fail(CONV_EALIAS, "%s: workspace overlaps a tensor", f);
-    if (ec.mode) {  // fused-epilogue arguments (smconv_epi.h)
+    if (ec.mode && ec.mode != kMcastEpi) {  // fused-epilogue arguments (smconv_epi.h)
         const bool fwd_ok = op == CONV_OP_FWD && (ec.mode == CONV_EPI_BN_STATS || ec.mode == CONV_EPI_LEAKY);
         const bool dx_ok = op == CONV_OP_BWD_DATA && (ec.mode == CONV_EPI_LEAKY_BWD || ec.mode == CONV_EPI_LEAKY_BWD_STATS);
         if (!fwd_ok && !dx_ok) return fail(CONV_EARG, "%s: epilogue %d is not defined for this op", f, ec.mode);
@@ -1038,6 +1060,40 @@ int conv2d_epi_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int 
     if (buf && len)
         snprintf(buf, len, "%s epi=%s groups=%d ws_epi=%zu kernels_epi=%d", base,
                  !epi ? "none" : pl.epi_fused ? "fused" : "pass", pl.epi_ngroups, pl.ws_bytes, plan_kernel_count(pl));
+    return CONV_OK;
+}
+
+// ---------------------------------------------------------------- fused dW all-reduce (include/smconv_mcast.h)
+size_t conv2d_bwd_filter_mcast_workspace_bytes(int N, int IH, int IW, int IC, int OC, int FH, int FW, int sh, int sw,
+                                               int ph, int pw, int math) {
+    Dims d = mk(N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw);
+    if (check_dims(CONV_OP_BWD_FILTER, d, math)) return (size_t)-1;
+    Plan pl;
+    if (make_plan(CONV_OP_BWD_FILTER, d, math, pl, kMcastEpi)) return (size_t)-1;
+    return pl.ws_bytes;
+}
+
+int conv2d_bwd_filter_mcast(const float* X, const float* dY, float* dW_mc, int N, int IH, int IW, int IC, int OC, int FH,
+                            int FW, int sh, int sw, int ph, int pw, int math, void* ws, size_t ws_bytes,
+                            conv_stream_t st) {
+    g_api_name = "conv2d_bwd_filter_mcast";
+    const int rc = entry(CONV_OP_BWD_FILTER, X, dY, dW_mc, mk(N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw), math, ws,
+                         ws_bytes, st, kMcastCall);
+    g_api_name = nullptr;
+    return rc;
+}
+
+int conv2d_bwd_filter_mcast_plan_describe(int N, int IH, int IW, int IC, int OC, int FH, int FW, int sh, int sw,
+                                          int ph, int pw, int math, char* buf, size_t len) {
+    Dims d = mk(N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw);
+    int rc = check_dims(CONV_OP_BWD_FILTER, d, math);
+    if (rc) return rc;
+    Plan pl;
+    rc = make_plan(CONV_OP_BWD_FILTER, d, math, pl, kMcastEpi);
+    if (rc) return rc;
+    if (buf && len)
+        snprintf(buf, len, "variant=%d BN=%d splits=%d mcast=%s ws=%zu kernels=%d", pl.variant, pl.BN, pl.splits,
+                 pl.mc_direct ? "epilogue" : "reduce", pl.ws_bytes, plan_kernel_count(pl));
     return CONV_OK;
 }
 

@@ -133,7 +133,7 @@ class ConvNetStep:
 
     def __init__(self, net: str, batch: int, device, math: str = "3xtf32", seed: int = 0,
                  bucket_mb: float = 16.0, chain: bool = True, rank: int = 0, epi: bool = False,
-                 leaky_k: float = 0.01):
+                 leaky_k: float = 0.01, mcast_group=None):
         import torch
         self.torch = torch
         self.net = net
@@ -147,7 +147,7 @@ class ConvNetStep:
         self.epi = epi
         self.leaky_k = leaky_k
         L = self.layers
-        if chain and net == "resnet18":
+        if chain and net.startswith("resnet18"):
             xs, ds, sh = _chain_resnet(L)
         elif chain and net == "vgg16":
             xs, ds, sh = _chain_vgg(L)
@@ -157,7 +157,22 @@ class ConvNetStep:
         f32 = torch.float32
         # flat dW buffer in BACKWARD order (bucket = contiguous run of finished layers)
         sizes = [l.OC * l.FH * l.FW * l.IC for l in L]
-        self.dw_flat = torch.zeros(sum(sizes), dtype=f32, device=device)
+        # fused dW all-reduce (include/smconv_mcast.h): dW lives in symmetric memory with an NVLink
+        # multicast mapping; the dW kernels add each rank's shard into every rank's copy (no NCCL pass)
+        self.mc_handle, self.mc_ptr = None, 0
+        if mcast_group is not None:
+            from torch.distributed import _symmetric_memory as symm
+            if hasattr(symm, "enable_symm_mem_for_group"):
+                symm.enable_symm_mem_for_group(mcast_group.group_name)
+            self.dw_flat = symm.empty(sum(sizes), dtype=f32, device=device)
+            self.mc_handle = symm.rendezvous(self.dw_flat, mcast_group.group_name)
+            self.mc_ptr = int(getattr(self.mc_handle, "multicast_ptr", 0) or 0)
+            if not self.mc_ptr:
+                raise RuntimeError("fused dW all-reduce: no NVLink multicast object (multicast_ptr == 0)")
+            self.dw_flat.zero_()
+        else:
+            self.dw_flat = torch.zeros(sum(sizes), dtype=f32, device=device)
+        self.dw_offs = flat_offsets_backward(sizes)
         offs = flat_offsets_backward(sizes)
         for i, l in enumerate(L):
             b = LayerBuf(l, x_src=xs[i], dy_src=ds[i], dy_share=sh[i])
@@ -189,6 +204,8 @@ class ConvNetStep:
         # one split-K workspace shared by every call (they are stream-ordered), sized by the library
         for b in self.bufs:
             b.ws_bytes = [sm.workspace_bytes(op, b.layer.dims(batch), self.math) for op in range(3)]
+            if self.mc_ptr:
+                b.ws_bytes[2] = sm.mcast_workspace_bytes(b.layer.dims(batch), self.math)
             if epi:
                 b.ws_bytes[0] = sm.epi_workspace_bytes(0, b.layer.dims(batch), self.math, "bn_stats")
                 b.ws_bytes[1] = sm.epi_workspace_bytes(1, b.layer.dims(batch), self.math, "leaky_bwd_stats")
@@ -200,7 +217,13 @@ class ConvNetStep:
             b.ws = ws
         # buckets over the backward-ordered flat buffer
         self.buckets = plan_buckets(sizes, int(bucket_mb * (1 << 20) / 4))
-        if epi:
+        if self.mc_ptr:
+            self.kernels_per_step = sum(
+                sm.plan_kernels(0, b.layer.dims(batch), self.math)
+                + int(sm.mcast_plan_describe(b.layer.dims(batch), self.math).rsplit("kernels=", 1)[1])
+                + (sm.plan_kernels(1, b.layer.dims(batch), self.math) if k > 0 else 0)
+                for k, b in enumerate(self.bufs))
+        elif epi:
             self.kernels_per_step = sum(
                 sm.epi_plan_kernels(0, b.layer.dims(batch), self.math, "bn_stats")
                 + sm.plan_kernels(2, b.layer.dims(batch), self.math)
@@ -215,6 +238,12 @@ class ConvNetStep:
     # ---------------------------------------------------------------- one step
     def _call(self, op, b: LayerBuf, a, bb, out, stream):
         ws = b.ws
+        if op == 2 and self.mc_ptr:  # dW + all-reduce in the dW kernels, into the multicast address
+            i = self.bufs.index(b)
+            sm.raw_call_mcast(a.data_ptr(), bb.data_ptr(), self.mc_ptr + 4 * self.dw_offs[i], b.layer.dims(self.batch),
+                              self.math, ws.data_ptr() if (ws is not None and b.ws_bytes[2]) else 0,
+                              b.ws_bytes[2] if ws is not None else 0, stream)
+            return
         if self.epi and op != 2:
             ep = sm.EPI["bn_stats"] if op == 0 else sm.EPI["leaky_bwd_stats"]
             st = b.stats_fwd if op == 0 else b.stats_dx
@@ -248,6 +277,10 @@ class ConvNetStep:
             self._call(0, b, b.X, b.W, b.Y, stream)
             mark(("fwd", i, 1))
         handles = []
+        if self.mc_ptr:
+            # every rank's dW copy is zero before any rank adds into it (smconv_mcast.h contract)
+            self.dw_flat.zero_()
+            self.mc_handle.barrier()
         for i in reversed(range(len(self.bufs))):
             b = self.bufs[i]
             # dW first: its bucket's all-reduce (NCCL waits on this stream's work so far) then
@@ -255,7 +288,7 @@ class ConvNetStep:
             mark(("dw", i, 0))
             self._call(2, b, b.X, b.dY, b.dW, stream)
             mark(("dw", i, 1))
-            if pg is not None:
+            if pg is not None and not self.mc_ptr:
                 handles += allreduce_buckets(self.dw_flat, self.buckets, pg, ready_layer=i)
             if i > 0:
                 mark(("dx", i, 0))
@@ -263,6 +296,8 @@ class ConvNetStep:
                 mark(("dx", i, 1))
         for h in handles:
             h.wait()
+        if self.mc_ptr:
+            self.mc_handle.barrier()  # every rank's additions have landed before dW is read
 
     def flops(self, valid=True):
         tot = 0

@@ -66,14 +66,16 @@ def vgg16() -> List[Layer]:
     ]
 
 
-def resnet18() -> List[Layer]:
+def resnet18(hw: int = 32) -> List[Layer]:
     """ResNet-18 CIFAR (3x3 stem at 32x32, 4 stages of 2 BasicBlocks), in forward order.
 
     Each stage change has a 3x3 stride-2 conv and a 1x1 stride-2 p0 shortcut.
-    20 convs: 17 3x3 + 3 1x1.
+    20 convs: 17 3x3 + 3 1x1.  `hw` != 32: the same network on larger inputs -- the large-map regime
+    where the paper reports cu32 losing to cuDNN ("when the input-feature-size >= 128 x 128",
+    PAPER.md:169).
     """
-    out = [L("conv1", 32, 3, 64)]
-    H, C = 32, 64
+    out = [L("conv1", hw, 3, 64)]
+    H, C = hw, 64
     for stage, OC in ((1, 64), (2, 128), (3, 256), (4, 512)):
         for blk in range(2):
             if blk == 0 and stage > 1:
@@ -120,7 +122,10 @@ def googlenet() -> List[Layer]:
     return out
 
 
-NETS = {"vgg16": vgg16, "resnet18": resnet18, "alexnet": alexnet, "googlenet": googlenet}
+NETS = {"vgg16": vgg16, "resnet18": resnet18, "alexnet": alexnet, "googlenet": googlenet,
+        # large-map regime: the CIFAR ResNet-18 on 64 / 128 / 224-pixel inputs
+        "resnet18@64": lambda: resnet18(64), "resnet18@128": lambda: resnet18(128),
+        "resnet18@224": lambda: resnet18(224)}
 
 
 def valid_pairs(layer: Layer) -> int:

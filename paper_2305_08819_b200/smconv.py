@@ -23,6 +23,8 @@ MATH = {"3xtf32": CONV_MATH_FP32_3XTF32, "fp32": CONV_MATH_FP32_3XTF32, "tf32": 
 
 EXPORTS = ("conv2d_out_hw", "conv2d_workspace_bytes", "conv2d_fwd", "conv2d_bwd_data", "conv2d_bwd_filter",
            "conv2d_strerror", "conv2d_last_error_detail")
+MCAST_EXPORTS = ("conv2d_bwd_filter_mcast_workspace_bytes", "conv2d_bwd_filter_mcast",
+                 "conv2d_bwd_filter_mcast_plan_describe")
 EPI_EXPORTS = ("conv2d_epi_workspace_bytes", "conv2d_fwd_epi", "conv2d_bwd_data_epi", "conv2d_epi_plan_describe")
 GEMM_EXPORTS = ("gemm_workspace_bytes", "gemm_matmul", "gemm_matmul_t1", "gemm_matmul_t2", "gemm_plan_describe")
 EXT_EXPORTS = ("conv2d_force_variant", "conv2d_plan_describe", "conv2d_plan_kernels", "smconv_selftest_host",
@@ -90,6 +92,12 @@ def lib():
                 L.conv2d_bwd_data_epi.restype = I
                 L.conv2d_epi_plan_describe.argtypes = [I] * 14 + [ctypes.c_char_p, Z]
                 L.conv2d_epi_plan_describe.restype = I
+                L.conv2d_bwd_filter_mcast_workspace_bytes.argtypes = [I] * 12
+                L.conv2d_bwd_filter_mcast_workspace_bytes.restype = Z
+                L.conv2d_bwd_filter_mcast.argtypes = [P, P, P] + [I] * 11 + [I, P, Z, P]
+                L.conv2d_bwd_filter_mcast.restype = I
+                L.conv2d_bwd_filter_mcast_plan_describe.argtypes = [I] * 12 + [ctypes.c_char_p, Z]
+                L.conv2d_bwd_filter_mcast_plan_describe.restype = I
                 L.smconv_set_trace.argtypes = [P]
                 L.smconv_set_trace.restype = I
                 L.smconv_probe_tf32.argtypes = [P]
@@ -381,6 +389,27 @@ def conv2d_bwd_data_epi(dy, w, a, input_hw, stride=(1, 1), padding=(1, 1), math=
                                      *dims, m, e, float(k), _ptr(ws) if ws is not None else None, nb,
                                      ctypes.c_void_p(st)))
     return out, stats
+
+
+# ------------------------------------------------------------------ fused dW all-reduce (include/smconv_mcast.h)
+def mcast_workspace_bytes(dims, math=CONV_MATH_FP32_3XTF32):
+    n = lib().conv2d_bwd_filter_mcast_workspace_bytes(*dims, _math(math))
+    if n == ctypes.c_size_t(-1).value:
+        raise ConvError(CONV_EARG, lib().conv2d_last_error_detail().decode())
+    return n
+
+
+def mcast_plan_describe(dims, math=CONV_MATH_FP32_3XTF32):
+    buf = ctypes.create_string_buffer(256)
+    _check(lib().conv2d_bwd_filter_mcast_plan_describe(*dims, _math(math), buf, 256))
+    return buf.value.decode()
+
+
+def raw_call_mcast(x_ptr, dy_ptr, dw_mc_ptr, dims, math, ws_ptr, ws_bytes, stream_handle):
+    """conv2d_bwd_filter_mcast with raw device pointers; dw_mc_ptr is a MULTICAST address (smconv_mcast.h)."""
+    P = ctypes.c_void_p
+    _check(lib().conv2d_bwd_filter_mcast(P(x_ptr), P(dy_ptr), P(dw_mc_ptr), *dims, _math(math), P(ws_ptr or 0),
+                                         ws_bytes, P(stream_handle)))
 
 
 # ------------------------------------------------------------------ GEMM (include/smgemm.h)

@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(sm):
     L = ctypes.CDLL(sm.LIB_PATH)
     for n in names:
         assert hasattr(L, n), n
-    assert set(sm.EXPORTS + sm.EXT_EXPORTS + sm.GEMM_EXPORTS + sm.EPI_EXPORTS) <= set(names)
+    assert set(sm.EXPORTS + sm.EXT_EXPORTS + sm.GEMM_EXPORTS + sm.EPI_EXPORTS + sm.MCAST_EXPORTS) <= set(names)
 
 
 def test_library_is_sm100a(sm):
@@ -255,3 +255,18 @@ def test_epi_plans(sm):
     assert sm.epi_plan_kernels(0, d_strip, 1, "bn_stats") == sm.plan_kernels(0, d_strip, 1) + 2
     assert sm.epi_plan_kernels(0, d_csk, 1, "bn_stats") == sm.plan_kernels(0, d_csk, 1) + 3
     assert sm.epi_plan_kernels(1, d_strip, 1, "leaky_bwd") == sm.plan_kernels(1, d_strip, 1)
+
+
+def test_mcast_plans(sm):
+    """Fused dW + all-reduce (include/smconv_mcast.h): the TMA dW epilogue adds into the multicast buffer
+    when the plan has one split; otherwise the split-K reduce kernel does (a single-split non-TMA plan
+    stages its tile in the workspace)."""
+    one = (128, 2, 2, 512, 512, 3, 3, 1, 1, 1, 1)     # VGG conv11 3xTF32: TMA pairs, one split
+    many = (128, 32, 32, 64, 64, 3, 3, 1, 1, 1, 1)    # DWS split-K
+    assert "mcast=epilogue" in sm.mcast_plan_describe(one, 0)
+    d = sm.mcast_plan_describe(many, 0)
+    assert "mcast=reduce" in d
+    assert sm.mcast_workspace_bytes(many, 0) == sm.workspace_bytes(2, many, 0)
+    stem = (8, 8, 8, 4, 64, 3, 3, 1, 1, 1, 1)
+    if "splits=1 " in sm.plan_describe(2, stem, 0):
+        assert sm.mcast_workspace_bytes(stem, 0) >= 64 * 9 * 4 * 4

@@ -9,6 +9,10 @@ oracle on outputs it can afford:
   * a property that holds at any size: the trilinear adjoint identity
     <fwd(X, W), dY> = <X, dX(dY, W)> = <W, dW(X, dY)> from the GPU outputs (fp64 dot products).
 
+The same checks run on the large-map regime ("input-feature-size
+>= 128 x 128"): the CIFAR ResNet-18 on 128 x 128 inputs at batch 64 and 224 x 224 at batch 16
+(nets.NETS["resnet18@128"], ["resnet18@224"]; bench.py --net resnet18@128).
+
 Tolerances: north_star / DESIGN.md reading L8 -- normwise max|g - r| / max|r|: 3xTF32 1e-5, TF32 5e-3
 (per sampled image; for dW samples relative to max|dW| of the GPU tensor).
 """
@@ -35,9 +39,12 @@ def env():
     return torch, oracle, sm, nets
 
 
+CONFIGS = [("resnet18", B), ("resnet18@128", 64), ("resnet18@224", 16)]
+
+
 def _layers():
     from paper_2305_08819_b200 import nets
-    return [(i, l) for i, l in enumerate(nets.resnet18())]
+    return [(net, nb, i, l) for net, nb in CONFIGS for i, l in enumerate(nets.NETS[net]())]
 
 
 def _nw(got, ref):
@@ -46,10 +53,10 @@ def _nw(got, ref):
 
 
 @pytest.mark.parametrize("math", ["3xtf32", "tf32"])
-@pytest.mark.parametrize("il", _layers(), ids=lambda il: il[1].name)
+@pytest.mark.parametrize("il", _layers(), ids=lambda il: "%s-%s" % (il[0], il[3].name))
 def test_resnet18_layer_full_batch(env, il, math, parity_log):
     torch, oracle, sm, nets = env
-    i, l = il
+    net, B, i, l = il
     from paper_2305_08819_b200 import synth
     dev = torch.device("cuda")
     X, W, dY = synth.torch_layer_inputs(l, B, dev, seed=5000 + i)
@@ -63,7 +70,7 @@ def test_resnet18_layer_full_batch(env, il, math, parity_log):
     m = sm.MATH[math]
 
     def log(op, e, cov):
-        parity_log.append({"config": "resnet18-b%d" % B, "layer": l.name, "op": op, "math": math,
+        parity_log.append({"config": "%s-b%d" % (net, B), "layer": l.name, "op": op, "math": math,
                            "check": "random", "coverage": cov, "normwise": e, "tol": TOL[math],
                            "plan": sm.plan_describe({"fwd": 0, "dx": 1, "dw": 2}[op], l.dims(B), m)})
 

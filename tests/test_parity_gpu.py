@@ -99,6 +99,9 @@ SWEEP = [
     (32, 8, 8, 24, 16, 1, 1, 1, 1, 0, 0),      # 1x1 with 16 / 24 channels (GoogLeNet 5x5 reduce)
     (256, 4, 4, 112, 208, 3, 3, 1, 1, 1, 1),   # CTA pairs with ragged channels
     (32, 8, 8, 144, 48, 3, 3, 2, 2, 1, 1),     # stride-2 phases, ragged channels
+    # the 64-channel dW kernel (DWS) on wide maps: 32-column blocks, rows innermost (large-map regime)
+    (8, 16, 96, 64, 64, 3, 3, 1, 1, 1, 1),
+    (4, 64, 64, 64, 64, 3, 3, 1, 1, 1, 1),
 ]
 
 
