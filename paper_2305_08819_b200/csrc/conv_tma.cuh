@@ -262,14 +262,17 @@ struct TileInfo {
     // source pixel in bounds)?  If so and t != nullptr, writes {dh, dw, fh * FW + fw}.
     SMCONV_DEV bool tap_valid(const GenParams& p, int kh, int kw, int4* t) const {
         const int ph_ = OP == OP_DX ? phase : 0;
-        const int dh = p.tf_off[ph_][0][kh], dw = p.tf_off[ph_][1][kw];
+        // fwd: the tap table is the identity (offset = filter index); reading it anyway cost a dependent
+        // dynamically indexed parameter load per candidate tap in every role's per-tile bookkeeping
+        const int dh = OP == OP_FWD ? kh : p.tf_off[ph_][0][kh], dw = OP == OP_FWD ? kw : p.tf_off[ph_][1][kw];
         const int srcH = OP == OP_FWD ? p.IH : p.OH;
         const int srcW = OP == OP_FWD ? p.IW : p.OW;
         bool any = false;
 #pragma unroll
         for (int g = 0; g < 4; ++g)
             if (g < ngrp) any |= grp[g].w && (unsigned)(grp[g].x + dh) < (unsigned)srcH && (unsigned)(grp[g].y + dw) < (unsigned)srcW;
-        if (any && t) *t = make_int4(dh, dw, p.tf_f[ph_][0][kh] * p.FW + p.tf_f[ph_][1][kw], 0);
+        if (any && t)
+            *t = make_int4(dh, dw, OP == OP_FWD ? kh * p.FW + kw : p.tf_f[ph_][0][kh] * p.FW + p.tf_f[ph_][1][kw], 0);
         return any;
     }
 
@@ -277,11 +280,16 @@ struct TileInfo {
     // (validity is separable); several positions -> the union over the groups, candidate by candidate.
     SMCONV_DEV int ntaps(const GenParams& p) const {
         const int ph_ = OP == OP_DX ? phase : 0;
-        const int nh = p.tf_n[ph_][0], nw = p.tf_n[ph_][1];
+        const int nh = OP == OP_FWD ? p.FH : p.tf_n[ph_][0], nw = OP == OP_FWD ? p.FW : p.tf_n[ph_][1];
         if (ngrp == 1) {
             if (!grp[0].w) return 0;
             const int srcH = OP == OP_FWD ? p.IH : p.OH;
             const int srcW = OP == OP_FWD ? p.IW : p.OW;
+            if (OP == OP_FWD) {  // rows / columns of the filter whose source is in range: a clamp, no loop
+                const int ch = min(nh, srcH - grp[0].x) - max(0, -grp[0].x);
+                const int cw = min(nw, srcW - grp[0].y) - max(0, -grp[0].y);
+                return ch > 0 && cw > 0 ? ch * cw : 0;
+            }
             int ch = 0, cw = 0;
             for (int k = 0; k < nh; ++k) ch += (unsigned)(grp[0].x + p.tf_off[ph_][0][k]) < (unsigned)srcH;
             for (int k = 0; k < nw; ++k) cw += (unsigned)(grp[0].y + p.tf_off[ph_][1][k]) < (unsigned)srcW;
@@ -420,8 +428,9 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                 if (OP == OP_FWD || OP == OP_DX) {
                     int nt = 0;
                     const int ph_ = OP == OP_DX ? ti.phase : 0;
-                    for (int kh = 0; kh < p.tf_n[ph_][0]; ++kh)
-                        for (int kw = 0; kw < p.tf_n[ph_][1]; ++kw)
+                    const int nth = OP == OP_FWD ? p.FH : p.tf_n[ph_][0], ntw = OP == OP_FWD ? p.FW : p.tf_n[ph_][1];
+                    for (int kh = 0; kh < nth; ++kh)
+                        for (int kw = 0; kw < ntw; ++kw)
                             if (ti.tap_valid(p, kh, kw, &taps[nt])) ++nt;  // same value from every lane
                     __syncwarp();
                     if (trc && lane == 0 && w == wfirst) trace_mark(trc, 12);
