@@ -51,6 +51,8 @@ def parse():
                     help="replay the timed steps as one CUDA graph (auto: on at 1 GPU).  Measured: no gain at "
                          "batch 4096/512 or VGG b128 (the GPU, not the host, bounds the step), and per-call "
                          "event nodes inside a graph are less reliable, so the default stays eager")
+    ap.add_argument("--dw-stream", action="store_true",
+                    help="run every dW on a second stream beside the dX chain (dp.ConvNetStep dw_stream)")
     ap.add_argument("--layers-out", default=os.path.join(ROOT, "gpurun_out", "bench_layers.json"))
     a = ap.parse_args()
     if a.global_batch is None:
@@ -268,7 +270,8 @@ def main():
     B = a.global_batch // world
     # filters replicated (rank-independent seed); activations / loss gradients differ per shard
     step = dp.ConvNetStep(a.net, B, dev, math=a.math, seed=1, bucket_mb=a.bucket_mb, rank=rank, epi=a.epi,
-                          mcast_group=(pg if pg is not None else _world1_group(dev)) if a.fused_allreduce else None)
+                          mcast_group=(pg if pg is not None else _world1_group(dev)) if a.fused_allreduce else None,
+                          dw_stream=a.dw_stream)
     torch.cuda.synchronize()
 
     def barrier():
@@ -357,21 +360,30 @@ def main():
     per.update(live)
     layer_rows = []
     P = peaks()
+
+    def tensor_div(op, plan):
+        # tensor-pipe cost per product in TF32-MMA units: 3xTF32 dW = 3 TF32 MMAs; 3xTF32 fwd / dX on the
+        # TMA / STRIP variants = 1 TF32 MMA + 1 bf16 MMA of twice the K at twice the rate = 2
+        hyb = op != "dw" and ("variant=tma" in plan or "variant=strip" in plan)
+        return (2.0 if hyb else 3.0) if a.math == "3xtf32" else 1.0
+
     for (op, i), v in per.items():
         l = step.bufs[i].layer
         avg = sum(v) / len(v)
         fl = nets.flops(l, B, valid=True)
         by = nets.bytes_compulsory(l, B, op)
+        plan = sm.plan_describe({"fwd": 0, "dx": 1, "dw": 2}[op], l.dims(B), step.math)
+        pk = P["tf32_sustained"] / tensor_div(op, plan)
+        # the layer's roofline time: max(flops / tensor peak, bytes / HBM peak); frac = that / measured
+        t_roof = max(fl / (pk * 1e12), by / (P["hbm_gbs"] * 1e9)) * 1e3
         layer_rows.append({"op": op, "layer": l.name, "i": i, "ms": avg, "flops": fl, "bytes": by,
                            "timed": "live (timed region)" if (op, i) in live else "profile pass",
                            "tflops": fl / avg / 1e9, "gbs": by / avg / 1e6,
-                           "plan": sm.plan_describe({"fwd": 0, "dx": 1, "dw": 2}[op], l.dims(B), step.math)})
+                           "bound": "tensor" if fl / (pk * 1e12) >= by / (P["hbm_gbs"] * 1e9) else "hbm",
+                           "roofline_ms": t_roof, "frac": t_roof / avg, "plan": plan})
     layer_rows.sort(key=lambda r: -r["ms"])
     top = [r for r in layer_rows if (r["op"], r["i"]) == top_key][0]
-    # tensor-pipe cost per product in TF32-MMA units: 3xTF32 dW = 3 TF32 MMAs; 3xTF32 fwd / dX on the
-    # TMA / STRIP variants = 1 TF32 MMA + 1 bf16 MMA of twice the K at twice the rate = 2
-    hyb = top["op"] != "dw" and ("variant=tma" in top["plan"] or "variant=strip" in top["plan"])
-    mathdiv = (2.0 if hyb else 3.0) if a.math == "3xtf32" else 1.0
+    mathdiv = tensor_div(top["op"], top["plan"])
     peak_t = P["tf32_sustained"] / mathdiv
     ridge = peak_t * 1e12 / (P["hbm_gbs"] * 1e9)
     ai = top["flops"] / top["bytes"]
@@ -407,7 +419,7 @@ def main():
                       "fwd_dx_cross_terms": "bf16" if a.math == "3xtf32" else None,
                       "epilogue": ("fused: fwd + BN statistics, dX + LeakyReLU backward + BN-backward statistics"
                                    if a.epi else "none (plain conv outputs)"),
-                      "cuda_graph": graph is not None,
+                      "cuda_graph": graph is not None, "dw_stream": a.dw_stream,
                       "parallelism": "dp%d" % world,
                       "dw_allreduce": ("fused in the dW kernels (NVLink multicast multimem.red)" if a.fused_allreduce
                                        else "NCCL all_reduce SUM, bucketed, async" if world > 1 else "none (1 GPU)"), "l2": "inputs larger than L2 (per-step working set "

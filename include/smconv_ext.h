@@ -25,8 +25,11 @@ enum {
     CONV_VARIANT_STRIP = 3,     /* TMA strips with input-slab reuse across filter columns:
                                    stride-1 3-wide fwd / dX, BN <= 128 (TF32) / 64 (3xTF32) */
     CONV_VARIANT_DIRECT = 4,    /* CUDA-core fp32 direct conv for few-channel (IC <= 8) stems, fwd / dW */
-    CONV_VARIANT_DWS = 5        /* dW of 3x3 s1 64->64 convs on 8/16/32-wide maps: one activation slab
+    CONV_VARIANT_DWS = 5,       /* dW of 3x3 s1 64->64 convs on 8/16/32-wide maps: one activation slab
                                    per k-block shared by 4 taps (shift applied by the TF32 split stage) */
+    CONV_VARIANT_STEM = 6       /* the IC = 4 (padded RGB) 3x3 stems on the tensor cores: fwd with the
+                                   IM2COL rows written into TMEM and a TMA-store epilogue (OC 64/128/192),
+                                   dW with dY by TMA and per-CTA partials (any OC % 4 == 0) */
 };
 
 /* Force a variant for all subsequent calls of `op` in this process (thread-safe);

@@ -45,10 +45,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB) and os.path.exists(STAMP) and open(STAMP).read() == h:
         return LIB
     tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [nvcc()] + NVCC_FLAGS + ["-I" + INCLUDE] + _sources() + ["-o", tmp]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd, cwd=CSRC)
+    # one object per source, compiled in parallel, then one link (the single-command build was ~90 s)
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "build", "obj%d" % os.getpid())
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [nvcc()] + cflags + ["-I" + INCLUDE, "-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd, cwd=CSRC)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(one, _sources()))
+    subprocess.check_call([nvcc()] + NVCC_FLAGS + objs + ["-o", tmp], cwd=CSRC)
+    for o in objs:
+        os.remove(o)
+    os.rmdir(objdir)
     os.replace(tmp, LIB)
     with open(STAMP, "w") as f:
         f.write(h)

@@ -424,8 +424,11 @@ int dws_splits(int N, int OH, int OW, int* kb_per_split) {
     const int RB = OW >= 32 ? 1 : 32 / OW;
     const long long kb_total = (long long)N * (OH / RB) * (OW >= 32 ? OW / 32 : 1);
     const long long need = (kb_total + 255) / 256;
+    // at least min_rounds waves of (3 x splits) CTAs; 4 cost the small batches a 196-split workspace
+    // round trip: VGG b128 vgg2 dW 101 us at 4, 77 us at 2, 64.5 us at 1 (r02z); b4096 needs 11 anyway
+    static const int min_rounds = getenv("SMCONV_DWS_MIN_ROUNDS") ? atoi(getenv("SMCONV_DWS_MIN_ROUNDS")) : 1;
     long long rounds = (3 * need + 147) / 148;
-    if (rounds < 4) rounds = 4;
+    if (rounds < min_rounds) rounds = min_rounds;
     long long smax = rounds * 148 / 3;
     if (smax > kb_total) smax = kb_total;
     if (smax < 1) smax = 1;

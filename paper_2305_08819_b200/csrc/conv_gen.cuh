@@ -65,6 +65,9 @@ struct GenParams {
     // super-pixel stride-2 dX run as a fwd conv (smconv.cu "s2dx"): output row (n, i', j') and
     // column (pi, pj, ic) go to dX[n, 2i'-2+pi, 2j'-2+pj, ic] (rows / columns i' = 0 / j' = 0 dropped)
     int s2dx, s2_IH, s2_IW, s2_IC;
+    // s2dx: taps (a, b) of the 2x2 filter W2 (bit 2a+b) with a non-zero block in n-tile t's columns;
+    // the others are skipped (phase (0,0) has 1 of the 4 taps, (0,1) / (1,0) 2, (1,1) 4)
+    uint8_t s2_tapmask[16];
     // TMA fwd / dX: split-K inside a thread-block cluster of csk CTAs (0 = off): the partial tiles are
     // summed through distributed shared memory instead of an HBM workspace + reduce kernel
     int csk;

@@ -207,7 +207,7 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
             grid = dim3(2 * pairs, 1, 1);
         }
     }
-    if (g.csk && (op == CONV_OP_FWD || op == CONV_OP_BWD_DATA)) {
+    if (g.csk && !g.dwt) {
         // one work item per CTA; the csk splits of a tile form one cluster (TileInfo::init)
         tp.csk = g.csk;
         grid = dim3(tp.work, 1, 1);

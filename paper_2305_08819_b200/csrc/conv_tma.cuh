@@ -168,7 +168,7 @@ struct TileInfo {
         int rest = dv(w, tp.fd_ntiles);
         int nt = w - rest * tp.n_tiles;
         int mt;
-        if (OP != OP_DW && OP != OP_DWT && tp.csk) {
+        if (OP != OP_DWT && tp.csk) {
             // cluster split-K: the splits of one tile are consecutive CTAs (one cluster)
             const int tile = dv(w, tp.fd_csk);
             split = w - tile * tp.csk;
@@ -271,6 +271,7 @@ struct TileInfo {
 #pragma unroll
         for (int g = 0; g < 4; ++g)
             if (g < ngrp) any |= grp[g].w && (unsigned)(grp[g].x + dh) < (unsigned)srcH && (unsigned)(grp[g].y + dw) < (unsigned)srcW;
+        if (OP == OP_FWD && p.s2dx) any &= (p.s2_tapmask[n0 & 15] >> (kh * 2 + kw)) & 1;  // W2 block all zero
         if (any && t)
             *t = make_int4(dh, dw, OP == OP_FWD ? kh * p.FW + kw : p.tf_f[ph_][0][kh] * p.FW + p.tf_f[ph_][1][kw], 0);
         return any;
@@ -285,10 +286,16 @@ struct TileInfo {
             if (!grp[0].w) return 0;
             const int srcH = OP == OP_FWD ? p.IH : p.OH;
             const int srcW = OP == OP_FWD ? p.IW : p.OW;
-            if (OP == OP_FWD) {  // rows / columns of the filter whose source is in range: a clamp, no loop
+            if (OP == OP_FWD && !p.s2dx) {  // rows / columns of the filter whose source is in range: a clamp
                 const int ch = min(nh, srcH - grp[0].x) - max(0, -grp[0].x);
                 const int cw = min(nw, srcW - grp[0].y) - max(0, -grp[0].y);
                 return ch > 0 && cw > 0 ? ch * cw : 0;
+            }
+            if (OP == OP_FWD) {  // s2dx: the zero W2 blocks of this n-tile are skipped
+                int n = 0;
+                for (int kh = 0; kh < nh; ++kh)
+                    for (int kw = 0; kw < nw; ++kw) n += tap_valid(p, kh, kw, nullptr);
+                return n;
             }
             int ch = 0, cw = 0;
             for (int k = 0; k < nh; ++k) ch += (unsigned)(grp[0].x + p.tf_off[ph_][0][k]) < (unsigned)srcH;
@@ -335,8 +342,23 @@ SMCONV_DEV void csk_reduce(const TmaParams& tp, const GenParams& p, uint32_t til
             if (it >= ITEMS) break;
             const int rr = crank * ROWS + it / C4, c4 = it % C4;
             const int col = n0 + 4 * c4;
-            const RowInfo ri = row_info<OP>(p, ti.phase, ti.m0 + rr);
-            if (!ri.ok || col >= p.Ngemm) continue;
+            if (col >= p.Ngemm) continue;
+            long long o;
+            if constexpr (OP == OP_DW) {  // row = output channel; padded (tap, ic) columns drop ic >= IC
+                const int oc = ti.m0 + rr;
+                if (oc >= p.OC) continue;
+                if (p.dw_icp) {
+                    const int tap = (int)fdiv((uint32_t)col, p.fd_icp), ic = col - tap * p.dw_icp;
+                    if (ic >= p.IC) continue;
+                    o = (long long)oc * p.FH * p.FW * p.IC + tap * p.IC + ic;
+                } else {
+                    o = (long long)oc * p.Ngemm + col;
+                }
+            } else {
+                const RowInfo ri = row_info<OP>(p, ti.phase, ti.m0 + rr);
+                if (!ri.ok) continue;
+                o = (long long)ri.orow * p.Ngemm + col;
+            }
             float4 a = v[u][0];
 #pragma unroll
             for (int q = 1; q < S; ++q) {
@@ -345,7 +367,7 @@ SMCONV_DEV void csk_reduce(const TmaParams& tp, const GenParams& p, uint32_t til
                 a.z += v[u][q].z;
                 a.w += v[u][q].w;
             }
-            *reinterpret_cast<float4*>(p.out + (long long)ri.orow * p.Ngemm + col) = a;
+            *reinterpret_cast<float4*>(p.out + o) = a;
         }
     }
 }
@@ -367,7 +389,8 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
     const int rank = PAIR ? (int)cluster_ctarank() : 0;
     const int wfirst = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
     const int wstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-    const uint32_t csk_rank = (!C::IS_DW && !PAIR && tp.csk) ? cluster_ctarank() : 0u;
+    constexpr bool CSK_OK = OP != OP_DWT && !PAIR;  // cluster split-K: fwd / dX / dW (not transposed), 1-CTA tiles
+    const uint32_t csk_rank = (CSK_OK && tp.csk) ? cluster_ctarank() : 0u;
     unsigned long long* const trc = p.trace;
     if (trc && tid == 0) {
         trace_mark(trc, 0);
@@ -798,7 +821,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             const int egrp = (((OP == OP_DX ? p.phase_tile0[ti.phase] : 0) << (tp.pair ? 8 : 7)) + ti.m0 >> 5) + qd;
             // 4 consecutive GEMM columns of this thread's row -> output
             auto st4 = [&](int col, float x, float y, float z, float w4) {
-                if (!C::IS_DW && tp.csk) {  // cluster split-K: this CTA's partial -> own shared memory
+                if (CSK_OK && tp.csk) {  // cluster split-K: this CTA's partial -> own shared memory
                     *reinterpret_cast<float4*>(tiles_ptr + ((size_t)row * C::PSTRIDE + (col - n0)) * 4) =
                         make_float4(x, y, z, w4);
                 } else if (C::IS_DW && p.mc_out) {  // fused dW all-reduce: add into every rank's copy
@@ -939,7 +962,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
     tc_fence_before();
     __syncthreads();
     if (tid == 0) trace_mark(trc, 8);
-    if (!C::IS_DW && !PAIR && tp.csk) {
+    if (CSK_OK && tp.csk) {
         // cluster split-K: every CTA of the cluster holds its partial of the same tile in shared memory
         // [128 rows][PSTRIDE]; CTA r sums rows [r*128/S, (r+1)*128/S) over the S partials (csk_reduce)
         cluster_sync_all();  // release / acquire at cluster scope: all partials visible

@@ -32,6 +32,10 @@ bool dws_supported(int op, int IC, int OC, int FH, int FW, int sh, int sw, int O
 int dws_splits(int N, int OH, int OW, int* kb_per_split);
 int dws_launch(int planes, const GenParams& g, int splits, int kb_per_split, cudaStream_t st, char* err,
                size_t errlen);
+bool stem_supported(int op, int IC, int OC, int FH, int FW);
+int stem_dw_split(long long M, int OC, int* kb_per_cta);
+int stem_launch(int op, int planes, const GenParams& g, int splits, int kb_per_split, cudaStream_t st, char* err,
+                size_t errlen);
 }  // namespace smconv
 
 using namespace smconv;
@@ -210,6 +214,53 @@ int est_taps(const Dims& d) {
     return t < 1 ? 1 : t;
 }
 
+// co-resident clusters of S CTAs (1 CTA per SM, ~200 KB smem): 8 GPCs of ~18 SMs hold 15 clusters
+// of 8 (ncu launch__cluster_max_active, r02d); a grid of 16 clusters ran in two waves (VGG conv11
+// 23.4 us at S = 8 vs 13.8 us at S = 4, r02h), so S is capped to keep one wave
+int max_clusters(int S) { return S <= 2 ? 74 : S <= 4 ? 32 : S <= 8 ? 15 : 7; }
+
+// TMA dW on small maps: (BN, split, cluster split) by an estimate in SM cycles.  Per k-block of a
+// 128 x BN tile: BN * 2 cycles of TF32 MMA (x3 in 3xTF32); waves of 148 CTAs; a cluster split adds
+// the DSMEM reduction of its partial tile (~20 B/cycle/SM, B300_MICROARCH.md) plus two cluster
+// barriers; an HBM split adds its partials' write + the reduce kernel's read (6.5 TB/s) and a launch.
+const int g_dw_csk = getenv("SMCONV_DW_CSK") ? atoi(getenv("SMCONV_DW_CSK")) : 1;
+struct DwChoice { int BN, S, csk; };
+DwChoice dw_choose(int planes, int BN0, int m_tiles, int Ngemm, int nkb, int need_prec, int hbm_splits,
+                   double out_bytes) {
+    const double kSMhz = 1.9e9, kHbm = 6.5e12;
+    auto cost = [&](int BN, int S, bool csk) {
+        const long long ctas = (long long)m_tiles * ((Ngemm + BN - 1) / BN) * S;
+        const double waves = (double)((ctas + kSMs - 1) / kSMs);
+        double c = 2500.0 + waves * ((nkb + S - 1) / S) * (2.0 * BN) * (planes == 2 ? 3 : 1);
+        if (S > 1 && csk) c += 128.0 * BN * 4 * (S - 1) / S / 20.0 + 3000.0;
+        if (S > 1 && !csk) c += (2.0 * S + 1) * out_bytes / kHbm * kSMhz + 6000.0;
+        return c;
+    };
+    const long long hbm_ctas = (long long)m_tiles * ((Ngemm + BN0 - 1) / BN0) * hbm_splits;
+    DwChoice best{BN0, hbm_splits, 0};
+    double bc = cost(BN0, hbm_splits, false);
+    const int bns[2] = {BN0, 128};
+    for (int b = 0; b < 2; ++b) {
+        const int BN = bns[b];
+        if (b == 1 && BN0 <= 128) break;
+        const int t2 = m_tiles * ((Ngemm + BN - 1) / BN);
+        if (t2 <= kSMs && need_prec <= 1) {  // one chain per tile, no split
+            const double c = cost(BN, 1, false);
+            if (c < bc) bc = c, best = DwChoice{BN, 1, 0};
+        }
+        for (int S = 2; S <= g_csk_max && t2 * S <= kSMs && t2 <= max_clusters(S) && 2 * S <= nkb; S *= 2) {
+            // measured (r02x, VGG b128 TF32): csk 4 on 72 CTAs lost to the HBM split on 140 (vgg5 dW 28.6 ->
+            // 33.2 us); csk 2 on 144 CTAs won over the HBM split 4 (vgg8 29.2 -> 23.0 us)
+            if (S < need_prec || 4LL * t2 * S < 3LL * hbm_ctas) continue;
+            const double c = cost(BN, S, true);
+            if (c < bc) bc = c, best = DwChoice{BN, S, S};
+        }
+    }
+    return best;
+}
+
+// SMCONV_STEM=0: keep the stems on DIRECT / GENERIC (A/B experiments)
+const int g_stem = getenv("SMCONV_STEM") ? atoi(getenv("SMCONV_STEM")) : 1;
 const long long g_direct_dw_min_rows =
     getenv("SMCONV_DIRECT_DW_MIN_ROWS") ? atoll(getenv("SMCONV_DIRECT_DW_MIN_ROWS")) : 32768;
 
@@ -226,6 +277,8 @@ Dims mk(int N, int IH, int IW, int IC, int OC, int FH, int FW, int sh, int sw, i
 // N = 4 IC wide with K = 4 OC (full-rate MMAs); the phase walk streamed dY 4x in 128-B rows and
 // starved the MMAs (ncu r01r).  The same sums as O2, in a different order.
 const int g_s2dx = getenv("SMCONV_S2DX") ? atoi(getenv("SMCONV_S2DX")) : 1;
+// SMCONV_S2DX_SKIP=0: issue the all-zero W2 blocks too (A/B experiments)
+const int g_s2dx_skip = getenv("SMCONV_S2DX_SKIP") ? atoi(getenv("SMCONV_S2DX_SKIP")) : 1;
 
 int make_plan_s2dx(const Dims& d, int math, Plan& pl) {
     if (!g_s2dx || g_force[CONV_OP_BWD_DATA].load() != CONV_VARIANT_AUTO) return -1;
@@ -243,6 +296,26 @@ int make_plan_s2dx(const Dims& d, int math, Plan& pl) {
     if (pl.variant != CONV_VARIANT_TMA || pl.splits != 1 || pl.zero_mask) return -1;
     pl.s2dx = 1;
     pl.gp.s2dx = 1;
+    // per n-tile tap mask (GenParams::s2_tapmask): column (pi, pj, ic) has a non-zero W2 block at tap
+    // (a, b) iff (pi == 1 || a == 0) && (pj == 1 || b == 0)
+    {
+        const int nt = (4 * d.IC + pl.BN - 1) / pl.BN;
+        if (nt > 16 || g_s2dx_skip == 0) {
+            memset(pl.gp.s2_tapmask, 0xF, sizeof pl.gp.s2_tapmask);
+        } else {
+            for (int t = 0; t < nt; ++t) {
+                uint8_t m = 0;
+                const int ph0 = t * pl.BN / d.IC, ph1 = ((t + 1) * pl.BN - 1) / d.IC;
+                for (int ph = ph0; ph <= ph1 && ph < 4; ++ph) {
+                    const int pi = ph >> 1, pj = ph & 1;
+                    for (int a = 0; a < 2; ++a)
+                        for (int b = 0; b < 2; ++b)
+                            if ((pi == 1 || a == 0) && (pj == 1 || b == 0)) m |= (uint8_t)(1u << (2 * a + b));
+                }
+                pl.gp.s2_tapmask[t] = m;
+            }
+        }
+    }
     pl.gp.s2_IH = d.IH;
     pl.gp.s2_IW = d.IW;
     pl.gp.s2_IC = d.IC;
@@ -414,6 +487,14 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
         else if (forced == CONV_VARIANT_DIRECT)
             return fail(CONV_EUNSUPPORTED, "%s: DIRECT variant forced but unsupported for this shape", op_name(op));
     }
+    if (forced == CONV_VARIANT_AUTO || forced == CONV_VARIANT_STEM) {
+        // few-channel stems on the tensor cores (conv_stem.cu): replaces DIRECT / GENERIC there
+        const bool stem_ok = g_stem && stem_supported(op, d.IC, d.OC, d.FH, d.FW) &&
+                             (long long)d.N * d.OH * d.OW < (1LL << 31);
+        if (stem_ok) pl.variant = CONV_VARIANT_STEM;
+        else if (forced == CONV_VARIANT_STEM)
+            return fail(CONV_EUNSUPPORTED, "%s: STEM variant forced but unsupported for this shape", op_name(op));
+    }
     if (forced == CONV_VARIANT_AUTO || forced == CONV_VARIANT_DWS) {
         const bool dws_ok = dws_supported(op, d.IC, d.OC, d.FH, d.FW, d.sh, d.sw, d.OH, d.OW);
         if (dws_ok) pl.variant = CONV_VARIANT_DWS;
@@ -528,6 +609,9 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
         if (op == CONV_OP_BWD_FILTER) splits = direct_dw_blocks(d.N, d.OH);
     } else if (pl.variant == CONV_VARIANT_DWS) {
         splits = dws_splits(d.N, d.OH, d.OW, &g.kb_per_split);
+    } else if (pl.variant == CONV_VARIANT_STEM) {
+        // fwd: persistent CTAs over 128-pixel tiles; dW: per-CTA pixel ranges -> fixed-order partial sum
+        if (op == CONV_OP_BWD_FILTER) splits = stem_dw_split((long long)d.N * d.OH * d.OW, d.OC, &g.kb_per_split);
     } else if (op == CONV_OP_BWD_FILTER) {
         // GENERIC accumulates its whole chain in TMEM (no chunked promotion) and tcgen05 adds by
         // truncation, so its 3xTF32 chains are capped at 16 k-blocks (512 products): GoogLeNet b256
@@ -541,8 +625,21 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
         splits = need_prec > fill ? need_prec : fill;
         if (splits > nkb_est) splits = nkb_est;
         if (splits < 1) splits = 1;
+        if (pl.variant == CONV_VARIANT_TMA && !g.dwt && splits > 1 && g_dw_csk) {
+            // small maps (VGG b128 8x8 .. 2x2): the HBM split-K above writes splits x |dW| of partials and
+            // needs a reduce kernel (vgg11 TF32: 2 x 9.4 MB, 28 us for a 1 GFLOP call).  Pick BN and a
+            // cluster split (csk: partials reduced through DSMEM in fixed rank order inside the kernel)
+            // by a cycle estimate; keep the HBM split when it is cheaper (b4096-sized K)
+            const DwChoice c = dw_choose(pl.planes, pl.BN, m_tiles, g.Ngemm, nkb_est, need_prec, splits,
+                                         (double)out_elems * 4);
+            pl.BN = c.BN;
+            n_tiles = (g.Ngemm + pl.BN - 1) / pl.BN;
+            splits = c.S;
+            g.csk = c.csk;
+        }
         g.kb_per_split = (nkb_est + splits - 1) / splits;
         splits = (nkb_est + g.kb_per_split - 1) / g.kb_per_split;
+        if (g.csk) splits = g.csk;  // a cluster has exactly csk CTAs (a split past the end sums nothing)
     } else if (tiles < kSMs && pl.variant == CONV_VARIANT_TMA && g_csk_max >= 2) {
         // small maps (VGG 8x8 .. 2x2 at batch 128): split K inside a cluster and reduce the partial
         // tiles through distributed shared memory (one launch; no HBM workspace, no reduce kernel).
@@ -554,10 +651,7 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
             n_tiles = (g.Ngemm + pl.BN - 1) / pl.BN;
         }
         const int t2 = m_tiles * n_tiles;
-        // co-resident clusters of S CTAs (1 CTA per SM, ~200 KB smem): 8 GPCs of ~18 SMs hold 15 clusters
-        // of 8 (ncu launch__cluster_max_active, r02d); a grid of 16 clusters ran in two waves (VGG conv11
-        // 23.4 us at S = 8 vs 13.8 us at S = 4, r02h), so S is capped to keep one wave
-        auto max_clusters = [](int S2) { return S2 <= 2 ? 74 : S2 <= 4 ? 32 : S2 <= 8 ? 15 : 7; };
+        // S capped by max_clusters (one wave of co-resident clusters)
         int S = 1;
         for (int S2 = 2; S2 <= g_csk_max && t2 * S2 <= kSMs && t2 <= max_clusters(S2) && 2 * S2 <= nkb_est; S2 *= 2)
             S = S2;
@@ -805,6 +899,8 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
         rc = direct_launch(op, g, pl.splits, st, g_detail, sizeof g_detail);
     } else if (pl.variant == CONV_VARIANT_STRIP) {
         rc = strip_launch(op, pl.BN, pl.planes, g, st, g_detail, sizeof g_detail);
+    } else if (pl.variant == CONV_VARIANT_STEM) {
+        rc = stem_launch(op, pl.planes, g, pl.splits, g.kb_per_split, st, g_detail, sizeof g_detail);
     } else if (pl.variant == CONV_VARIANT_DWS) {
         rc = dws_launch(pl.planes, g, pl.splits, g.kb_per_split, st, g_detail, sizeof g_detail);
     } else if (pl.variant == CONV_VARIANT_TMA) {
@@ -825,7 +921,7 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
         int blocks = (int)((n4 + 255) / 256);
         if (blocks > kSMs * 8) blocks = kSMs * 8;
         launch_k(splitk_reduce_kernel<0>, dim3(blocks), dim3(256), 0, st, 1, (const float4*)ws, (float4*)conv_out, n4,
-                 pl.splits, n4, pl.mc_reduce ? out : (float*)nullptr);
+                 pl.gp.csk ? 1 : pl.splits, n4, pl.mc_reduce ? out : (float*)nullptr);
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: reduce launch failed: %s", op_name(op), cudaGetErrorString(e));
     }
@@ -1105,7 +1201,7 @@ int smconv_set_trace(void* device_buf) {
 }
 
 int conv2d_force_variant(int op, int variant) {
-    if (op < 0 || op > 2 || variant < 0 || variant > 5) return fail(CONV_EARG, "conv2d_force_variant: bad op/variant");
+    if (op < 0 || op > 2 || variant < 0 || variant > 6) return fail(CONV_EARG, "conv2d_force_variant: bad op/variant");
     read_env_once();
     g_force[op].store(variant);
     return CONV_OK;
@@ -1123,6 +1219,7 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
         snprintf(buf, len, "variant=%s%s%s BN=%d planes=%d splits=%d grid=%ux%ux%u ws=%zu kernels=%d",
                  pl.s2dx ? "tma s2dx" :
                  pl.variant == CONV_VARIANT_DWS      ? "dws"
+                 : pl.variant == CONV_VARIANT_STEM   ? "stem"
                  : pl.variant == CONV_VARIANT_DIRECT ? "direct"
                  : pl.variant == CONV_VARIANT_STRIP ? "strip"
                  : pl.variant == CONV_VARIANT_TMA   ? "tma"

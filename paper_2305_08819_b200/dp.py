@@ -133,7 +133,7 @@ class ConvNetStep:
 
     def __init__(self, net: str, batch: int, device, math: str = "3xtf32", seed: int = 0,
                  bucket_mb: float = 16.0, chain: bool = True, rank: int = 0, epi: bool = False,
-                 leaky_k: float = 0.01, mcast_group=None):
+                 leaky_k: float = 0.01, mcast_group=None, dw_stream: bool = False):
         import torch
         self.torch = torch
         self.net = net
@@ -215,6 +215,15 @@ class ConvNetStep:
         ws = torch.empty(max(mx, 16), dtype=torch.uint8, device=device) if mx else None
         for b in self.bufs:
             b.ws = ws
+        # dW on a second stream (dw_stream): dW_l needs only X_l and dY_l, nothing on the critical dX
+        # chain needs it, so it runs beside the next dX calls (small-map layers leave SMs idle: 64-CTA
+        # cluster grids, prologues, split-K tails).  Its calls get their own workspace.
+        self.side = None
+        self.ws_dw = None
+        if dw_stream:
+            self.side = torch.cuda.Stream(device=device)
+            mdw = max(b.ws_bytes[2] for b in self.bufs)
+            self.ws_dw = torch.empty(max(mdw, 16), dtype=torch.uint8, device=device) if mdw else None
         # buckets over the backward-ordered flat buffer
         self.buckets = plan_buckets(sizes, int(bucket_mb * (1 << 20) / 4))
         if self.mc_ptr:
@@ -237,7 +246,7 @@ class ConvNetStep:
 
     # ---------------------------------------------------------------- one step
     def _call(self, op, b: LayerBuf, a, bb, out, stream):
-        ws = b.ws
+        ws = self.ws_dw if (op == 2 and self.side is not None) else b.ws
         if op == 2 and self.mc_ptr:  # dW + all-reduce in the dW kernels, into the multicast address
             i = self.bufs.index(b)
             sm.raw_call_mcast(a.data_ptr(), bb.data_ptr(), self.mc_ptr + 4 * self.dw_offs[i], b.layer.dims(self.batch),
@@ -281,19 +290,33 @@ class ConvNetStep:
             # every rank's dW copy is zero before any rank adds into it (smconv_mcast.h contract)
             self.dw_flat.zero_()
             self.mc_handle.barrier()
+        side = self.side
+        if side is not None:
+            side.wait_stream(torch.cuda.current_stream(self.device))  # X of every layer, the loss gradients
         for i in reversed(range(len(self.bufs))):
             b = self.bufs[i]
             # dW first: its bucket's all-reduce (NCCL waits on this stream's work so far) then
             # overlaps this layer's dX and the rest of the backward pass
-            mark(("dw", i, 0))
-            self._call(2, b, b.X, b.dY, b.dW, stream)
-            mark(("dw", i, 1))
+            if side is not None:
+                side.wait_stream(torch.cuda.current_stream(self.device))  # dY_l (the previous dX)
+                with torch.cuda.stream(side):
+                    mark(("dw", i, 0))
+                    self._call(2, b, b.X, b.dY, b.dW, side.cuda_stream)
+                    mark(("dw", i, 1))
+            else:
+                mark(("dw", i, 0))
+                self._call(2, b, b.X, b.dY, b.dW, stream)
+                mark(("dw", i, 1))
             if pg is not None and not self.mc_ptr:
+                if side is not None:
+                    torch.cuda.current_stream(self.device).wait_stream(side)
                 handles += allreduce_buckets(self.dw_flat, self.buckets, pg, ready_layer=i)
             if i > 0:
                 mark(("dx", i, 0))
                 self._call(1, b, b.dY, b.W, b.dX, stream)
                 mark(("dx", i, 1))
+        if side is not None:
+            torch.cuda.current_stream(self.device).wait_stream(side)
         for h in handles:
             h.wait()
         if self.mc_ptr:

@@ -19,6 +19,7 @@ CONV_MATH_FP32_3XTF32, CONV_MATH_TF32 = 0, 1
 CONV_OP_FWD, CONV_OP_BWD_DATA, CONV_OP_BWD_FILTER = 0, 1, 2
 CONV_VARIANT_AUTO, CONV_VARIANT_GENERIC, CONV_VARIANT_TMA, CONV_VARIANT_STRIP, CONV_VARIANT_DIRECT = 0, 1, 2, 3, 4
 CONV_VARIANT_DWS = 5
+CONV_VARIANT_STEM = 6
 MATH = {"3xtf32": CONV_MATH_FP32_3XTF32, "fp32": CONV_MATH_FP32_3XTF32, "tf32": CONV_MATH_TF32}
 
 EXPORTS = ("conv2d_out_hw", "conv2d_workspace_bytes", "conv2d_fwd", "conv2d_bwd_data", "conv2d_bwd_filter",

@@ -132,12 +132,22 @@ def test_plans_cover_network_shapes(sm):
                         ("s2dx" in d), (l.name, op, d)
 
 
-def test_stem_dw_heuristic(sm):
-    """Stem dW: GENERIC split-K below 32768 (n, oh) rows, DIRECT above (measured crossover, r01z)."""
-    for N, want in ((128, "generic"), (512, "generic"), (1024, "direct"), (4096, "direct")):
+def test_stem_plans(sm):
+    """The IC = 4 3x3 stems (every network's first conv) go to the tensor-core STEM variant: fwd for
+    OC 64 / 128 / 192, dW for any OC % 4 == 0 (per-CTA pixel ranges + the fixed-order partial sum);
+    other few-channel shapes keep DIRECT / GENERIC."""
+    for N in (128, 512, 4096):
         s = (N, 32, 32, 4, 64, 3, 3, 1, 1, 1, 1)
-        assert "variant=" + want in sm.plan_describe(2, s, 0), (N, sm.plan_describe(2, s, 0))
-        assert "variant=direct" in sm.plan_describe(0, s, 0)  # fwd stays DIRECT
+        for math in (0, 1):
+            assert sm.plan_describe(0, s, math).startswith("variant=stem"), sm.plan_describe(0, s, math)
+            d = sm.plan_describe(2, s, math)
+            assert d.startswith("variant=stem") and sm.plan_kernels(2, s, math) == 2, d
+            assert sm.plan_kernels(0, s, math) == 1
+    assert sm.plan_describe(0, (256, 32, 32, 4, 192, 3, 3, 1, 1, 1, 1), 0).startswith("variant=stem")
+    assert not sm.plan_describe(0, (8, 32, 32, 4, 96, 3, 3, 1, 1, 1, 1), 0).startswith("variant=stem")
+    assert sm.plan_describe(2, (8, 32, 32, 4, 96, 3, 3, 1, 1, 1, 1), 0).startswith("variant=stem")
+    assert not sm.plan_describe(0, (8, 32, 32, 8, 64, 3, 3, 1, 1, 1, 1), 0).startswith("variant=stem")
+    assert not sm.plan_describe(0, (8, 32, 32, 4, 64, 5, 5, 1, 1, 2, 2), 0).startswith("variant=stem")
 
 
 def test_force_variant(sm):
@@ -148,11 +158,11 @@ def test_force_variant(sm):
         sm.force_variant(5, 0)
 
 
-VARIANT_NAMES = {1: "generic", 2: "tma", 3: "strip", 4: "direct", 5: "dws"}
+VARIANT_NAMES = {1: "generic", 2: "tma", 3: "strip", 4: "direct", 5: "dws", 6: "stem"}
 
 
 @pytest.mark.parametrize("op", [0, 1, 2])
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6])
 def test_forced_variant_is_served_or_refused(sm, op, variant):
     """Forcing a variant either yields a plan of THAT variant or CONV_EUNSUPPORTED -- never a plan whose
     launch would write the wrong buffer extent (e.g. STRIP forced for dW)."""
@@ -177,7 +187,11 @@ def test_direct_only_when_launch_fits(sm):
     then return CONV_EUNSUPPORTED for a valid call)."""
     assert "direct" not in sm.plan_describe(0, (8, 8, 8, 8, 1024, 3, 3, 1, 1, 1, 1), 0)
     assert "direct" not in sm.plan_describe(2, (2048, 32, 32, 8, 256, 3, 3, 1, 1, 1, 1), 0)
-    assert "direct" in sm.plan_describe(0, (4096, 32, 32, 4, 64, 3, 3, 1, 1, 1, 1), 0)  # the stem still is
+    sm.force_variant(0, sm.CONV_VARIANT_DIRECT)
+    try:  # the stem still fits DIRECT when forced (AUTO now sends it to STEM)
+        assert "direct" in sm.plan_describe(0, (4096, 32, 32, 4, 64, 3, 3, 1, 1, 1, 1), 0)
+    finally:
+        sm.force_variant(0, 0)
 
 
 def test_plan_cache_tracks_forced_variant(sm):

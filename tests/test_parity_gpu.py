@@ -446,6 +446,69 @@ def test_direct_parity(env, force_direct, s):
                 assert normwise(y, ry) <= 1e-6 and normwise(dw, rw) <= 1e-6, (normwise(y, ry), normwise(dw, rw))
 
 
+# ---------------------------------------------------------------- STEM variant (IC = 4 stems, tensor cores)
+SWEEP_STEM = [
+    (4, 32, 32, 4, 64, 3, 3, 1, 1, 1, 1),     # the CIFAR stem (IC 3 -> 4)
+    (77, 30, 30, 4, 64, 3, 3, 1, 1, 1, 1),    # 541 tiles of 128 pixels, ragged last tile; 2166 dW k-blocks
+    (3, 9, 13, 4, 64, 3, 3, 2, 2, 1, 1),      # stride 2, ragged map
+    (30, 32, 32, 4, 128, 3, 3, 1, 1, 1, 1),   # OC 128, 240 tiles (148 persistent CTAs)
+    (5, 7, 7, 4, 192, 3, 3, 1, 1, 0, 0),      # GoogLeNet-stem OC (two dW m-tiles), no padding
+    (40, 32, 32, 4, 192, 3, 3, 1, 1, 1, 1),   # OC 192 (one accumulator, 4 A slots), 320 tiles: 2-3 per CTA
+    (3, 11, 6, 4, 20, 3, 3, 1, 1, 2, 2),      # dW only (fwd OC must be 64 / 128 / 192), pad 2
+]
+
+
+@pytest.fixture
+def force_stem(env):
+    _, _, sm = env
+    for op in (0, 2):
+        sm.force_variant(op, sm.CONV_VARIANT_STEM)
+    yield
+    for op in (0, 2):
+        sm.force_variant(op, sm.CONV_VARIANT_AUTO)
+
+
+@pytest.mark.parametrize("s", SWEEP_STEM, ids=_id)
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+def test_stem_parity(env, force_stem, s, math, parity_log):
+    torch, oracle, sm = env
+    N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw = s
+    fwd_ok = OC in (64, 128, 192)
+    if fwd_ok:
+        assert "stem" in sm.plan_describe(0, s, sm.MATH[math])
+    assert "stem" in sm.plan_describe(2, s, sm.MATH[math])
+    for integer in (2, 0):
+        X, W, dY = gen(s, 50 + integer, integer=integer, stem=not integer)
+        x, w, dy = (torch.from_numpy(a).cuda() for a in (X, W, dY))
+        rw = oracle.conv2d_bwd_filter(X, dY, (FH, FW), (sh, sw), (ph, pw))
+        dw = sm.conv2d_bwd_filter(x, dy, (FH, FW), (sh, sw), (ph, pw), math=math).cpu().numpy()
+        outs = [("dw", dw, rw)]
+        if fwd_ok:
+            ry = oracle.conv2d_fwd(X, W, (sh, sw), (ph, pw))
+            y = sm.conv2d_fwd(x, w, (sh, sw), (ph, pw), math=math).cpu().numpy()
+            outs.append(("fwd", y, ry))
+        for name, got, ref in outs:
+            if integer:
+                assert np.array_equal(got.astype(np.float64), ref), name
+            else:
+                e = normwise(got, ref)
+                parity_log.append({"config": "stem-sweep", "layer": "x".join(map(str, s)), "op": name, "math": math,
+                                   "normwise": e, "tol": TOL[math],
+                                   "plan": sm.plan_describe({"fwd": 0, "dw": 2}[name], s, sm.MATH[math])})
+                assert e <= TOL[math], (name, e)
+
+
+def test_stem_deterministic(env):
+    """dW partials are summed in a fixed order: two calls are bitwise identical."""
+    torch, oracle, sm = env
+    s = (64, 32, 32, 4, 64, 3, 3, 1, 1, 1, 1)
+    X, W, dY = gen(s, 7)
+    x, dy = torch.from_numpy(X).cuda(), torch.from_numpy(dY).cuda()
+    a = sm.conv2d_bwd_filter(x, dy, (3, 3), (1, 1), (1, 1))
+    b = sm.conv2d_bwd_filter(x, dy, (3, 3), (1, 1), (1, 1))
+    assert "stem" in sm.plan_describe(2, s) and torch.equal(a, b)
+
+
 # ---------------------------------------------------------------- DWS variant (dW, 3x3 s1 64->64)
 SWEEP_DWS = [
     (2, 32, 32, 64, 64, 3, 3, 1, 1, 1, 1),    # r.l1 / vgg2 geometry: one output row per k-block
