@@ -324,38 +324,45 @@ SMCONV_DEV void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint64_t* bar,
         : "memory");
 }
 
-template <int PLANES>
+template <int PLANES, int OCB>
 struct StemDwCfg {
     static constexpr int TMA_W = 0, BLD_W0 = 1, NBLD = 4, CONV_W0 = 5, PRO_W0 = 9, MMA_W = 13;
     static constexpr int NTHREADS = 14 * 32;
-    static constexpr int STAGES = 4;
-    static constexpr int A_BYTES = 128 * 32 * 4;       // [32 px][128 oc] MN-major: 4 blocks of [32 px][32 oc]
+    // A = [32 px][OCB x 32 oc] MN-major (OCB = 2 for OC <= 64: the M = 128 MMA's rows 64..127 then read
+    // whatever follows in the stage -- rows nobody stores); the dY stream is latency-bound, so the
+    // narrower stage buys ring depth (4 stages of 44 KB held ~3.6k cycles of look-ahead for ~1-2 us of
+    // HBM latency: conv1 dW 2.7 TB/s, ncu r02aa)
+    static constexpr int A_BYTES = OCB * 4096;
     static constexpr int B_BYTES = kDwN * 128;         // [48 k][32 px] K-major SW128
     static constexpr int STAGE = PLANES * (A_BYTES + B_BYTES);
+    static constexpr int STAGES_RAW = (200 * 1024) / STAGE;
+    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
     static constexpr int CHUNK = 8;                    // promotion interval (k-blocks)
-    static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+    static constexpr int PAD = (4 - OCB) * 4096;       // the last stage's junk-row reads stay inside the allocation
+    static constexpr int SMEM = 1024 + STAGES * STAGE + PAD + 256;
+    static_assert(STAGES >= NBLD, "builders own k-blocks mod 4: the ring must be at least that deep");
 };
 
 struct StemDwAux {
-    uint64_t afull[4], cfull[4], bfull[4], sfree[4], accfull[2], accfree[2];
+    uint64_t afull[8], cfull[8], bfull[8], sfree[8], accfull[2], accfree[2];
     uint32_t tmem_base;
 };
 
 // grid (pixel ranges, m-tiles of 128 output channels).  dY arrives by TMA as MN-major [32 px][32 oc]
 // boxes (the layout the tensor core reads A from, SWIZZLE_128B_BASE32B), so the MMAs are SS-form:
 // A = dY^T (M = oc), B = Xcol^T (N = k) built by CUDA-core threads, K = 32 pixels per k-block.
-template <int PLANES>
-__global__ void __launch_bounds__(StemDwCfg<PLANES>::NTHREADS, 1)
+template <int PLANES, int OCB>
+__global__ void __launch_bounds__(StemDwCfg<PLANES, OCB>::NTHREADS, 1)
     stem_dw_kernel(const __grid_constant__ StemParams p, const __grid_constant__ CUtensorMap mapA) {
-    using C = StemDwCfg<PLANES>;
+    using C = StemDwCfg<PLANES, OCB>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* bptr = smem_raw + (base - raw);
-    StemDwAux* aux = reinterpret_cast<StemDwAux*>(bptr + C::STAGES * C::STAGE);
+    StemDwAux* aux = reinterpret_cast<StemDwAux*>(bptr + C::STAGES * C::STAGE + C::PAD);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int oc0 = blockIdx.y * 128;
-    const int nblk = min(4, (p.OC - oc0 + 31) / 32);  // 32-channel dY boxes of this m-tile
+    const int nblk = min(OCB, (p.OC - oc0 + 31) / 32);  // 32-channel dY boxes of this m-tile
 
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
@@ -613,14 +620,16 @@ int stem_launch(int op, int planes, const GenParams& g, int splits, int kb_per_s
     auto go = [&](auto kern, int smem) -> int {
         int rc = set_smem(kern, smem, err, errlen);
         if (rc) return rc;
-        const cudaError_t e = launch_k(kern, grid, dim3(StemDwCfg<1>::NTHREADS), smem, st, 1, p, mapA);
+        const cudaError_t e = launch_k(kern, grid, dim3(StemDwCfg<1, 4>::NTHREADS), smem, st, 1, p, mapA);
         if (e != cudaSuccess) {
             snprintf(err, errlen, "stem dw launch: %s", cudaGetErrorString(e));
             return CONV_ECUDA;
         }
         return CONV_OK;
     };
-    return planes == 2 ? go(stem_dw_kernel<2>, StemDwCfg<2>::SMEM) : go(stem_dw_kernel<1>, StemDwCfg<1>::SMEM);
+    if (g.OC <= 64)
+        return planes == 2 ? go(stem_dw_kernel<2, 2>, StemDwCfg<2, 2>::SMEM) : go(stem_dw_kernel<1, 2>, StemDwCfg<1, 2>::SMEM);
+    return planes == 2 ? go(stem_dw_kernel<2, 4>, StemDwCfg<2, 4>::SMEM) : go(stem_dw_kernel<1, 4>, StemDwCfg<1, 4>::SMEM);
 }
 
 }  // namespace smconv

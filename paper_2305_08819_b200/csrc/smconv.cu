@@ -398,6 +398,10 @@ void plan_mcast(Plan& pl) {
     }
 }
 
+// split-K reduce form: one warp per output float4 when the output is small (<= 148 x 2048 lanes) and
+// the partials many (splitk_reduce_wide_kernel)
+bool reduce_wide(long long n4, int splits) { return splits >= 16 && n4 * 32 <= (long long)kSMs * 2048; }
+
 int plan_kernel_count(const Plan& pl) {
     return 1 + ((pl.splits > 1 && !pl.gp.csk) || pl.mc_reduce) + (pl.zero_mask != 0) + (pl.wx_bytes != 0) + (pl.s2dx != 0) +
            (pl.epi && !pl.epi_fused) + 2 * epi_has_stats(pl.epi);
@@ -918,10 +922,17 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
     if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: kernel launch failed: %s", op_name(op), cudaGetErrorString(e));
     if (ws_split) {
         const long long n4 = pl.out_elems / 4;
-        int blocks = (int)((n4 + 255) / 256);
-        if (blocks > kSMs * 8) blocks = kSMs * 8;
-        launch_k(splitk_reduce_kernel<0>, dim3(blocks), dim3(256), 0, st, 1, (const float4*)ws, (float4*)conv_out, n4,
-                 pl.gp.csk ? 1 : pl.splits, n4, pl.mc_reduce ? out : (float*)nullptr);
+        const int nsp = pl.gp.csk ? 1 : pl.splits;
+        if (reduce_wide(n4, nsp)) {  // many partials of a small output: one warp per float4
+            const int blocks = (int)((n4 * 32 + 255) / 256);
+            launch_k(splitk_reduce_wide_kernel<0>, dim3(blocks), dim3(256), 0, st, 1, (const float4*)ws,
+                     (float4*)conv_out, n4, nsp, n4, pl.mc_reduce ? out : (float*)nullptr);
+        } else {
+            int blocks = (int)((n4 + 255) / 256);
+            if (blocks > kSMs * 8) blocks = kSMs * 8;
+            launch_k(splitk_reduce_kernel<0>, dim3(blocks), dim3(256), 0, st, 1, (const float4*)ws, (float4*)conv_out,
+                     n4, nsp, n4, pl.mc_reduce ? out : (float*)nullptr);
+        }
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail(CONV_ECUDA, "%s: reduce launch failed: %s", op_name(op), cudaGetErrorString(e));
     }

@@ -308,8 +308,8 @@ class ConvNetStep:
                 self._call(2, b, b.X, b.dY, b.dW, stream)
                 mark(("dw", i, 1))
             if pg is not None and not self.mc_ptr:
-                if side is not None:
-                    torch.cuda.current_stream(self.device).wait_stream(side)
+                if side is not None and any(r == i for (r, _, _) in self.buckets):
+                    torch.cuda.current_stream(self.device).wait_stream(side)  # the bucket's dW are written
                 handles += allreduce_buckets(self.dw_flat, self.buckets, pg, ready_layer=i)
             if i > 0:
                 mark(("dx", i, 0))
