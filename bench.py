@@ -51,9 +51,11 @@ def parse():
                     help="replay the timed steps as one CUDA graph (auto: on at 1 GPU).  Measured: no gain at "
                          "batch 4096/512 or VGG b128 (the GPU, not the host, bounds the step), and per-call "
                          "event nodes inside a graph are less reliable, so the default stays eager")
-    ap.add_argument("--dw-stream", default="on", choices=["on", "off"],
+    ap.add_argument("--dw-stream", default="auto", choices=["auto", "on", "off"],
                     help="run every dW on a second stream beside the dX chain (dp.ConvNetStep dw_stream); "
-                         "measured r02aa/r02z: VGG-16 b128 -4..5 %%, ResNet-18 b512 -4.3 %%, b4096 -0.4 %% step time")
+                         "measured r02aa/r02z: VGG-16 b128 -4..5 %%, ResNet-18 b512 -4.3 %%, b4096 -0.4 %% step "
+                         "time.  auto = on below 1024 images per GPU (at b4096 the gain is noise and the dominant "
+                         "call's live duration would include its overlap with the dX kernels)")
     ap.add_argument("--layers-out", default=os.path.join(ROOT, "gpurun_out", "bench_layers.json"))
     a = ap.parse_args()
     if a.global_batch is None:
@@ -269,10 +271,11 @@ def main():
     if a.global_batch % world:
         raise SystemExit("global batch %d not divisible by %d ranks" % (a.global_batch, world))
     B = a.global_batch // world
+    dw_stream = a.dw_stream == "on" or (a.dw_stream == "auto" and B < 1024)
     # filters replicated (rank-independent seed); activations / loss gradients differ per shard
     step = dp.ConvNetStep(a.net, B, dev, math=a.math, seed=1, bucket_mb=a.bucket_mb, rank=rank, epi=a.epi,
                           mcast_group=(pg if pg is not None else _world1_group(dev)) if a.fused_allreduce else None,
-                          dw_stream=a.dw_stream == "on")
+                          dw_stream=dw_stream)
     torch.cuda.synchronize()
 
     def barrier():
@@ -288,8 +291,8 @@ def main():
     # event between two kernels serialises them (no programmatic dependent launch overlap) and adds its
     # own cost, so per-call events on every call would distort the step being measured.
     prof_events = []
-    for _ in range(2):
-        step.step(pg, events=prof_events)
+    for _ in range(2):  # serial: per-call times of kernels that do not share the GPU with a dW stream
+        step.step(pg, events=prof_events, serial=True)
     torch.cuda.synchronize()
     prof = {}
     pend = {}
@@ -420,7 +423,7 @@ def main():
                       "fwd_dx_cross_terms": "bf16" if a.math == "3xtf32" else None,
                       "epilogue": ("fused: fwd + BN statistics, dX + LeakyReLU backward + BN-backward statistics"
                                    if a.epi else "none (plain conv outputs)"),
-                      "cuda_graph": graph is not None, "dw_stream": a.dw_stream == "on",
+                      "cuda_graph": graph is not None, "dw_stream": dw_stream,
                       "parallelism": "dp%d" % world,
                       "dw_allreduce": ("fused in the dW kernels (NVLink multicast multimem.red)" if a.fused_allreduce
                                        else "NCCL all_reduce SUM, bucketed, async" if world > 1 else "none (1 GPU)"), "l2": "inputs larger than L2 (per-step working set "

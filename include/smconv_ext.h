@@ -46,6 +46,13 @@ int conv2d_force_variant(int op, int variant);
  * dW pairs -> 57.5 ms).  Returns the previous value. */
 int smconv_set_pair(int on);
 
+/* 3xTF32 fwd / dX on the TMA variant: calls with less than `gflop` GFLOP of valid-tap work run three
+ * TF32 MMAs per product with b_lo split in the kernel ("3mma" in the plan text) instead of the hybrid
+ * form (a_hi*b_hi TF32 + the cross terms as one K-doubled bf16 MMA on a W' plane that a separate
+ * wx_prep kernel builds per call).  Default 12 (SMCONV_HYB_MIN_GFLOP at load time); 0 = always hybrid.
+ * Clears the plan cache.  Returns the previous value. */
+double smconv_set_hybrid_min_gflop(double gflop);
+
 /* Plan the call would use, as text: "variant=.. BN=.. splits=.. tiles=.. kernels=..".
  * Returns CONV_OK and writes at most `len` bytes (NUL-terminated) into `buf`. */
 int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, int FW,

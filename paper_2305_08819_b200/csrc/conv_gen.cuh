@@ -65,6 +65,10 @@ struct GenParams {
     // super-pixel stride-2 dX run as a fwd conv (smconv.cu "s2dx"): output row (n, i', j') and
     // column (pi, pj, ic) go to dX[n, 2i'-2+pi, 2j'-2+pj, ic] (rows / columns i' = 0 / j' = 0 dropped)
     int s2dx, s2_IH, s2_IW, s2_IC;
+    // TMA fwd / dX in 3xTF32: 1 = hybrid (a_hi*b_hi TF32 + the cross terms as one K-doubled bf16 MMA on
+    // the precomputed W' plane), 0 = three TF32 MMAs with b_lo split by the converter warps (no W' plane,
+    // no wx_prep kernel: the small-map calls, where that launch cost more than the third MMA)
+    int hyb;
     // s2dx: taps (a, b) of the 2x2 filter W2 (bit 2a+b) with a non-zero block in n-tile t's columns;
     // the others are skipped (phase (0,0) has 1 of the 4 taps, (0,1) / (1,0) 2, (1,1) 4)
     uint8_t s2_tapmask[16];

@@ -263,7 +263,7 @@ int tma_launch(int op, int BN, int planes, const GenParams& g, TmaParams& tp, di
         uint64_t db[3] = {IC, T, OC}, sb[2] = {IC * 4, T * IC * 4};
         uint32_t bb[3] = {32, 1, (uint32_t)(tp.pair ? BN / 2 : BN)};  // a pair splits B by columns
         ok &= encode(&tp.mapB, g.B, 3, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B);
-        if (planes == 2) ok &= g.Bx && tma_encode_wx(&tp.mapBx, g.Bx, (int)OC, (int)IC, (int)T, tp.pair ? BN / 2 : BN);
+        if (planes == 2 && g.hyb) ok &= g.Bx && tma_encode_wx(&tp.mapBx, g.Bx, (int)OC, (int)IC, (int)T, tp.pair ? BN / 2 : BN);
     } else if (op == CONV_OP_BWD_DATA) {
         // A = dY (OC, OW, OH, N); B = W viewed (32 ic, OC, IC/32, T), MN-major
         uint64_t da[4] = {OC, OW, OH, N}, sa[3] = {OC * 4, OW * OC * 4, OH * OW * OC * 4};
@@ -279,7 +279,7 @@ int tma_launch(int op, int BN, int planes, const GenParams& g, TmaParams& tp, di
             uint32_t bb[3] = {32, 32, 1};
             ok &= encode(&tp.mapB, g.B, 3, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
         }
-        if (planes == 2) ok &= g.Bx && tma_encode_wx(&tp.mapBx, g.Bx, (int)IC, (int)OC, (int)T, tp.pair ? BN / 2 : BN);
+        if (planes == 2 && g.hyb) ok &= g.Bx && tma_encode_wx(&tp.mapBx, g.Bx, (int)IC, (int)OC, (int)T, tp.pair ? BN / 2 : BN);
     } else if (g.dwt) {
         // transposed dW: A = X viewed (32 ic, N, IC/32, IW, IH), B = dY viewed (32 oc, N, OC/32, OH*OW)
         uint64_t da[5] = {32, N, IC / 32, IW, IH}, sa[4] = {IH * IW * IC * 4, 128, IC * 4, IW * IC * 4};

@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
     if (warp == C::TMA_W && lane == 0) {
         prefetch_tmap(&tp.mapA);
         prefetch_tmap(&tp.mapB);
-        if (C::HYB) prefetch_tmap(&tp.mapBx);
+        if (C::HYB && p.hyb) prefetch_tmap(&tp.mapBx);
     }
     if (warp == C::MMA_W) {
         if (PAIR) tmem_alloc2(&aux->tmem_base, C::TMEM_COLS);
@@ -430,7 +430,10 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
     const uint32_t tmem = aux->tmem_base;
     if (tid == 0) trace_mark(trc, 1);
     pdl_trigger();
-    pdl_wait();  // launch.cuh: no global-memory access before the previous kernels completed
+    // launch.cuh: no global-memory access before the previous kernels completed.  The wait sits in
+    // each role right before its first global access, so the producer's first-tile bookkeeping (work
+    // item decode + tap list, ~1.5 us on a cold CTA, r02j trace) overlaps the previous kernel's tail
+    // under programmatic dependent launch; the MMA and converter warps touch only smem / TMEM.
 
     if (warp == C::TMA_W) {
         // ======================= TMA producer
@@ -441,6 +444,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             int s = 0;
             uint32_t r = 0;  // stage index, ring round
             int4* taps = aux->ptaps;
+            bool waited = false;  // pdl_wait before the first TMA load
             for (int w = wfirst; w < tp.work; w += wstep) {
                 TileInfo<OP> ti;
                 ti.init(tp, p, w, rank);
@@ -457,6 +461,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                             if (ti.tap_valid(p, kh, kw, &taps[nt])) ++nt;  // same value from every lane
                     __syncwarp();
                     if (trc && lane == 0 && w == wfirst) trace_mark(trc, 12);
+                    if (!waited) pdl_wait(), waited = true;
                     int j = (int)fdiv((uint32_t)ti.kb_begin, tp.fd_CB), cb = ti.kb_begin - j * tp.CB;
                     int4 tap = taps[j];
                     for (int it = 0; it < nkb; ++it) {
@@ -468,7 +473,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                         const uint32_t sB = sA + C::B_OFF;
                         if (trc && lane == 0 && r == 0 && s == 0) trace_mark(trc, 2);
                         if (elect_one()) {
-                            mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + (C::HYB ? 2 : 1) * C::B_BYTES);
+                            mbar_arrive_expect_tx(&aux->full[s], C::A_BYTES + (C::HYB && p.hyb ? 2 : 1) * C::B_BYTES);
 #pragma unroll
                             for (int g = 0; g < 4; ++g)
                                 if (g < ti.ngrp) tma_load_4d(sA + g * tp.G * 128, &tp.mapA, &aux->full[s], cb * 32,
@@ -483,7 +488,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                             } else {
                                 tma_load_4d(sB, &tp.mapB, &aux->full[s], 0, cb * 32, nb0 / 32, tap.z);
                             }
-                            if (C::HYB) tma_load_4d(sB + C::B_BYTES, &tp.mapBx, &aux->full[s], 0, cb, nb0, tap.z);
+                            if (C::HYB && p.hyb) tma_load_4d(sB + C::B_BYTES, &tp.mapBx, &aux->full[s], 0, cb, nb0, tap.z);
                         }
                         __syncwarp();
                         if (++cb == tp.CB) {
@@ -516,6 +521,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                         ++nbox;
                     }
                     __syncwarp();
+                    if (!waited) pdl_wait(), waited = true;
                     const uint32_t xbytes = nbox * bcols * 128;
                     const uint32_t tx = OP == OP_DWT ? xbytes + C::B_BYTES : C::A_BYTES + xbytes;
                     for (int it = 0; it < nkb; ++it) {
@@ -622,14 +628,14 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                             const uint64_t adH = adH0 + so + g * A_G, bdH = bdH0 + so + g * B_G;
                             const uint32_t acc0 = (in_chunk > 0 || g > 0) ? 1u : 0u;
                             const uint32_t ahi = tmem + (uint32_t)(C::A_TCOL0 + t * 64 + g * 8);
-                            if (C::HYB) {  // a_hi * b_hi (TF32); cross terms below
+                            if (C::HYB && p.hyb) {  // a_hi * b_hi (TF32); cross terms below
                                 if (PAIR) mma2_tf32_ts(d, ahi, bdH, IDESC, acc0);
                                 else mma_tf32_ts(d, ahi, bdH, IDESC, acc0);
-                            } else if (C::A_TMEM && PAIR) {  // dW pairs: three TF32 MMAs, M = 256
+                            } else if (C::A_TMEM && PAIR) {  // three TF32 MMAs, M = 256 (dW; fwd / dX !hyb)
                                 mma2_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);
                                 mma2_tf32_ts(d, ahi, bdH + (C::B_BYTES >> 4), IDESC, 1u);
                                 mma2_tf32_ts(d, ahi, bdH, IDESC, 1u);
-                            } else if (C::A_TMEM) {  // dW: three TF32 MMAs, b_lo plane after b_hi
+                            } else if (C::A_TMEM) {  // three TF32 MMAs, b_lo plane after b_hi (dW; fwd / dX !hyb)
                                 mma_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);
                                 mma_tf32_ts(d, ahi, bdH + (C::B_BYTES >> 4), IDESC, 1u);
                                 mma_tf32_ts(d, ahi, bdH, IDESC, 1u);
@@ -637,7 +643,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                                 mma_tf32_ss(d, adH, bdH, IDESC, acc0);
                             }
                         }
-                        if (C::HYB) {
+                        if (C::HYB && p.hyb) {
                             // cross terms a_hi*b_lo + a_lo*b in bf16: A' = [bf16(a_hi) | bf16(a_lo)]
                             // (TMEM, 32 columns), B' = [bf16(b_lo) | bf16(b)]: K = 64 in 4 MMAs
 #pragma unroll
@@ -729,7 +735,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     // pairs, [48,64) bf16(a_lo) likewise; this thread has k in [16h, 16h+16)
                     // (dW: [32,64) a_lo fp32 for the third TF32 MMA)
                     const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(C::A_TCOL0 + t * 64);
-                    if (C::HYB) {
+                    if (C::HYB && p.hyb) {
                         uint32_t hi[16], xh[8], xl[8];
                         split_a16(e, hi, xh, xl);
                         tmem_st_32x32b_x16(ta + h * 16, hi);
@@ -757,7 +763,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
 #pragma unroll
                     for (int i = 0; i < NA; ++i) aL[ct + i * NCT] = lo4(va[i]);
                 }
-                if (!C::HYB) {  // b_lo plane (dW, and the TF32-free SS fallback)
+                if (!(C::HYB && p.hyb)) {  // b_lo plane (dW, fwd / dX without the W' plane, the SS fallback)
                     const float4* bH = reinterpret_cast<const float4*>(st + C::B_OFF);
                     float4* bL = reinterpret_cast<float4*>(st + C::B_OFF + C::B_BYTES);
                     float4 vb[NB];
@@ -779,6 +785,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
         }
     } else {
         // ======================= epilogue warps 0-7 (+ promotion of TMEM chunks, 3xTF32)
+        pdl_wait();  // global stores (and the fused epilogue's reads of A) follow
         const int qd = warp & 3, half = warp >> 2;
         const int row = qd * 32 + lane;
         constexpr int HALF = BN / 2;
@@ -963,6 +970,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
     __syncthreads();
     if (tid == 0) trace_mark(trc, 8);
     if (CSK_OK && tp.csk) {
+        pdl_wait();  // every thread stores in the reduction (a no-op once satisfied)
         // cluster split-K: every CTA of the cluster holds its partial of the same tile in shared memory
         // [128 rows][PSTRIDE]; CTA r sums rows [r*128/S, (r+1)*128/S) over the S partials (csk_reduce)
         cluster_sync_all();  // release / acquire at cluster scope: all partials visible

@@ -259,6 +259,8 @@ DwChoice dw_choose(int planes, int BN0, int m_tiles, int Ngemm, int nkb, int nee
     return best;
 }
 
+// SMCONV_HYB_MIN_GFLOP: TMA fwd / dX calls below this much work skip the hybrid form (GenParams::hyb)
+std::atomic<double> g_hyb_min_gflop{getenv("SMCONV_HYB_MIN_GFLOP") ? atof(getenv("SMCONV_HYB_MIN_GFLOP")) : 12.0};
 // SMCONV_STEM=0: keep the stems on DIRECT / GENERIC (A/B experiments)
 const int g_stem = getenv("SMCONV_STEM") ? atoi(getenv("SMCONV_STEM")) : 1;
 const long long g_direct_dw_min_rows =
@@ -688,7 +690,14 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
     pl.ws_bytes = ws_split ? (size_t)splits * out_elems * sizeof(float) : 0;
     g.split_stride = ws_split ? out_elems : 0;
     pl.wx_off = pl.wx_bytes = 0;
-    if (pl.planes == 2 && op != CONV_OP_BWD_FILTER &&
+    // TMA fwd / dX in 3xTF32: the hybrid form (W' plane + one bf16 cross-term MMA) costs a wx_prep launch
+    // per call; below g_hyb_min_gflop of valid-tap work the call runs three TF32 MMAs with b_lo split in
+    // the kernel instead (GenParams::hyb)
+    g.hyb = 1;
+    if (pl.variant == CONV_VARIANT_TMA && pl.planes == 2 && op != CONV_OP_BWD_FILTER &&
+        2.0 * (double)out_elems * est_taps(d) * (op == CONV_OP_FWD ? d.IC : d.OC) < g_hyb_min_gflop.load() * 1e9)
+        g.hyb = 0;
+    if (pl.planes == 2 && op != CONV_OP_BWD_FILTER && g.hyb &&
         (pl.variant == CONV_VARIANT_TMA || pl.variant == CONV_VARIANT_STRIP)) {
         // W' = [bf16(w_lo) | bf16(w)] per (tap, GEMM column, 32-k block): 4 bytes per weight
         pl.wx_off = (pl.ws_bytes + 1023) & ~(size_t)1023;
@@ -1211,6 +1220,13 @@ int smconv_set_trace(void* device_buf) {
     return CONV_OK;
 }
 
+double smconv_set_hybrid_min_gflop(double gflop) {
+    const double old = g_hyb_min_gflop.exchange(gflop);
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    g_plans.clear();  // plans depend on it
+    return old;
+}
+
 int conv2d_force_variant(int op, int variant) {
     if (op < 0 || op > 2 || variant < 0 || variant > 6) return fail(CONV_EARG, "conv2d_force_variant: bad op/variant");
     read_env_once();
@@ -1227,7 +1243,7 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
     rc = make_plan(op, d, math, pl);
     if (rc) return rc;
     if (buf && len)
-        snprintf(buf, len, "variant=%s%s%s BN=%d planes=%d splits=%d grid=%ux%ux%u ws=%zu kernels=%d",
+        snprintf(buf, len, "variant=%s%s%s%s BN=%d planes=%d splits=%d grid=%ux%ux%u ws=%zu kernels=%d",
                  pl.s2dx ? "tma s2dx" :
                  pl.variant == CONV_VARIANT_DWS      ? "dws"
                  : pl.variant == CONV_VARIANT_STEM   ? "stem"
@@ -1238,7 +1254,10 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
                  ((pl.variant == CONV_VARIANT_TMA && pl.tp.pair) ||
                   (pl.variant == CONV_VARIANT_STRIP && strip_pair(op, N, pl.BN, pl.planes)))
                      ? " pair=2cta"
-                     : "", pl.gp.csk ? " csk" : "", pl.BN, pl.planes, pl.splits, pl.grid.x,
+                     : "", pl.gp.csk ? " csk" : "",
+                 (pl.variant == CONV_VARIANT_TMA && pl.planes == 2 && op != CONV_OP_BWD_FILTER && !pl.gp.hyb) ? " 3mma"
+                                                                                                              : "",
+                 pl.BN, pl.planes, pl.splits, pl.grid.x,
                  pl.grid.y, pl.grid.z, pl.ws_bytes, plan_kernel_count(pl));
     return CONV_OK;
 }

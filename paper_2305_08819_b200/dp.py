@@ -265,9 +265,11 @@ class ConvNetStep:
                     ws.data_ptr() if (ws is not None and b.ws_bytes[op]) else 0,
                     b.ws_bytes[op] if ws is not None else 0, stream)
 
-    def step(self, pg=None, events: Optional[list] = None, external_events: bool = False, only=None):
+    def step(self, pg=None, events: Optional[list] = None, external_events: bool = False, only=None,
+             serial: bool = False):
         """Enqueue fwd for all layers, then dX/dW in reverse with bucketed async all-reduce.
-        external_events: timing events that stay valid inside CUDA-graph capture."""
+        external_events: timing events that stay valid inside CUDA-graph capture.  serial: every call on
+        the current stream even with dw_stream (per-call profiling: no kernel overlaps another)."""
         torch = self.torch
         stream = torch.cuda.current_stream(self.device).cuda_stream
         rec = events is not None
@@ -290,7 +292,7 @@ class ConvNetStep:
             # every rank's dW copy is zero before any rank adds into it (smconv_mcast.h contract)
             self.dw_flat.zero_()
             self.mc_handle.barrier()
-        side = self.side
+        side = None if serial else self.side
         if side is not None:
             side.wait_stream(torch.cuda.current_stream(self.device))  # X of every layer, the loss gradients
         for i in reversed(range(len(self.bufs))):

@@ -29,7 +29,7 @@ MCAST_EXPORTS = ("conv2d_bwd_filter_mcast_workspace_bytes", "conv2d_bwd_filter_m
 EPI_EXPORTS = ("conv2d_epi_workspace_bytes", "conv2d_fwd_epi", "conv2d_bwd_data_epi", "conv2d_epi_plan_describe")
 GEMM_EXPORTS = ("gemm_workspace_bytes", "gemm_matmul", "gemm_matmul_t1", "gemm_matmul_t2", "gemm_plan_describe")
 EXT_EXPORTS = ("conv2d_force_variant", "conv2d_plan_describe", "conv2d_plan_kernels", "smconv_selftest_host",
-               "smconv_probe_tf32", "smconv_set_trace")
+               "smconv_probe_tf32", "smconv_set_trace", "smconv_set_hybrid_min_gflop")
 
 
 class ConvError(RuntimeError):
@@ -103,6 +103,8 @@ def lib():
                 L.smconv_set_trace.restype = I
                 L.smconv_probe_tf32.argtypes = [P]
                 L.smconv_probe_tf32.restype = I
+                L.smconv_set_hybrid_min_gflop.argtypes = [ctypes.c_double]
+                L.smconv_set_hybrid_min_gflop.restype = ctypes.c_double
                 _lib = L
     return _lib
 
@@ -147,6 +149,12 @@ def plan_kernels(op, dims, math=CONV_MATH_FP32_3XTF32):
 
 def force_variant(op, variant):
     _check(lib().conv2d_force_variant(op, variant))
+
+
+def set_hybrid_min_gflop(gflop):
+    """TMA fwd / dX calls below `gflop` GFLOP run three TF32 MMAs instead of the hybrid W' form; returns
+    the previous threshold (smconv_ext.h)."""
+    return float(lib().smconv_set_hybrid_min_gflop(float(gflop)))
 
 
 def set_pair(on):

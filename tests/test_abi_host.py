@@ -125,7 +125,7 @@ def test_plans_cover_network_shapes(sm):
                     # [+ zero fill of tap-less dX stride phases]
                     # [+ the bf16 W' prep of 3xTF32 fwd / dX on the TMA and STRIP variants]
                     k = sm.plan_kernels(op, l.dims(128), math)
-                    wx = math == 0 and op != 2 and ("variant=tma" in d or "variant=strip" in d)
+                    wx = math == 0 and op != 2 and ("variant=tma" in d or "variant=strip" in d) and " 3mma" not in d
                     hbm_split = "splits=1 " not in d and " csk" not in d
                     assert k == 1 + hbm_split + (op == 1 and l.sh * l.sw > 1 and
                                                                "variant=tma" in d and l.FH == 1) + wx + \
@@ -284,3 +284,21 @@ def test_mcast_plans(sm):
     stem = (8, 8, 8, 4, 64, 3, 3, 1, 1, 1, 1)
     if "splits=1 " in sm.plan_describe(2, stem, 0):
         assert sm.mcast_workspace_bytes(stem, 0) >= 64 * 9 * 4 * 4
+
+
+def test_hybrid_threshold(sm):
+    """3xTF32 TMA fwd / dX: small calls run three TF32 MMAs (no W' plane, one kernel fewer), large ones
+    the hybrid form; the threshold is settable and the plan cache follows it."""
+    small = (128, 4, 4, 512, 512, 3, 3, 1, 1, 1, 1)   # VGG vgg9 at b128: 6.7 GFLOP
+    big = (4096, 8, 8, 256, 256, 3, 3, 1, 1, 1, 1)    # ResNet l3 at b4096: 309 GFLOP
+    assert " 3mma" in sm.plan_describe(0, small, 0) and " 3mma" in sm.plan_describe(1, small, 0)
+    assert " 3mma" not in sm.plan_describe(0, big, 0)
+    assert " 3mma" not in sm.plan_describe(0, small, 1)  # TF32 mode has no split at all
+    k_small = sm.plan_kernels(0, small, 0)
+    old = sm.set_hybrid_min_gflop(0.0)
+    try:
+        assert " 3mma" not in sm.plan_describe(0, small, 0)
+        assert sm.plan_kernels(0, small, 0) == k_small + 1  # + wx_prep
+    finally:
+        sm.set_hybrid_min_gflop(old)
+    assert " 3mma" in sm.plan_describe(0, small, 0)

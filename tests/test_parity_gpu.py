@@ -273,15 +273,19 @@ SWEEP_TMA = [
 ]
 
 
-@pytest.fixture(params=["single", "pair"])
+@pytest.fixture(params=["single", "pair", "single-3mma", "pair-3mma"])
 def force_tma(env, request):
-    """TMA variant forced; run once with 1-CTA tiles and once with CTA-pair (cta_group::2) tiles
-    (pairs apply to fwd / dX in 3xTF32 when N % 256 == 0, other cases are unchanged)."""
+    """TMA variant forced; run with 1-CTA tiles and with CTA-pair (cta_group::2) tiles (pairs apply to
+    fwd / dX in 3xTF32 when N % 256 == 0, other cases are unchanged), and 3xTF32 fwd / dX once in the
+    hybrid form (W' plane + bf16 cross-term MMA) and once as three TF32 MMAs ("3mma", the small-call
+    default, smconv_set_hybrid_min_gflop)."""
     _, _, sm = env
     for op in (0, 1, 2):
         sm.force_variant(op, sm.CONV_VARIANT_TMA)
-    old = sm.set_pair(request.param == "pair")
+    old = sm.set_pair(request.param.startswith("pair"))
+    old_h = sm.set_hybrid_min_gflop(1e9 if request.param.endswith("3mma") else 0.0)
     yield
+    sm.set_hybrid_min_gflop(old_h)
     sm.set_pair(old)
     for op in (0, 1, 2):
         sm.force_variant(op, sm.CONV_VARIANT_AUTO)
