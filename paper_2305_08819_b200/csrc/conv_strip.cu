@@ -20,6 +20,7 @@ int tma_get_pair();                                                             
 namespace {
 
 const int g_knob_chunk_s = getenv("SMCONV_TMA_CHUNK") ? atoi(getenv("SMCONV_TMA_CHUNK")) : 8;
+const int g_knob_coalesce_s = getenv("SMCONV_COALESCE") ? atoi(getenv("SMCONV_COALESCE")) : 1;
 
 template <int OP, int BN, int PLANES, int R, bool PAIR = false>
 int launch_t(const StripParams& sp, const GenParams& g, cudaStream_t st, char* err, size_t errlen) {
@@ -100,6 +101,7 @@ int strip_launch(int op, int BN, int planes, const GenParams& g, cudaStream_t st
     const uint64_t N = g.N, T = (uint64_t)g.FH * g.FW;
     const uint64_t C = fwd ? g.IC : g.OC;                 // channels of the activation operand
     const uint64_t H = fwd ? g.IH : g.OH, W = fwd ? g.IW : g.OW;
+    sp.coalesce = g_knob_coalesce_s;
     sp.CB = (int)(C / 32);
     sp.NG = g.N / 32;
     sp.OHo = fwd ? g.OH : g.IH;

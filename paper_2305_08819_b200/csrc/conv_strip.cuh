@@ -41,6 +41,7 @@ struct __align__(64) StripParams {
     int col_off;       // first slab column = strip origin + col_off (fwd: -pw, dX: pw - (FW-1))
     int pair;          // work items are pair tiles (two 32-image groups), kernel template PAIR
     FastDiv fd_ntiles, fd_strips, fd_OHo;
+    int coalesce;      // row-coalesced epilogue stores (StripCfg::EPW)
 };
 
 template <int OP, int BN, int PLANES, int R, bool PAIR = false>
@@ -69,7 +70,13 @@ struct StripCfg {
     static constexpr int A_TCOL0 = 2 * R * BN;
     static constexpr int ACC_COLS = 2 * R * BN + (A_TMEM ? NT * A_SLOT_COLS : 0);
     static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128 : ACC_COLS <= 256 ? 256 : 512;
-    static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 1024;
+    static constexpr int SMEM_BASE = 1024 + STAGES * STAGE_BYTES + 1024;
+    // row-coalesced epilogue stores (conv_tma.cuh warp_rows_store): a lane is one image, so a warp's
+    // direct st.global.v4 scatter over 32 rows OH*OW*C*4 bytes apart
+    static constexpr int SMEM_FREE = 232448 - SMEM_BASE;
+    static constexpr int EPW = (BN / 2 >= 32 && SMEM_FREE >= NEPI * 32 * 32 * 4) ? 32
+                             : (BN / 2 >= 16 && SMEM_FREE >= NEPI * 32 * 16 * 4) ? 16 : 0;
+    static constexpr int SMEM_BYTES = SMEM_BASE + NEPI * 32 * EPW * 4;
     static_assert(STAGES >= 2 && NT >= 1, "strip stage does not fit");
     static_assert(!A_TMEM || (R == 1 && NT * FW <= 8), "3xTF32 strips: one window per filter column, per-window barriers");
     static_assert(ACC_COLS <= 512, "TMEM");
@@ -395,6 +402,8 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
         const int qd = warp & 3, half = warp >> 2;
         constexpr int HALF = BN / 2;
         const uint32_t lane_addr = (uint32_t)(qd * 32) << 16;
+        uint8_t* const stg = tiles_ptr + C::STAGES * C::STAGE_BYTES + 1024 + warp * (32 * C::EPW * 4);
+        const bool coal = C::EPW > 0 && sp.coalesce;
         uint32_t c = 0;
         for (int w = wfirst; w < sp.work; w += wstep) {
             StripTile t;
@@ -441,7 +450,37 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
                         mbar_arrive(&aux->tempty[buf]);
                     }
                 }
-                if (p.epi.mode != EPI_NONE) {  // fused epilogue (epilogue.cuh)
+                bool stored = false;
+                if constexpr (C::EPW > 0) {
+                    if (coal) {
+#pragma unroll
+                        for (int j = 0; j < R; ++j)
+#pragma unroll
+                            for (int c0 = 0; c0 < HALF; c0 += C::EPW) {
+                                const int col0 = n0 + half * HALF + c0;
+                                float f[C::EPW];
+#pragma unroll
+                                for (int e = 0; e < C::EPW; ++e) f[e] = acc[j][c0 + e];
+                                if (p.epi.mode != EPI_NONE) {
+#pragma unroll
+                                    for (int q = 0; q < C::EPW; q += 16) {
+                                        float v[16];
+#pragma unroll
+                                        for (int e = 0; e < 16; ++e) v[e] = f[q + e];
+                                        epi_apply16(p.epi, v,
+                                                    obase[j] >= 0 && col0 + q < p.Ngemm ? obase[j] + col0 + q : -1,
+                                                    col0 + q, p.Ngemm, strip_grp<R>(sp, t, j, qd), lane);
+#pragma unroll
+                                        for (int e = 0; e < 16; ++e) f[q + e] = v[e];
+                                    }
+                                }
+                                warp_rows_store<C::EPW>(stg, f, obase[j], outp, col0, p.Ngemm, 0, lane);
+                            }
+                        stored = true;
+                    }
+                }
+                if (stored) {
+                } else if (p.epi.mode != EPI_NONE) {  // fused epilogue (epilogue.cuh)
 #pragma unroll
                     for (int j = 0; j < R; ++j)
 #pragma unroll
@@ -479,6 +518,43 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
                 }
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
+                    if constexpr (C::EPW > 0) {
+                        if (coal) {
+#pragma unroll 1
+                            for (int c0 = 0; c0 < HALF; c0 += C::EPW) {
+                                float f[C::EPW];
+                                if (nch > 0) {
+                                    uint32_t v[C::EPW];
+#pragma unroll
+                                    for (int q = 0; q < C::EPW / 16; ++q)
+                                        tmem_ld_32x32b_x16(tmem + lane_addr + (uint32_t)((buf * R + j) * BN + half * HALF + c0 + 16 * q),
+                                                           *reinterpret_cast<uint32_t(*)[16]>(&v[16 * q]));
+                                    tmem_ld_wait();
+#pragma unroll
+                                    for (int e = 0; e < C::EPW; ++e) f[e] = __uint_as_float(v[e]);
+                                } else {
+#pragma unroll
+                                    for (int e = 0; e < C::EPW; ++e) f[e] = 0.f;
+                                }
+                                const int col0 = n0 + half * HALF + c0;
+                                if (p.epi.mode != EPI_NONE) {
+#pragma unroll
+                                    for (int q = 0; q < C::EPW; q += 16) {
+                                        float v[16];
+#pragma unroll
+                                        for (int e = 0; e < 16; ++e) v[e] = f[q + e];
+                                        epi_apply16(p.epi, v,
+                                                    obase[j] >= 0 && col0 + q < p.Ngemm ? obase[j] + col0 + q : -1,
+                                                    col0 + q, p.Ngemm, strip_grp<R>(sp, t, j, qd), lane);
+#pragma unroll
+                                        for (int e = 0; e < 16; ++e) f[q + e] = v[e];
+                                    }
+                                }
+                                warp_rows_store<C::EPW>(stg, f, obase[j], outp, col0, p.Ngemm, 0, lane);
+                            }
+                            continue;
+                        }
+                    }
 #pragma unroll 1
                     for (int c0 = 0; c0 < HALF; c0 += 16) {
                         uint32_t v[16];

@@ -23,6 +23,8 @@ int env_int(const char* name, int dflt) {
 const int g_knob_G = env_int("SMCONV_TMA_G", 0);
 const int g_knob_promo = env_int("SMCONV_TMA_L2PROMO", 3);
 const int g_knob_chunk = env_int("SMCONV_TMA_CHUNK", 8);
+// SMCONV_COALESCE=0: fwd / dX epilogue stores straight from the TMEM lanes (A/B experiments)
+const int g_knob_coalesce = env_int("SMCONV_COALESCE", 1);
 std::atomic<int> g_pair{env_int("SMCONV_PAIR", 1)};  // CTA pairs (smconv_set_pair); on by default since r01o
 const int g_dw_pair = env_int("SMCONV_DW_PAIR", 1);  // dW pairs (A/B knob; follows g_pair when on)
 
@@ -118,6 +120,19 @@ int launch_bn(int BN, const TmaParams& tp, const GenParams& g, dim3 grid, cudaSt
     }
 }
 
+template <int OP, int PLANES>
+int epw_bn(int BN, int pair) {
+    constexpr bool PAIRABLE = PLANES == 2 && (OP == OP_FWD || OP == OP_DX || OP == OP_DW);
+    if (PAIRABLE && pair) return BN == 64 ? TmaCfg<OP, 64, PLANES, PAIRABLE>::EPW : TmaCfg<OP, 128, PLANES, PAIRABLE>::EPW;
+    switch (BN) {
+        case 32: return TmaCfg<OP, 32, PLANES, false>::EPW;
+        case 64: return TmaCfg<OP, 64, PLANES, false>::EPW;
+        case 128: return TmaCfg<OP, 128, PLANES, false>::EPW;
+        default: return TmaCfg<OP, (PLANES == 2 ? 128 : 256), PLANES, false>::EPW;
+    }
+}
+
+
 template <int OP>
 int launch_op(int BN, int planes, const TmaParams& tp, const GenParams& g, dim3 grid, cudaStream_t st, char* err,
               size_t n) {
@@ -125,6 +140,12 @@ int launch_op(int BN, int planes, const TmaParams& tp, const GenParams& g, dim3 
 }
 
 }  // namespace
+
+int tma_epw(int op, int BN, int planes, int pair) {
+    if (op == CONV_OP_FWD) return planes == 2 ? epw_bn<OP_FWD, 2>(BN, pair) : epw_bn<OP_FWD, 1>(BN, pair);
+    if (op == CONV_OP_BWD_DATA) return planes == 2 ? epw_bn<OP_DX, 2>(BN, pair) : epw_bn<OP_DX, 1>(BN, pair);
+    return 0;
+}
 
 int tma_set_pair(int on) { return g_pair.exchange(on); }
 int tma_get_pair() { return g_pair.load(); }
@@ -168,6 +189,7 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
     tp.G = (g.N % 128 == 0) ? 128 : 32;
     if (g_knob_G == 32) tp.G = 32;
     tp.chunk_kb = g_knob_chunk > 0 ? g_knob_chunk : 8;
+    tp.coalesce = g_knob_coalesce;
     if (planes == 2 && BN > 128) {
         snprintf(err, errlen, "tma plan: BN %d > 128 in 3xTF32", BN);
         return CONV_EUNSUPPORTED;

@@ -69,6 +69,11 @@ struct __align__(64) TmaParams {
                     // block (the TMA zero-fills ic >= IC) instead of one 4-D box of BNC / 32 blocks
     int dw_a_ragged;  // dW with OC % 32 != 0: A = dY viewed (OC, N, P), 4 boxes (32 oc, 32 n, 1) per k-block
     int dw_b_ragged;  // dW with IC % 32 != 0: B = X viewed (IC, N, IW, IH), boxes (32 ic, 32 n, 1, 1)
+    int coalesce;     // fwd / dX: row-coalesced epilogue stores through the per-warp staging (TmaCfg::EPW)
+    // dX of a 1x1 stride-2 conv (only phase (0, 0) has a tap): the epilogue also writes the zeros of
+    // pixels (2a, 2b+1), (2a+1, 2b), (2a+1, 2b+1) next to each row (2a, 2b) -- element offsets zf1
+    // (one pixel) and zf2 (one dX row) -- instead of a separate zero_phases_kernel pass (0: off)
+    long long zf1, zf2;
 };
 
 template <int OP, int BN, int PLANES, bool PAIR = false>
@@ -106,7 +111,19 @@ struct TmaCfg {
     static constexpr int ACC_COLS = 2 * BN + (A_TMEM ? NT * 64 : 0);
     static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128 : ACC_COLS <= 256 ? 256 : 512;
     static constexpr int AUX_BYTES = 1024 + kMaxTaps * 16;
-    static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + AUX_BYTES;
+    static constexpr int SMEM_BASE = 1024 + STAGES * STAGE_BYTES + AUX_BYTES;
+    // Row-coalesced epilogue (fwd / dX).  A TMEM lane is a GEMM row = one output pixel of one image, so a
+    // warp's st.global.v4 of 32 lanes scatters 16 B to each of 32 rows (OH*OW*C*4 bytes apart under the
+    // position-major walk): 32 L2 requests per instruction.  The 1x1 shortcut fwd (K = 2 k-blocks) was
+    // bound by it (ncu r02bb: stall_long_sb on the registers of outstanding STGs, 2.5 TB/s).  Each
+    // epilogue warp stages 32 rows x EPW columns in shared memory (XOR-swizzled 16-B units: both the
+    // row-wise writes and the column-wise reads are bank-conflict free) and stores EPW*4-byte row runs.
+    static constexpr int SMEM_FREE = 232448 - SMEM_BASE;  // 227 KB opt-in maximum per CTA
+    static constexpr int EPW = IS_DW ? 0
+                             : (BN / 2 >= 32 && SMEM_FREE >= NEPI * 32 * 32 * 4) ? 32
+                             : (BN / 2 >= 16 && SMEM_FREE >= NEPI * 32 * 16 * 4) ? 16 : 0;
+    static constexpr int STG_BYTES = NEPI * 32 * EPW * 4;
+    static constexpr int SMEM_BYTES = SMEM_BASE + STG_BYTES;
     // cluster split-K partial [128 rows][BN + 4] fp32 in the (drained) stage ring; +4 floats per row
     // keep a quarter-warp's 16-B row stores on distinct banks
     static constexpr int PSTRIDE = BN + 4;
@@ -368,6 +385,42 @@ SMCONV_DEV void csk_reduce(const TmaParams& tp, const GenParams& p, uint32_t til
                 a.w += v[u][q].w;
             }
             *reinterpret_cast<float4*>(p.out + o) = a;
+        }
+    }
+}
+
+// Row-coalesced store of one epilogue warp's 32 rows x PW columns (TmaCfg::EPW): lane l holds columns
+// [col0, col0 + PW) of row l in f; row r goes to out + ob(lane r) + shift + col (ob < 0: row dropped).
+// Staged in the warp's slice of shared memory as 16-B units, unit j of row r at slot j ^ swz(r): the
+// row-wise writes (8 lanes = 8 rows per phase) and the run-wise reads (8 lanes = 8 units of 1-2 rows)
+// both hit 8 distinct 16-B bank groups.  One STG then covers 32 / (PW / 4) rows of PW * 4 bytes.
+template <int PW>
+SMCONV_DEV void warp_rows_store(uint8_t* stg, const float (&f)[PW], long long ob, float* out, int col0, int ncols,
+                                long long shift, int lane, long long zf1 = 0, long long zf2 = 0) {
+    constexpr int F4 = PW / 4, RPI = 32 / F4;
+    static_assert(F4 == 4 || F4 == 8, "piece of 16 or 32 columns");
+    auto swz = [](int r) { return F4 == 8 ? (r & 7) : ((r >> 1) & 3); };
+    __syncwarp();  // the previous piece's reads are done
+#pragma unroll
+    for (int j = 0; j < F4; ++j)
+        *reinterpret_cast<float4*>(stg + (lane * F4 + (j ^ swz(lane))) * 16) =
+            make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+    __syncwarp();
+    const int j = lane % F4, col = col0 + 4 * j;
+#pragma unroll
+    for (int i = 0; i < F4; ++i) {
+        const int r = lane / F4 + RPI * i;
+        const long long o = __shfl_sync(0xffffffffu, ob, r);
+        const float4 x = *reinterpret_cast<const float4*>(stg + (r * F4 + (j ^ swz(r))) * 16);
+        if (o >= 0 && col < ncols) {
+            float* const d = out + o + shift + col;
+            *reinterpret_cast<float4*>(d) = x;
+            if (zf1) {  // TmaParams::zf1 / zf2: the empty stride phases around this pixel
+                const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                *reinterpret_cast<float4*>(d + zf1) = z;
+                *reinterpret_cast<float4*>(d + zf2) = z;
+                *reinterpret_cast<float4*>(d + zf2 + zf1) = z;
+            }
         }
     }
 }
@@ -790,6 +843,8 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
         const int row = qd * 32 + lane;
         constexpr int HALF = BN / 2;
         const uint32_t lane_addr = (uint32_t)(qd * 32) << 16;
+        uint8_t* const stg = tiles_ptr + C::STAGES * C::STAGE_BYTES + C::AUX_BYTES + warp * (32 * C::EPW * 4);
+        const bool coal = C::EPW > 0 && tp.coalesce && !(CSK_OK && tp.csk);
         uint32_t c = 0;
         for (int w = wfirst; w < tp.work; w += wstep) {
             TileInfo<OP> ti;
@@ -826,6 +881,10 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             // fused epilogue (epilogue.cuh): 32-row group of this warp for the statistics partial rows
             // (dX: rows of phase k start at phase_tile0[k] tiles of 128 rows, or of 256 for pair tiles)
             const int egrp = (((OP == OP_DX ? p.phase_tile0[ti.phase] : 0) << (tp.pair ? 8 : 7)) + ti.m0 >> 5) + qd;
+            // row-coalesced stores (TmaCfg::EPW): s2dx columns (pi = 1, pj, ic) land one dX row further
+            auto s2shift = [&](int col0) -> long long {
+                return (OP == OP_FWD && p.s2dx && col0 >= 2 * p.s2_IC) ? (long long)(p.s2_IW - 2) * p.s2_IC : 0;
+            };
             // 4 consecutive GEMM columns of this thread's row -> output
             auto st4 = [&](int col, float x, float y, float z, float w4) {
                 if (CSK_OK && tp.csk) {  // cluster split-K: this CTA's partial -> own shared memory
@@ -888,7 +947,34 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                         mbar_arrive(&aux->tempty[buf]);
                     }
                 }
-                if (!C::IS_DW && p.epi.mode != EPI_NONE) {
+                bool stored = false;
+                if constexpr (C::EPW > 0) {
+                    if (coal) {
+#pragma unroll
+                        for (int c0 = 0; c0 < HALF; c0 += C::EPW) {
+                            const int col0 = n0 + half * HALF + c0;
+                            float f[C::EPW];
+#pragma unroll
+                            for (int e = 0; e < C::EPW; ++e) f[e] = acc[c0 + e];
+                            if (p.epi.mode != EPI_NONE) {
+#pragma unroll
+                                for (int q = 0; q < C::EPW; q += 16) {
+                                    float v[16];
+#pragma unroll
+                                    for (int e = 0; e < 16; ++e) v[e] = f[q + e];
+                                    epi_apply16(p.epi, v, obase >= 0 && col0 + q < p.Ngemm ? out_off(col0 + q) : -1,
+                                                col0 + q, p.Ngemm, egrp, lane);
+#pragma unroll
+                                    for (int e = 0; e < 16; ++e) f[q + e] = v[e];
+                                }
+                            }
+                            warp_rows_store<C::EPW>(stg, f, obase, outp, col0, p.Ngemm, s2shift(col0), lane, tp.zf1, tp.zf2);
+                        }
+                        stored = true;
+                    }
+                }
+                if (stored) {
+                } else if (!C::IS_DW && p.epi.mode != EPI_NONE) {
 #pragma unroll
                     for (int c0 = 0; c0 < HALF; c0 += 16) {
                         const int col0 = n0 + half * HALF + c0;
@@ -929,9 +1015,39 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                             tmem_ld_32x32b_x16(tmem + lane_addr + (uint32_t)(buf * BN + half * HALF + c0 + 16 * q),
                                                *reinterpret_cast<uint32_t(*)[16]>(&v[16 * q]));
                         tmem_ld_wait();
+                        if (c0 + CH >= HALF) {  // last TMEM read of this tile: release the buffer before the stores
+                            tc_fence_before();
+                            mbar_arrive(&aux->tempty[buf]);
+                        }
                     } else {
 #pragma unroll
                         for (int e = 0; e < CH; ++e) v[e] = 0u;
+                    }
+                    if constexpr (C::EPW > 0) {
+                        if (coal) {
+#pragma unroll
+                            for (int q = 0; q < CH / 16; ++q) {
+                                const int col0 = n0 + half * HALF + c0 + 16 * q;
+                                if (p.epi.mode != EPI_NONE) {
+                                    float f[16];
+#pragma unroll
+                                    for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[16 * q + e]);
+                                    epi_apply16(p.epi, f, obase >= 0 && col0 < p.Ngemm ? out_off(col0) : -1, col0,
+                                                p.Ngemm, egrp, lane);
+#pragma unroll
+                                    for (int e = 0; e < 16; ++e) v[16 * q + e] = __float_as_uint(f[e]);
+                                }
+                            }
+#pragma unroll
+                            for (int p0 = 0; p0 < CH; p0 += C::EPW) {
+                                float f[C::EPW];
+#pragma unroll
+                                for (int e = 0; e < C::EPW; ++e) f[e] = __uint_as_float(v[p0 + e]);
+                                const int col0 = n0 + half * HALF + c0 + p0;
+                                warp_rows_store<C::EPW>(stg, f, obase, outp, col0, p.Ngemm, s2shift(col0), lane, tp.zf1, tp.zf2);
+                            }
+                            continue;
+                        }
                     }
 #pragma unroll
                     for (int q = 0; q < CH / 16; ++q) {
@@ -956,11 +1072,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                         }
                     }
                 }
-                if (nch > 0) {
-                    tc_fence_before();
-                    mbar_arrive(&aux->tempty[buf]);
-                    ++c;
-                }
+                if (nch > 0) ++c;
             }
         }
     }
@@ -995,6 +1107,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
 
 // ------------------------------------------------------------------ host side
 bool tma_supported(int op, int N, int IC, int OC, int FH, int FW, int sh, int sw);
+int tma_epw(int op, int BN, int planes, int pair);  // TmaCfg::EPW of the kernel tma_launch would pick
 int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3& grid, char* err, size_t errlen);
 int tma_launch(int op, int BN, int planes, const GenParams& g, TmaParams& tp, dim3 grid, cudaStream_t st, char* err,
                size_t errlen);

@@ -187,6 +187,8 @@ constexpr int kMaxKbPerChain = 256;
 constexpr int kGenMaxKbPerChain3x = 16;  // GENERIC 3xTF32 (no chunked promotion)
 // largest cluster split-K (TMA fwd / dX on small maps); SMCONV_CSK=0 turns it off (A/B experiments)
 const int g_csk_max = getenv("SMCONV_CSK") ? atoi(getenv("SMCONV_CSK")) : 8;
+// SMCONV_ZFILL=0: keep zero_phases_kernel for the 1x1 stride-2 dX (A/B experiments)
+const int g_zfill = getenv("SMCONV_ZFILL") ? atoi(getenv("SMCONV_ZFILL")) : 1;
 constexpr int kSMs = 148;
 
 void fill_common(GenParams& g, const Dims& d) {
@@ -709,6 +711,15 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
     if (pl.variant == CONV_VARIANT_TMA) {
         int rc = tma_make_plan(op, g, pl.BN, pl.planes, pl.tp, pl.grid, g_detail, sizeof g_detail);
         if (rc) return rc;
+        // 1x1 stride-2 dX (ResNet shortcuts): only phase (0, 0) has a tap; the row-coalesced epilogue
+        // writes the three empty phases' zeros beside each of its rows (one pass over dX instead of the
+        // conv + a zero_phases_kernel pass that ran at ~3.5 TB/s, ncu r02bb)
+        if (op == CONV_OP_BWD_DATA && g_zfill && pl.zero_mask == 0xEu && d.sh == 2 && d.sw == 2 && d.IH % 2 == 0 &&
+            d.IW % 2 == 0 && splits == 1 && !g.csk && pl.tp.coalesce && tma_epw(op, pl.BN, pl.planes, pl.tp.pair) > 0) {
+            pl.tp.zf1 = d.IC;
+            pl.tp.zf2 = (long long)d.IW * d.IC;
+            pl.zero_mask = 0;
+        }
     }
     return CONV_OK;
 }
@@ -1243,7 +1254,7 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
     rc = make_plan(op, d, math, pl);
     if (rc) return rc;
     if (buf && len)
-        snprintf(buf, len, "variant=%s%s%s%s BN=%d planes=%d splits=%d grid=%ux%ux%u ws=%zu kernels=%d",
+        snprintf(buf, len, "variant=%s%s%s%s%s BN=%d planes=%d splits=%d grid=%ux%ux%u ws=%zu kernels=%d",
                  pl.s2dx ? "tma s2dx" :
                  pl.variant == CONV_VARIANT_DWS      ? "dws"
                  : pl.variant == CONV_VARIANT_STEM   ? "stem"
@@ -1257,6 +1268,7 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
                      : "", pl.gp.csk ? " csk" : "",
                  (pl.variant == CONV_VARIANT_TMA && pl.planes == 2 && op != CONV_OP_BWD_FILTER && !pl.gp.hyb) ? " 3mma"
                                                                                                               : "",
+                 (pl.variant == CONV_VARIANT_TMA && pl.tp.zf1) ? " zfill" : "",
                  pl.BN, pl.planes, pl.splits, pl.grid.x,
                  pl.grid.y, pl.grid.z, pl.ws_bytes, plan_kernel_count(pl));
     return CONV_OK;

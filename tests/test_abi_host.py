@@ -122,13 +122,14 @@ def test_plans_cover_network_shapes(sm):
                     d = sm.plan_describe(op, l.dims(128), math)
                     assert "variant=" in d
                     # main kernel [+ split-K reduce, unless the split is reduced in-cluster (csk)]
-                    # [+ zero fill of tap-less dX stride phases]
+                    # [+ zero fill of tap-less dX stride phases, unless the epilogue writes them (zfill)]
                     # [+ the bf16 W' prep of 3xTF32 fwd / dX on the TMA and STRIP variants]
                     k = sm.plan_kernels(op, l.dims(128), math)
                     wx = math == 0 and op != 2 and ("variant=tma" in d or "variant=strip" in d) and " 3mma" not in d
                     hbm_split = "splits=1 " not in d and " csk" not in d
                     assert k == 1 + hbm_split + (op == 1 and l.sh * l.sw > 1 and
-                                                               "variant=tma" in d and l.FH == 1) + wx + \
+                                                               "variant=tma" in d and l.FH == 1 and
+                                                               " zfill" not in d) + wx + \
                         ("s2dx" in d), (l.name, op, d)
 
 
