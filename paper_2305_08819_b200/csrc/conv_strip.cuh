@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
         constexpr int HALF = BN / 2;
         const uint32_t lane_addr = (uint32_t)(qd * 32) << 16;
         uint8_t* const stg = tiles_ptr + C::STAGES * C::STAGE_BYTES + 1024 + warp * (32 * C::EPW * 4);
-        const bool coal = C::EPW > 0 && sp.coalesce;
+        const bool coal = C::EPW > 0 && (sp.coalesce || p.epi.mode != EPI_NONE);  // as conv_tma.cuh
         uint32_t c = 0;
         for (int w = wfirst; w < sp.work; w += wstep) {
             StripTile t;
@@ -458,29 +458,21 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
 #pragma unroll
                             for (int c0 = 0; c0 < HALF; c0 += C::EPW) {
                                 const int col0 = n0 + half * HALF + c0;
-                                float f[C::EPW];
+                                if (p.epi.mode != EPI_NONE) {  // in place on acc, 16 columns at a time
 #pragma unroll
-                                for (int e = 0; e < C::EPW; ++e) f[e] = acc[j][c0 + e];
-                                if (p.epi.mode != EPI_NONE) {
-#pragma unroll
-                                    for (int q = 0; q < C::EPW; q += 16) {
-                                        float v[16];
-#pragma unroll
-                                        for (int e = 0; e < 16; ++e) v[e] = f[q + e];
-                                        epi_apply16(p.epi, v,
+                                    for (int q = 0; q < C::EPW; q += 16)
+                                        epi_apply16(p.epi, *reinterpret_cast<float(*)[16]>(&acc[j][c0 + q]),
                                                     obase[j] >= 0 && col0 + q < p.Ngemm ? obase[j] + col0 + q : -1,
                                                     col0 + q, p.Ngemm, strip_grp<R>(sp, t, j, qd), lane);
-#pragma unroll
-                                        for (int e = 0; e < 16; ++e) f[q + e] = v[e];
-                                    }
                                 }
-                                warp_rows_store<C::EPW>(stg, f, obase[j], outp, col0, p.Ngemm, 0, lane);
+                                warp_rows_store<C::EPW>(stg, *reinterpret_cast<const float(*)[C::EPW]>(&acc[j][c0]), obase[j],
+                                                        outp, col0, p.Ngemm, 0, lane);
                             }
                         stored = true;
                     }
                 }
                 if (stored) {
-                } else if (p.epi.mode != EPI_NONE) {  // fused epilogue (epilogue.cuh)
+                } else if (C::EPW == 0 && p.epi.mode != EPI_NONE) {  // fused epilogue (epilogue.cuh)
 #pragma unroll
                     for (int j = 0; j < R; ++j)
 #pragma unroll
@@ -565,7 +557,7 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
 #pragma unroll
                             for (int e = 0; e < 16; ++e) v[e] = 0u;
                         }
-                        if (p.epi.mode != EPI_NONE) {  // fused epilogue (epilogue.cuh)
+                        if (C::EPW == 0 && p.epi.mode != EPI_NONE) {  // fused epilogue (epilogue.cuh)
                             const int col0 = n0 + half * HALF + c0;
                             float f[16];
 #pragma unroll

@@ -844,7 +844,9 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
         constexpr int HALF = BN / 2;
         const uint32_t lane_addr = (uint32_t)(qd * 32) << 16;
         uint8_t* const stg = tiles_ptr + C::STAGES * C::STAGE_BYTES + C::AUX_BYTES + warp * (32 * C::EPW * 4);
-        const bool coal = C::EPW > 0 && tp.coalesce && !(CSK_OK && tp.csk);
+        // the fused epilogue (p.epi) always takes the coalesced path when the kernel has one, so its
+        // inlined transform / statistics code exists once per column loop (code size: see epilogue.cuh)
+        const bool coal = C::EPW > 0 && (tp.coalesce || p.epi.mode != EPI_NONE) && !(CSK_OK && tp.csk);
         uint32_t c = 0;
         for (int w = wfirst; w < tp.work; w += wstep) {
             TileInfo<OP> ti;
@@ -951,30 +953,25 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                 if constexpr (C::EPW > 0) {
                     if (coal) {
 #pragma unroll
+                        if (p.epi.mode != EPI_NONE) {  // in place on acc, 16 columns at a time
+#pragma unroll
+                            for (int c0 = 0; c0 < HALF; c0 += 16) {
+                                const int col0 = n0 + half * HALF + c0;
+                                epi_apply16(p.epi, *reinterpret_cast<float(*)[16]>(&acc[c0]),
+                                            obase >= 0 && col0 < p.Ngemm ? out_off(col0) : -1, col0, p.Ngemm, egrp, lane);
+                            }
+                        }
+#pragma unroll
                         for (int c0 = 0; c0 < HALF; c0 += C::EPW) {
                             const int col0 = n0 + half * HALF + c0;
-                            float f[C::EPW];
-#pragma unroll
-                            for (int e = 0; e < C::EPW; ++e) f[e] = acc[c0 + e];
-                            if (p.epi.mode != EPI_NONE) {
-#pragma unroll
-                                for (int q = 0; q < C::EPW; q += 16) {
-                                    float v[16];
-#pragma unroll
-                                    for (int e = 0; e < 16; ++e) v[e] = f[q + e];
-                                    epi_apply16(p.epi, v, obase >= 0 && col0 + q < p.Ngemm ? out_off(col0 + q) : -1,
-                                                col0 + q, p.Ngemm, egrp, lane);
-#pragma unroll
-                                    for (int e = 0; e < 16; ++e) f[q + e] = v[e];
-                                }
-                            }
-                            warp_rows_store<C::EPW>(stg, f, obase, outp, col0, p.Ngemm, s2shift(col0), lane, tp.zf1, tp.zf2);
+                            warp_rows_store<C::EPW>(stg, *reinterpret_cast<const float(*)[C::EPW]>(&acc[c0]), obase, outp,
+                                                    col0, p.Ngemm, s2shift(col0), lane, tp.zf1, tp.zf2);
                         }
                         stored = true;
                     }
                 }
                 if (stored) {
-                } else if (!C::IS_DW && p.epi.mode != EPI_NONE) {
+                } else if (C::EPW == 0 && !C::IS_DW && p.epi.mode != EPI_NONE) {
 #pragma unroll
                     for (int c0 = 0; c0 < HALF; c0 += 16) {
                         const int col0 = n0 + half * HALF + c0;
@@ -1052,7 +1049,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
 #pragma unroll
                     for (int q = 0; q < CH / 16; ++q) {
                         const int col0 = n0 + half * HALF + c0 + 16 * q;
-                        if (!C::IS_DW && p.epi.mode != EPI_NONE) {
+                        if (C::EPW == 0 && !C::IS_DW && p.epi.mode != EPI_NONE) {
                             float f[16];
 #pragma unroll
                             for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[16 * q + e]);

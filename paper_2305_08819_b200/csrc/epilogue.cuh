@@ -64,6 +64,11 @@ struct EpiArgs {
 // Transforms v in place (LEAKY: y -> leaky(y); LEAKY_BWD*: dx -> dx * slope(A[addr])) and, in the
 // stats modes, writes the 16 column sums of the warp's 32 rows to partial row `grp`.
 // `ncols_valid` bounds the columns (a ragged last n-tile).
+// Inlined (an out-of-line call passes v through local memory: 576 threads x ~300-B stack frames do not
+// fit L1, and the fused ResNet step went 53.7 -> 78 ms, r02bf).  Code size: the kernels keep ONE
+// unrolled column loop that calls it (the row-coalesced store path; conv_tma.cuh), since every inlined
+// copy is ~1.3k SASS instructions and a cold instruction cache stalls the short small-map calls
+// (ncu r02be, VGG conv11: stall_no_inst 39 % of the samples).
 SMCONV_DEV void epi_apply16(const EpiArgs& e, float (&v)[16], long long addr, int col0, int ncols_valid, int grp,
                             int lane) {
     const bool row_ok = addr >= 0;
