@@ -297,6 +297,14 @@ SMCONV_DEV void cluster_arrive_wait() {  // same as cluster_sync_all, for one ro
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// arrival without release semantics: `.release` compiles to MEMBAR.ALL.GPU + ERRBAR, i.e. the
+// arriving thread first waits for ALL of its outstanding global stores (3-4 % of the stall samples of
+// the small-map csk kernels, ncu r02bg); enough where the barrier only keeps a CTA alive while its
+// peers still read its shared memory (the reads completed before the arrival: their values were used)
+SMCONV_DEV void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
 SMCONV_DEV void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }

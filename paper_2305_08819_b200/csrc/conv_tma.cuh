@@ -1091,7 +1091,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             default: csk_reduce<OP, BN, C::PSTRIDE, 16>(tp, p, tiles_addr, (int)csk_rank, tid, C::NTHREADS); break;
         }
         if (tid == 0) trace_mark(trc, 10);
-        cluster_sync_all();  // no CTA exits while a peer still reads its shared memory
+        cluster_sync_relaxed();  // no CTA exits while a peer still reads its shared memory
     }
     if (PAIR) cluster_sync_all();  // the peer's MMAs / arrivals are done before TMEM is released
     if (warp == C::MMA_W) {
