@@ -24,6 +24,13 @@
 // chunk_kb k-blocks into fp32 registers, the truncating TMEM accumulation is bounded as in
 // conv_tma.cuh).  Partials per split go to the workspace; splitk_reduce_kernel sums them in
 // fixed order (deterministic).
+//
+// 3xTF32 (HYB, the default): per m-tile and k-block a_hi*b_hi as 4 TF32 MMAs and the cross terms
+// a_hi*b_lo + a_lo*b as 4 bf16 MMAs (K' = 64) on A' = [bf16(a_hi) | bf16(a_lo)] (TMEM, written by
+// the converters next to a_hi) and B' = [bf16(b_lo) | bf16(b)] (a bf16 MN-major plane the
+// converters build from the dY tile in place of the old b_lo plane; common.cuh "3xTF32 operand
+// split"): 8 MMAs of tensor-pipe time per m-tile and k-block instead of 12.  HYB = false keeps
+// the three-TF32-MMA form (SMCONV_DWS_HYB=0, A/B and fallback).
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -56,6 +63,9 @@ constexpr int kDwsTaps = 9;
 
 template <int PLANES, int OW>
 struct DwsCfg {
+    // B' plane of the bf16 cross terms: [K' = 64][64 oc] bf16, MN-major SWIZZLE_128B (8-row x 128-B
+    // atoms, SBO 1024), the same 8 KB as the fp32 b_lo plane it replaces
+    static constexpr int YX_BYTES = 64 * 64 * 2;
     static constexpr int RB = 32 / OW, XW = OW + 2;  // k-block rows; slab columns
     static constexpr int BN = 64;                    // OC
     static constexpr int Y_BYTES = BN * 32 * 4;      // dY k-block [2 ocb][32 px][32 oc]
@@ -100,7 +110,12 @@ struct DwsItem {
     }
 };
 
-template <int PLANES, int OW>
+// byte offset of bf16 elements (k, mn..mn+3), mn % 4 == 0, in a [K][64] MN-major SWIZZLE_128B tile
+SMCONV_DEV uint32_t mnmaj16_off(uint32_t k, uint32_t mn) {
+    return (k >> 3) * 1024u + (k & 7u) * 128u + ((((mn >> 3) & 7u) ^ (k & 7u)) << 4) + (mn & 7u) * 2u;
+}
+
+template <int PLANES, int OW, bool HYB>
 __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
     conv_dws_kernel(const __grid_constant__ DwsParams dp, const __grid_constant__ GenParams p) {
     using C = DwsCfg<PLANES, OW>;
@@ -174,7 +189,9 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
     } else if (warp == C::MMA_W) {
         // ======================= MMA issuer: ntile m-tiles x 4 k-steps (x3 for 3xTF32) per k-block
         constexpr uint32_t IDESC = idesc_tf32(128, C::BN, false, true);  // A from TMEM, B (dY) MN-major
+        constexpr uint32_t IDESC_X = idesc_bf16(128, C::BN, false, true);
         const uint64_t bd0 = make_sdesc(tiles_addr, 4096u, 512u, kLayoutSW128Base32);
+        const uint64_t bx0 = make_sdesc(tiles_addr + C::Y_OFF_LO, 8192u, 1024u, kLayoutSW128);  // B' plane
         constexpr uint64_t B_LO = C::Y_BYTES >> 4;
         uint32_t q = 0, c = 0;
         int in_chunk = 0;
@@ -204,12 +221,22 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
                                 const uint64_t bdH = bd0 + so + g4 * 64;  // 8 K-rows x 128 B
                                 const uint32_t acc0 = (in_chunk > 0 || g4 > 0) ? 1u : 0u;
                                 const uint32_t ahi = tmem + (uint32_t)(C::ACC_COLS + t * C::SLOT_COLS + j * C::TILE_COLS + g4 * 8);
-                                if (PLANES == 2) {
+                                if (PLANES == 2 && HYB) {
+                                    mma_tf32_ts(d, ahi, bdH, IDESC, acc0);  // a_hi * b_hi
+                                } else if (PLANES == 2) {
                                     mma_tf32_ts(d, ahi + 32, bdH, IDESC, acc0);  // a_lo * b_hi
                                     mma_tf32_ts(d, ahi, bdH + B_LO, IDESC, 1u);  // a_hi * b_lo
                                     mma_tf32_ts(d, ahi, bdH, IDESC, 1u);         // a_hi * b_hi
                                 } else {
                                     mma_tf32_ts(d, ahi, bdH, IDESC, acc0);
+                                }
+                            }
+                            if (PLANES == 2 && HYB) {
+                                // cross terms: A' columns [32, 64) of the m-tile's slot, B' rows 16 j..16 j+15
+#pragma unroll
+                                for (int j4 = 0; j4 < 4; ++j4) {
+                                    const uint32_t ax = tmem + (uint32_t)(C::ACC_COLS + t * C::SLOT_COLS + j * C::TILE_COLS + 32 + j4 * 8);
+                                    mma_bf16_ts(d, ax, bx0 + so + j4 * (2048 >> 4), IDESC_X, 1u);
                                 }
                             }
                         }
@@ -264,7 +291,24 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
 #pragma unroll
                     for (int e = 0; e < NB; ++e) v[e] = bH[ct + e * C::NCONV * 32];
 #pragma unroll
-                    for (int e = 0; e < NB; ++e) {
+                    for (int e = 0; e < NB && HYB; ++e) {
+                        // float4 i of the fp32 MN-major tile: oc block i / 256, K-row (i % 256) / 8,
+                        // 32-B chunk (i % 8) / 2 (swizzled with k % 4), 16-B half i % 2
+                        const uint32_t i = (uint32_t)(ct + e * C::NCONV * 32);
+                        const uint32_t k = (i & 255u) >> 3, c32 = (i & 7u) >> 1;
+                        const uint32_t mn = (i >> 8) * 32u + ((c32 ^ (k & 3u)) << 3) + ((i & 1u) << 2);
+                        const float4 b = v[e];
+                        const float l0 = b.x - __uint_as_float(__float_as_uint(b.x) & 0xFFFFE000u);
+                        const float l1 = b.y - __uint_as_float(__float_as_uint(b.y) & 0xFFFFE000u);
+                        const float l2 = b.z - __uint_as_float(__float_as_uint(b.z) & 0xFFFFE000u);
+                        const float l3 = b.w - __uint_as_float(__float_as_uint(b.w) & 0xFFFFE000u);
+                        *reinterpret_cast<uint2*>(st + C::Y_OFF_LO + mnmaj16_off(k, mn)) =
+                            make_uint2(pack_bf16x2(l0, l1), pack_bf16x2(l2, l3));
+                        *reinterpret_cast<uint2*>(st + C::Y_OFF_LO + mnmaj16_off(k + 32u, mn)) =
+                            make_uint2(pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+                    }
+#pragma unroll
+                    for (int e = 0; e < NB && !HYB; ++e) {
                         float4 o;
                         o.x = v[e].x - __uint_as_float(__float_as_uint(v[e].x) & 0xFFFFE000u);
                         o.y = v[e].y - __uint_as_float(__float_as_uint(v[e].y) & 0xFFFFE000u);
@@ -283,6 +327,7 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
                 for (int j = 0; j < 2; ++j) {
                     if (j < it.ntile) {
                         uint32_t hi[16], lo[16];
+                        float ev[16];
                         if (bsr[j] >= 0) {
                             const uint8_t* p0 = (bsr[j] == 0 ? row0 : row1 + (bsr[j] - 1) * C::ROW_BYTES) + coff[j];
                             const uint8_t* p1 = row1 + bsr[j] * C::ROW_BYTES + coff[j];  // rows after the first
@@ -292,6 +337,7 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
                                                     ? *reinterpret_cast<const float*>(p0 + (k % OW) * 256)
                                                     : *reinterpret_cast<const float*>(
                                                           p1 + (k / OW - 1) * C::ROW_BYTES + (k % OW) * 256);
+                                ev[k] = e;
                                 if (PLANES == 2) {
                                     const uint32_t hb = __float_as_uint(e) & 0xFFFFE000u;
                                     hi[k] = hb;
@@ -303,12 +349,25 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
                             }
                         } else {
 #pragma unroll
-                            for (int k = 0; k < 16; ++k) hi[k] = lo[k] = 0u;  // half-empty last m-tile
+                            for (int k = 0; k < 16; ++k) {  // half-empty last m-tile
+                                hi[k] = lo[k] = 0u;
+                                ev[k] = 0.f;
+                            }
                         }
                         const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) +
                                             (uint32_t)(C::ACC_COLS + t * C::SLOT_COLS + j * C::TILE_COLS + h * 16);
-                        tmem_st_32x32b_x16(ta, hi);
-                        if (PLANES == 2) tmem_st_32x32b_x16(ta + 32, lo);
+                        if (PLANES == 2 && HYB) {
+                            // slot columns [0,32) a_hi, [32,48) bf16(a_hi) pairs, [48,64) bf16(a_lo) pairs
+                            uint32_t xh[8], xl[8];
+                            split_a16(ev, hi, xh, xl);
+                            const uint32_t tb = ta - (uint32_t)(h * 16);
+                            tmem_st_32x32b_x16(ta, hi);
+                            tmem_st_32x32b_x8(tb + 32 + h * 8, xh);
+                            tmem_st_32x32b_x8(tb + 48 + h * 8, xl);
+                        } else {
+                            tmem_st_32x32b_x16(ta, hi);
+                            if (PLANES == 2) tmem_st_32x32b_x16(ta + 32, lo);
+                        }
                         tmem_st_wait();
                     }
                     if (j == 0) fence_proxy_async_smem();  // b_lo (written above) before the first release
@@ -383,7 +442,9 @@ namespace {
 
 const int g_knob_chunk_d = getenv("SMCONV_TMA_CHUNK") ? atoi(getenv("SMCONV_TMA_CHUNK")) : 8;
 
-template <int PLANES, int OW>
+const int g_dws_hyb = getenv("SMCONV_DWS_HYB") ? atoi(getenv("SMCONV_DWS_HYB")) : 0;
+
+template <int PLANES, int OW, bool HYB>
 int launch_t(const DwsParams& dp, const GenParams& g, cudaStream_t st, char* err, size_t errlen) {
     using C = DwsCfg<PLANES, OW>;
     static std::atomic<unsigned long long> attr_done{0};
@@ -391,7 +452,7 @@ int launch_t(const DwsParams& dp, const GenParams& g, cudaStream_t st, char* err
     cudaGetDevice(&dev);
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(attr_done.load() & bit)) {
-        if (cudaFuncSetAttribute(conv_dws_kernel<PLANES, OW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(conv_dws_kernel<PLANES, OW, HYB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::SMEM_BYTES) != cudaSuccess) {
             snprintf(err, errlen, "cudaFuncSetAttribute(dws smem=%d): %s", C::SMEM_BYTES,
                      cudaGetErrorString(cudaGetLastError()));
@@ -400,7 +461,8 @@ int launch_t(const DwsParams& dp, const GenParams& g, cudaStream_t st, char* err
         attr_done.fetch_or(bit);
     }
     const int grid = dp.work < 148 ? dp.work : 148;
-    const cudaError_t e = launch_k(conv_dws_kernel<PLANES, OW>, dim3(grid), dim3(C::NTHREADS), C::SMEM_BYTES, st, 1, dp, g);
+    const cudaError_t e = launch_k(conv_dws_kernel<PLANES, OW, HYB>, dim3(grid), dim3(C::NTHREADS), C::SMEM_BYTES, st, 1,
+                                   dp, g);
     if (e != cudaSuccess) {
         snprintf(err, errlen, "cudaLaunchKernelEx(dws): %s", cudaGetErrorString(e));
         return CONV_ECUDA;
@@ -468,14 +530,19 @@ int dws_launch(int planes, const GenParams& g, int splits, int kb_per_split, cud
         snprintf(err, errlen, "dws: cuTensorMapEncodeTiled failed");
         return CONV_ECUDA;
     }
-    if (planes == 2) {
-        if (g.OW >= 32) return launch_t<2, 32>(dp, g, st, err, errlen);
-        if (g.OW == 16) return launch_t<2, 16>(dp, g, st, err, errlen);
-        return launch_t<2, 8>(dp, g, st, err, errlen);
+    if (planes == 2 && g_dws_hyb) {
+        if (g.OW >= 32) return launch_t<2, 32, true>(dp, g, st, err, errlen);
+        if (g.OW == 16) return launch_t<2, 16, true>(dp, g, st, err, errlen);
+        return launch_t<2, 8, true>(dp, g, st, err, errlen);
     }
-    if (g.OW >= 32) return launch_t<1, 32>(dp, g, st, err, errlen);
-    if (g.OW == 16) return launch_t<1, 16>(dp, g, st, err, errlen);
-    return launch_t<1, 8>(dp, g, st, err, errlen);
+    if (planes == 2) {
+        if (g.OW >= 32) return launch_t<2, 32, false>(dp, g, st, err, errlen);
+        if (g.OW == 16) return launch_t<2, 16, false>(dp, g, st, err, errlen);
+        return launch_t<2, 8, false>(dp, g, st, err, errlen);
+    }
+    if (g.OW >= 32) return launch_t<1, 32, false>(dp, g, st, err, errlen);
+    if (g.OW == 16) return launch_t<1, 16, false>(dp, g, st, err, errlen);
+    return launch_t<1, 8, false>(dp, g, st, err, errlen);
 }
 
 }  // namespace smconv

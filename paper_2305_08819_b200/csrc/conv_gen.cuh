@@ -40,6 +40,7 @@ struct GenParams {
     const float* B;  // fwd: W   dx: W    dw: X
     float* out;      // output tensor, or split-K workspace (slice s at out + s * split_stride)
     const void* Bx;  // 3xTF32 fwd / dX on TMA / STRIP: bf16 W' plane in the workspace (wx_prep_kernel)
+    const float* Bt;  // 3xTF32 dX on TMA (TmaParams::dx_bk): fp32 Wt[IC][T][OC] in the workspace (wx_prep_kernel)
     long long split_stride;
     int N, IH, IW, IC, OC, FH, FW, sh, sw, ph, pw, OH, OW;
     int M;       // fwd: N*OH*OW; dw: OC (dx: per phase, see phase table)

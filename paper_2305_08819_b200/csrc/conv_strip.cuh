@@ -337,27 +337,33 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
                     // column: split the window into TMEM and that tap's B block into b_lo, then
                     // release it to the MMA warp (conv[ts * FW + fw]) before starting the next one
                     const int qd = warp & 3, h = (warp - C::CONV_W0) >> 2;
-#pragma unroll
-                    for (int fw = 0; fw < C::FW; ++fw) {
+                    // window fw's 16 values of this thread; the next window's loads are issued before
+                    // this window's tcgen05.wait::st (the per-window chain LDS -> split -> STTM -> wait
+                    // was serial; the converters bound the strip pipeline: 2 TMEM slots, ncu r02be)
+                    auto ld16 = [&](int fw, float (&e)[16]) {
                         const int woff = OP == OP_FWD ? fw : C::FW - 1 - fw;
                         const uint8_t* slab = st + (woff + qd) * 4096;
-                        float e[16];
 #pragma unroll
                         for (int cq = 0; cq < 4; ++cq) {
                             const float4 v = *reinterpret_cast<const float4*>(
                                 slab + kmaj_off((uint32_t)lane, (uint32_t)(4 * h + cq)));
                             e[4 * cq] = v.x, e[4 * cq + 1] = v.y, e[4 * cq + 2] = v.z, e[4 * cq + 3] = v.w;
                         }
+                    };
+                    float ebuf[2][16];
+                    ld16(0, ebuf[0]);
+#pragma unroll
+                    for (int fw = 0; fw < C::FW; ++fw) {
                         // window columns: [0,32) a_hi, [32,48) bf16(a_hi) pairs, [48,64) bf16(a_lo) pairs
                         uint32_t hi[16], xh[8], xl[8];
-                        split_a16(e, hi, xh, xl);
+                        split_a16(ebuf[fw & 1], hi, xh, xl);
                         const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) +
                                             (uint32_t)(C::A_TCOL0 + ts * C::A_SLOT_COLS + fw * 64);
                         tmem_st_32x32b_x16(ta + h * 16, hi);
                         tmem_st_32x32b_x8(ta + 32 + h * 8, xh);
                         tmem_st_32x32b_x8(ta + 48 + h * 8, xl);
-                        tmem_st_wait();
-                        fence_proxy_async_smem();
+                        if (fw + 1 < C::FW) ld16(fw + 1, ebuf[(fw + 1) & 1]);
+                        tmem_st_wait();  // (no generic-proxy shared-memory writes here: no proxy fence)
                         tc_fence_before();
                         if (PAIR) {  // one arrival per warp, on CTA 0's barrier (it issues the MMAs)
                             __syncwarp();

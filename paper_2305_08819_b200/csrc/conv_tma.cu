@@ -291,7 +291,11 @@ int tma_launch(int op, int BN, int planes, const GenParams& g, TmaParams& tp, di
         uint64_t da[4] = {OC, OW, OH, N}, sa[3] = {OC * 4, OW * OC * 4, OH * OW * OC * 4};
         uint32_t ba[4] = {32, 1, 1, (uint32_t)tp.G};
         ok &= encode(&tp.mapA, g.A, 4, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B);
-        if (IC % 32 == 0) {
+        if (tp.dx_bk) {  // Wt[IC][T][OC] (wx_prep_kernel, after the W' plane): like the fwd's W
+            uint64_t db[3] = {OC, T, IC}, sb[2] = {OC * 4, T * OC * 4};
+            uint32_t bb[3] = {32, 1, (uint32_t)(tp.pair ? BN / 2 : BN)};
+            ok &= g.Bt && encode(&tp.mapB, g.Bt, 3, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B);
+        } else if (IC % 32 == 0) {
             uint64_t db[4] = {32, OC, IC / 32, T}, sb[3] = {T * IC * 4, 128, IC * 4};
             uint32_t bb[4] = {32, 32, (uint32_t)((tp.pair ? BN / 2 : BN) / 32), 1};
             ok &= encode(&tp.mapB, g.B, 4, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);

@@ -74,6 +74,10 @@ struct __align__(64) TmaParams {
     // pixels (2a, 2b+1), (2a+1, 2b), (2a+1, 2b+1) next to each row (2a, 2b) -- element offsets zf1
     // (one pixel) and zf2 (one dX row) -- instead of a separate zero_phases_kernel pass (0: off)
     long long zf1, zf2;
+    // dX with the K-major transposed filter plane Wt[IC][T][OC] (written by wx_prep_kernel with the W'
+    // plane, 3xTF32 hybrid only): B is staged like the fwd's W (box (32 oc, 1, BNC ic)), K-major
+    // SWIZZLE_128B, instead of the MN-major 32-B-atom view of W
+    int dx_bk;
 };
 
 template <int OP, int BN, int PLANES, bool PAIR = false>
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                                 if (g < ti.ngrp) tma_load_4d(sA + g * tp.G * 128, &tp.mapA, &aux->full[s], cb * 32,
                                             ti.grp[g].y + tap.y, ti.grp[g].x + tap.x, ti.grp[g].z);
                             const int nb0 = n0 + rank * C::BNC;  // this CTA's half of B (pairs)
-                            if (OP == OP_FWD) {
+                            if (OP == OP_FWD || tp.dx_bk) {  // W (OC, T, IC) / Wt (IC, T, OC): K-major box
                                 tma_load_3d(sB, &tp.mapB, &aux->full[s], cb * 32, tap.z, nb0);
                             } else if (tp.dx_ragged) {
 #pragma unroll 1
@@ -641,15 +645,20 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
         // ======================= MMA issuer (whole warp runs the loop, one elected lane issues)
         // pairs: CTA 0 issues M = 256 MMAs for both CTAs; CTA 1's MMA warp only owns its TMEM
         if (!PAIR || rank == 0) {
-            constexpr uint32_t IDESC = idesc_tf32(PAIR ? 256 : 128, BN, C::A_TMEM ? false : C::A_MN, C::B_MN);  // TMEM A: K along columns
-            const uint32_t albo = C::A_MN ? 4096u : 16u, blbo = C::B_MN ? 4096u : 16u;
-            const uint32_t asbo = C::A_MN ? 512u : 1024u, bsbo = C::B_MN ? 512u : 1024u;
+            // dX with the transposed plane (TmaParams::dx_bk): B K-major like the fwd
+            const bool bmn = C::B_MN && !(OP == OP_DX && tp.dx_bk);
+            constexpr uint32_t IDESC_MN = idesc_tf32(PAIR ? 256 : 128, BN, C::A_TMEM ? false : C::A_MN, C::B_MN);  // TMEM A: K along columns
+            constexpr uint32_t IDESC_KM = idesc_tf32(PAIR ? 256 : 128, BN, C::A_TMEM ? false : C::A_MN, false);
+            const uint32_t IDESC = bmn ? IDESC_MN : IDESC_KM;
+            const uint32_t albo = C::A_MN ? 4096u : 16u, blbo = bmn ? 4096u : 16u;
+            const uint32_t asbo = C::A_MN ? 512u : 1024u, bsbo = bmn ? 512u : 1024u;
             const uint32_t alay = C::A_MN ? kLayoutSW128Base32 : kLayoutSW128;
-            const uint32_t blay = C::B_MN ? kLayoutSW128Base32 : kLayoutSW128;
+            const uint32_t blay = bmn ? kLayoutSW128Base32 : kLayoutSW128;
             // descriptors of stage 0; stage s / k-step g only add to the 14-bit start-address field
             const uint64_t adH0 = make_sdesc(tiles_addr, albo, asbo, alay);
             const uint64_t bdH0 = make_sdesc(tiles_addr + C::B_OFF, blbo, bsbo, blay);
-            constexpr uint64_t A_G = C::A_MN ? 64 : 2, B_G = C::B_MN ? 64 : 2;  // (1024 or 32 bytes) >> 4
+            constexpr uint64_t A_G = C::A_MN ? 64 : 2;  // (1024 or 32 bytes) >> 4
+            const uint64_t B_G = bmn ? 64 : 2;
             // 3xTF32 cross terms: bf16 B' plane [b_lo | b] (K-major, 128 B per row) after b_hi
             constexpr uint32_t IDESC_X = idesc_bf16(PAIR ? 256 : 128, BN, false, false);
             const uint64_t bx0 = make_sdesc(tiles_addr + C::B_OFF + C::B_BYTES, 16u, 1024u, kLayoutSW128);
@@ -826,7 +835,9 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     for (int i = 0; i < NB; ++i) bL[ct + i * NCT] = lo4(vb[i]);
                 }
                 if (C::A_TMEM) tmem_st_wait();
-                fence_proxy_async_smem();
+                // generic-proxy shared-memory writes (a_lo / b_lo planes) must be visible to the MMA's
+                // async proxy; the hybrid fwd / dX converters write TMEM only
+                if (!C::A_TMEM || !(C::HYB && p.hyb)) fence_proxy_async_smem();
                 tc_fence_before();
                 if (PAIR) {  // one arrival per warp, on CTA 0's barrier (it issues the MMAs)
                     __syncwarp();

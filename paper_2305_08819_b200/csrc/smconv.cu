@@ -157,6 +157,7 @@ struct Plan {
     dim3 grid;
     size_t ws_bytes;
     size_t wx_off, wx_bytes;  // 3xTF32 fwd / dX (TMA, STRIP): bf16 W' plane in the workspace
+    size_t wt_off, wt_bytes;  // 3xTF32 dX (TMA, TmaParams::dx_bk): fp32 Wt[IC][T][OC] after it
     long long out_elems;
     GenParams gp;
     TmaParams tp;
@@ -187,6 +188,8 @@ constexpr int kMaxKbPerChain = 256;
 constexpr int kGenMaxKbPerChain3x = 16;  // GENERIC 3xTF32 (no chunked promotion)
 // largest cluster split-K (TMA fwd / dX on small maps); SMCONV_CSK=0 turns it off (A/B experiments)
 const int g_csk_max = getenv("SMCONV_CSK") ? atoi(getenv("SMCONV_CSK")) : 8;
+// SMCONV_DX_BK=0: 3xTF32 TMA dX reads the MN-major view of W instead of the transposed plane (A/B)
+const int g_dx_bk = getenv("SMCONV_DX_BK") ? atoi(getenv("SMCONV_DX_BK")) : 1;
 // SMCONV_ZFILL=0: keep zero_phases_kernel for the 1x1 stride-2 dX (A/B experiments)
 const int g_zfill = getenv("SMCONV_ZFILL") ? atoi(getenv("SMCONV_ZFILL")) : 1;
 constexpr int kSMs = 148;
@@ -706,11 +709,21 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
         const int Kp = ((op == CONV_OP_FWD ? d.IC : d.OC) + 31) / 32 * 32;  // reduction channels padded to 32
         pl.wx_bytes = (size_t)d.FH * d.FW * (op == CONV_OP_FWD ? d.OC : d.IC) * Kp * 4;
         pl.ws_bytes = pl.wx_off + pl.wx_bytes;
+        // dX: the same launch also writes the K-major transposed filter (TmaParams::dx_bk), so the
+        // TF32 MMA reads B like the fwd does (the MN-major 32-B-atom B made 3xTF32 dX 9-13 % slower
+        // than fwd on the same shape, r02bc; TF32 dX, which reads the MN-major view, runs at fwd speed)
+        pl.wt_off = pl.wt_bytes = 0;
+        if (op == CONV_OP_BWD_DATA && pl.variant == CONV_VARIANT_TMA && g_dx_bk) {
+            pl.wt_off = (pl.ws_bytes + 1023) & ~(size_t)1023;
+            pl.wt_bytes = (size_t)d.FH * d.FW * d.OC * d.IC * 4;
+            pl.ws_bytes = pl.wt_off + pl.wt_bytes;
+        }
     }
     pl.grid = dim3(m_tiles, n_tiles, splits);
     if (pl.variant == CONV_VARIANT_TMA) {
         int rc = tma_make_plan(op, g, pl.BN, pl.planes, pl.tp, pl.grid, g_detail, sizeof g_detail);
         if (rc) return rc;
+        pl.tp.dx_bk = pl.wt_bytes ? 1 : 0;
         // 1x1 stride-2 dX (ResNet shortcuts): only phase (0, 0) has a tap; the row-coalesced epilogue
         // writes the three empty phases' zeros beside each of its rows (one pass over dX instead of the
         // conv + a zero_phases_kernel pass that ran at ~3.5 TB/s, ncu r02bb)
@@ -763,7 +776,7 @@ int launch_gen_op(const Plan& pl, const GenParams& g, cudaStream_t st) {
 // [bf16(w_lo) for k = 32cb..32cb+31 | bf16(w) for the same k], w_lo = w - trunc_tf32(w); the GEMM
 // column n / reduction index k are (oc, ic) for fwd and (ic, oc) for dX.  One thread per row.
 __global__ void __launch_bounds__(256) wx_prep_kernel(const float* __restrict__ W, uint4* __restrict__ Wx, int OC,
-                                                      int IC, int T, int dx) {
+                                                      int IC, int T, int dx, float* __restrict__ Wt) {
     pdl_trigger();
     pdl_wait();
     // Kc need not be a multiple of 32 (GoogLeNet 16/24/48/112/...-channel layers): the last block's
@@ -784,6 +797,7 @@ __global__ void __launch_bounds__(256) wx_prep_kernel(const float* __restrict__ 
             tap = (int)(q / Nn);
         }
         uint32_t lo[16], hi[16];
+        float wv[32];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
             float w0 = 0.f, w1 = 0.f;
@@ -798,9 +812,18 @@ __global__ void __launch_bounds__(256) wx_prep_kernel(const float* __restrict__ 
                     w1 = v.y;
                 }
             }
+            wv[2 * i] = w0;
+            wv[2 * i + 1] = w1;
             lo[i] = pack_bf16x2(w0 - __uint_as_float(__float_as_uint(w0) & 0xFFFFE000u),
                                 w1 - __uint_as_float(__float_as_uint(w1) & 0xFFFFE000u));
             hi[i] = pack_bf16x2(w0, w1);
+        }
+        if (Wt) {  // dX: Wt[ic = n][tap][oc = k] for this row's 32 k (Kc % 4 == 0: whole float4s in range)
+            float* t = Wt + ((size_t)n * T + tap) * Kc + 32 * cb;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (32 * cb + 4 * q < Kc)
+                    *reinterpret_cast<float4*>(t + 4 * q) = make_float4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
         }
         uint4* o = Wx + (((size_t)tap * Nn + n) * CB + cb) * 8;
 #pragma unroll
@@ -868,6 +891,7 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
     const bool ws_split = (pl.splits > 1 && !pl.gp.csk) || pl.mc_reduce;
     g.out = ws_split ? (float*)ws : out;
     g.Bx = nullptr;
+    g.Bt = nullptr;
     g.mc_out = pl.mc_direct ? out : nullptr;  // `out` is the multicast address in the mcast plans
     g.trace = g_trace.load();
     // pass form of the LEAKY_BWD modes: the conv (and its reduce / zero fill) write the staging buffer
@@ -900,7 +924,8 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
             g.Bx = (char*)ws + pl.wx_off;
             const long long rows = 4LL * d.OC * 4 * d.IC / 32;
             const int bl = (int)((rows + 255) / 256 < kSMs * 4 ? (rows + 255) / 256 : kSMs * 4);
-            launch_k(wx_prep_kernel, dim3(bl), dim3(256), 0, st, 1, (const float*)w2, (uint4*)g.Bx, 4 * d.IC, d.OC, 4, 0);
+            launch_k(wx_prep_kernel, dim3(bl), dim3(256), 0, st, 1, (const float*)w2, (uint4*)g.Bx, 4 * d.IC, d.OC, 4, 0,
+                     (float*)nullptr);
         }
         TmaParams tp = pl.tp;
         rc = tma_launch(CONV_OP_FWD, pl.BN, pl.planes, g, tp, pl.grid, st, g_detail, sizeof g_detail);
@@ -914,10 +939,11 @@ int run(int op, const float* A, const float* B, float* out, const Dims& d, int m
     }
     if (pl.wx_bytes) {
         g.Bx = (char*)ws + pl.wx_off;
+        g.Bt = pl.wt_bytes ? (const float*)((char*)ws + pl.wt_off) : nullptr;
         const long long rows = (long long)pl.wx_bytes / 128;  // one 64-bf16 row per (tap, column, 32-k block)
         const int blocks = (int)((rows + 255) / 256 < kSMs * 4 ? (rows + 255) / 256 : kSMs * 4);
         launch_k(wx_prep_kernel, dim3(blocks), dim3(256), 0, st, 1, B, (uint4*)g.Bx, d.OC, d.IC, d.FH * d.FW,
-                 (int)(op == CONV_OP_BWD_DATA));
+                 (int)(op == CONV_OP_BWD_DATA), (float*)g.Bt);
     }
     if (pl.variant == CONV_VARIANT_DIRECT) {
         rc = direct_launch(op, g, pl.splits, st, g_detail, sizeof g_detail);
