@@ -368,7 +368,8 @@ def main():
     def tensor_div(op, plan):
         # tensor-pipe cost per product in TF32-MMA units: 3xTF32 dW = 3 TF32 MMAs; 3xTF32 fwd / dX on the
         # TMA / STRIP variants = 1 TF32 MMA + 1 bf16 MMA of twice the K at twice the rate = 2
-        hyb = op != "dw" and ("variant=tma" in plan or "variant=strip" in plan) and " 3mma" not in plan
+        hyb = (op != "dw" and ("variant=tma" in plan or "variant=strip" in plan) and " 3mma" not in plan) or \
+            " hybw" in plan  # TMA dW with the bf16 cross terms (TmaParams::dw_hyb)
         return (2.0 if hyb else 3.0) if a.math == "3xtf32" else 1.0
 
     for (op, i), v in per.items():
@@ -412,7 +413,7 @@ def main():
     roof["kernel"] = "%s %s (%s)" % (top["op"], top["layer"], top["plan"])
     roof["peak_src"] = "%s; TF32 = bf16_tflops_sustained x 1.1/2.25%s" % (
         P["src"], {3.0: " / 3 (3xTF32 dW issues 3 TF32 MMAs per product)",
-                   2.0: " / 2 (3xTF32 fwd/dX: 1 TF32 MMA + 1 K-doubled bf16 MMA per product)"}.get(mathdiv, ""))
+                   2.0: " / 2 (3xTF32 hybrid: 1 TF32 MMA + 1 K-doubled bf16 MMA per product)"}.get(mathdiv, ""))
     roof["share_of_step"] = top["ms"] * a.steps / ms
 
     imgs = a.global_batch * a.steps
@@ -424,6 +425,9 @@ def main():
                                   % (a.net, a.global_batch),
                       "global_batch": a.global_batch, "per_gpu_batch": B, "math": a.math,
                       "fwd_dx_cross_terms": "bf16" if a.math == "3xtf32" else None,
+                      "cross_terms": ("bf16 (1 TF32 + 1 K-doubled bf16 MMA per product): fwd/dX on TMA and STRIP, "
+                                      "dW on TMA; strict 3xTF32 (3 TF32 MMAs): DWS / STEM / GENERIC dW")
+                      if a.math == "3xtf32" else None,
                       "epilogue": ("fused: fwd + BN statistics, dX + LeakyReLU backward + BN-backward statistics"
                                    if a.epi else "none (plain conv outputs)"),
                       "cuda_graph": graph is not None, "dw_stream": dw_stream,

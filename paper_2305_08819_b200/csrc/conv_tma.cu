@@ -25,6 +25,10 @@ const int g_knob_promo = env_int("SMCONV_TMA_L2PROMO", 3);
 const int g_knob_chunk = env_int("SMCONV_TMA_CHUNK", 8);
 // SMCONV_COALESCE=0: fwd / dX epilogue stores straight from the TMEM lanes (A/B experiments)
 const int g_knob_coalesce = env_int("SMCONV_COALESCE", 1);
+// 3xTF32 TMA dW with bf16 cross terms (TmaCfg::HYBW; SMCONV_DW_HYB=0: three TF32 MMAs).  Measured
+// r02bl: isolated l2-l4 dW -4..7 %, ResNet-18 b4096 step 54.5 -> 53.6 ms in three same-box A/B pairs
+// (the step is power-capped: 2 instead of 3 MMA-equivalents per product is less energy per step)
+const int g_knob_dw_hyb = env_int("SMCONV_DW_HYB", 1);
 std::atomic<int> g_pair{env_int("SMCONV_PAIR", 1)};  // CTA pairs (smconv_set_pair); on by default since r01o
 const int g_dw_pair = env_int("SMCONV_DW_PAIR", 1);  // dW pairs (A/B knob; follows g_pair when on)
 
@@ -190,6 +194,7 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
     if (g_knob_G == 32) tp.G = 32;
     tp.chunk_kb = g_knob_chunk > 0 ? g_knob_chunk : 8;
     tp.coalesce = g_knob_coalesce;
+    tp.dw_hyb = (op == CONV_OP_BWD_FILTER && !g.dwt && planes == 2) ? g_knob_dw_hyb : 0;
     if (planes == 2 && BN > 128) {
         snprintf(err, errlen, "tma plan: BN %d > 128 in 3xTF32", BN);
         return CONV_EUNSUPPORTED;

@@ -78,7 +78,15 @@ struct __align__(64) TmaParams {
     // plane, 3xTF32 hybrid only): B is staged like the fwd's W (box (32 oc, 1, BNC ic)), K-major
     // SWIZZLE_128B, instead of the MN-major 32-B-atom view of W
     int dx_bk;
+    int dw_hyb;  // dW cross terms in bf16 (TmaCfg::HYBW)
 };
+
+// byte offset of bf16 elements (k, mn..mn+3), mn % 4 == 0, in a [K][MN] MN-major SWIZZLE_128B bf16 tile:
+// 64-element (128-B) MN atoms of K rows each (atom stride K * 128 B), 8-row x 128-B swizzle groups
+SMCONV_DEV uint32_t mnmaj16_off(uint32_t k, uint32_t mn, uint32_t krows) {
+    return (mn >> 6) * krows * 128u + (k >> 3) * 1024u + (k & 7u) * 128u + ((((mn >> 3) & 7u) ^ (k & 7u)) << 4) +
+           (mn & 7u) * 2u;
+}
 
 template <int OP, int BN, int PLANES, bool PAIR = false>
 struct TmaCfg {
@@ -109,6 +117,10 @@ struct TmaCfg {
     // b_lo plane split by the converters (its B is an activation tile; the bf16 split of an
     // MN-major activation tile cost more converter time than the tensor pipe saved, r01l)
     static constexpr bool HYB = A_TMEM && !IS_DW;
+    // dW (not transposed) with the same cross-term form (TmaParams::dw_hyb): A' = [bf16(a_hi) | bf16(a_lo)]
+    // in TMEM next to a_hi, B' = [bf16(b_lo) ; bf16(b)] as a K' = 64 bf16 MN-major plane the converters
+    // build from the X tile in place of the fp32 b_lo plane (same bytes): 2 MMA-equivalents per product
+    static constexpr bool HYBW = A_TMEM && OP == OP_DW;
     static constexpr bool A_MN = IS_DW;
     static constexpr bool B_MN = (OP != OP_FWD);
     static constexpr int A_TCOL0 = 2 * BN;  // TMEM column of A slot 0 (A_TMEM)
@@ -662,6 +674,10 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             // 3xTF32 cross terms: bf16 B' plane [b_lo | b] (K-major, 128 B per row) after b_hi
             constexpr uint32_t IDESC_X = idesc_bf16(PAIR ? 256 : 128, BN, false, false);
             const uint64_t bx0 = make_sdesc(tiles_addr + C::B_OFF + C::B_BYTES, 16u, 1024u, kLayoutSW128);
+            // dW hybrid: B' [64 k'][BNC] bf16 MN-major (LBO = one 64-column atom = 64 rows x 128 B)
+            constexpr uint32_t IDESC_XW = idesc_bf16(PAIR ? 256 : 128, BN, false, true);
+            const uint64_t bxw0 = make_sdesc(tiles_addr + C::B_OFF + C::B_BYTES, 8192u, 1024u, kLayoutSW128);
+            const bool hybw = C::HYBW && tp.dw_hyb;
             int s = 0, in_chunk = 0;
             uint32_t r = 0, c = 0, q = 0;  // stage, ring round, chunk counter, k-block (global across tiles)
             for (int w = wfirst; w < tp.work; w += wstep) {
@@ -690,7 +706,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                             const uint64_t adH = adH0 + so + g * A_G, bdH = bdH0 + so + g * B_G;
                             const uint32_t acc0 = (in_chunk > 0 || g > 0) ? 1u : 0u;
                             const uint32_t ahi = tmem + (uint32_t)(C::A_TCOL0 + t * 64 + g * 8);
-                            if (C::HYB && p.hyb) {  // a_hi * b_hi (TF32); cross terms below
+                            if ((C::HYB && p.hyb) || hybw) {  // a_hi * b_hi (TF32); cross terms below
                                 if (PAIR) mma2_tf32_ts(d, ahi, bdH, IDESC, acc0);
                                 else mma_tf32_ts(d, ahi, bdH, IDESC, acc0);
                             } else if (C::A_TMEM && PAIR) {  // three TF32 MMAs, M = 256 (dW; fwd / dX !hyb)
@@ -713,6 +729,14 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                                 const uint32_t ax = tmem + (uint32_t)(C::A_TCOL0 + t * 64 + 32 + j * 8);
                                 if (PAIR) mma2_bf16_ts(d, ax, bx0 + so + j * 2, IDESC_X, 1u);
                                 else mma_bf16_ts(d, ax, bx0 + so + j * 2, IDESC_X, 1u);
+                            }
+                        }
+                        if (hybw) {  // dW: the same cross terms, B' rows 16 j .. 16 j + 15 (2 KB apart)
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const uint32_t ax = tmem + (uint32_t)(C::A_TCOL0 + t * 64 + 32 + j * 8);
+                                if (PAIR) mma2_bf16_ts(d, ax, bxw0 + so + j * (2048 >> 4), IDESC_XW, 1u);
+                                else mma_bf16_ts(d, ax, bxw0 + so + j * (2048 >> 4), IDESC_XW, 1u);
                             }
                         }
                         if (trc && last) trace_mark(trc, 5);
@@ -797,7 +821,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                     // pairs, [48,64) bf16(a_lo) likewise; this thread has k in [16h, 16h+16)
                     // (dW: [32,64) a_lo fp32 for the third TF32 MMA)
                     const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(C::A_TCOL0 + t * 64);
-                    if (C::HYB && p.hyb) {
+                    if ((C::HYB && p.hyb) || (C::HYBW && tp.dw_hyb)) {
                         uint32_t hi[16], xh[8], xl[8];
                         split_a16(e, hi, xh, xl);
                         tmem_st_32x32b_x16(ta + h * 16, hi);
@@ -825,7 +849,28 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
 #pragma unroll
                     for (int i = 0; i < NA; ++i) aL[ct + i * NCT] = lo4(va[i]);
                 }
-                if (!(C::HYB && p.hyb)) {  // b_lo plane (dW, fwd / dX without the W' plane, the SS fallback)
+                if (C::HYBW && tp.dw_hyb) {
+                    // dW hybrid: B' = [bf16(b_lo) ; bf16(b)] from the fp32 MN-major X tile.  float4 i of the
+                    // tile: 32-column block i / 256, K-row (i % 256) / 8, 32-B chunk (i % 8) / 2 stored
+                    // swizzled with k % 4 (mnmaj_off), 16-B half i % 2
+                    const float4* bH = reinterpret_cast<const float4*>(st + C::B_OFF);
+                    uint8_t* bX = st + C::B_OFF + C::B_BYTES;
+                    float4 vb[NB];
+#pragma unroll
+                    for (int i = 0; i < NB; ++i) vb[i] = bH[ct + i * NCT];
+#pragma unroll
+                    for (int e2 = 0; e2 < NB; ++e2) {
+                        const uint32_t i = (uint32_t)(ct + e2 * NCT);
+                        const uint32_t k = (i & 255u) >> 3, c32 = (i & 7u) >> 1;
+                        const uint32_t mn = (i >> 8) * 32u + ((c32 ^ (k & 3u)) << 3) + ((i & 1u) << 2);
+                        const float4 b = vb[e2];
+                        const float4 l = lo4(b);
+                        *reinterpret_cast<uint2*>(bX + mnmaj16_off(k, mn, 64u)) =
+                            make_uint2(pack_bf16x2(l.x, l.y), pack_bf16x2(l.z, l.w));
+                        *reinterpret_cast<uint2*>(bX + mnmaj16_off(k + 32u, mn, 64u)) =
+                            make_uint2(pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+                    }
+                } else if (!(C::HYB && p.hyb)) {  // b_lo plane (dW, fwd / dX without the W' plane, the SS fallback)
                     const float4* bH = reinterpret_cast<const float4*>(st + C::B_OFF);
                     float4* bL = reinterpret_cast<float4*>(st + C::B_OFF + C::B_BYTES);
                     float4 vb[NB];

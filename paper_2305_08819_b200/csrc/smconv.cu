@@ -1294,7 +1294,8 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
                      : "", pl.gp.csk ? " csk" : "",
                  (pl.variant == CONV_VARIANT_TMA && pl.planes == 2 && op != CONV_OP_BWD_FILTER && !pl.gp.hyb) ? " 3mma"
                                                                                                               : "",
-                 (pl.variant == CONV_VARIANT_TMA && pl.tp.zf1) ? " zfill" : "",
+                 (pl.variant == CONV_VARIANT_TMA && pl.tp.zf1) ? " zfill"
+                 : (pl.variant == CONV_VARIANT_TMA && pl.tp.dw_hyb) ? " hybw" : "",
                  pl.BN, pl.planes, pl.splits, pl.grid.x,
                  pl.grid.y, pl.grid.z, pl.ws_bytes, plan_kernel_count(pl));
     return CONV_OK;
