@@ -79,7 +79,46 @@ struct __align__(64) TmaParams {
     // SWIZZLE_128B, instead of the MN-major 32-B-atom view of W
     int dx_bk;
     int dw_hyb;  // dW cross terms in bf16 (TmaCfg::HYBW)
+    // fwd / dX: the row-coalesced epilogue's pieces leave by TMA tensor store (cp.async.bulk.tensor) from
+    // the warp's staging slice instead of LDS + SHFL + STG per thread: mapY views the output as
+    // (C, pixels, N), box (EPW, 1, 32 images); the staging slice already holds the TMA's 64B / 128B
+    // swizzle (warp_rows_store's XOR pattern).  0: per-thread stores (s2dx, zfill, csk, odd N)
+    int tstore;
+    CUtensorMap mapY;
 };
+
+SMCONV_DEV void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+SMCONV_DEV void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+SMCONV_DEV void bulk_wait_group_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+SMCONV_DEV void bulk_wait_group0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// The same staging as warp_rows_store, then ONE TMA tensor store of the warp's 32 rows x PW columns
+// (rows = 32 consecutive images at output pixel `pix`, starting at image n0).  Lane 0 owns the bulk
+// group: it waits until the previous store has READ the slice before the lanes overwrite it.
+template <int PW>
+SMCONV_DEV void warp_rows_tstore(uint8_t* stg, const float (&f)[PW], const CUtensorMap* map, int col0, int pix, int n0,
+                                 bool valid, int lane) {
+    constexpr int F4 = PW / 4;
+    static_assert(F4 == 4 || F4 == 8, "piece of 16 or 32 columns");
+    auto swz = [](int r) { return F4 == 8 ? (r & 7) : ((r >> 1) & 3); };
+    if (lane == 0) bulk_wait_group_read0();
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < F4; ++j)
+        *reinterpret_cast<float4*>(stg + (lane * F4 + (j ^ swz(lane))) * 16) =
+            make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+    fence_proxy_async_smem();  // generic-proxy writes -> visible to the TMA (async proxy)
+    __syncwarp();
+    if (lane == 0 && valid) {
+        tma_store_3d(map, smem_u32(stg), col0, pix, n0);
+        bulk_commit_group();
+    }
+}
 
 // byte offset of bf16 elements (k, mn..mn+3), mn % 4 == 0, in a [K][MN] MN-major SWIZZLE_128B bf16 tile:
 // 64-element (128-B) MN atoms of K rows each (atom stride K * 128 B), 8-row x 128-B swizzle groups
@@ -912,6 +951,8 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             const int nch = nkb > 0 ? (nkb + CHK - 1) / CHK : 0;
             float* outp = p.out + (long long)ti.split * p.split_stride;
             long long obase = -1;
+            int ts_n0 = 0, ts_pix = 0;
+            bool ts_ok = false;
             if (OP == OP_DW) {
                 const int oc = ti.m0 + row;
                 if (oc < p.OC) obase = (long long)oc * (p.dw_icp ? p.FH * p.FW * p.IC : p.Ngemm);
@@ -920,6 +961,11 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                 if (m < p.M) obase = m;
             } else {
                 RowInfo ri = row_info<OP>(p, ti.phase, ti.m0 + row);
+                // TMA-store coordinates of this warp's 32 rows (lane 0's row: 32 consecutive images at one pixel)
+                const int P_ = OP == OP_FWD ? p.OH * p.OW : p.IH * p.IW;
+                ts_n0 = __shfl_sync(0xffffffffu, ri.n, 0);
+                ts_pix = __shfl_sync(0xffffffffu, ri.orow - ri.n * P_, 0);
+                ts_ok = __shfl_sync(0xffffffffu, (int)ri.ok, 0) != 0;
                 if (OP == OP_FWD && p.s2dx) {
                     if (ri.ok) {
                         const int pos = ri.orow - ri.n * p.OH * p.OW, oh = pos / p.OW, ow = pos - oh * p.OW;
@@ -1020,8 +1066,12 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
 #pragma unroll
                         for (int c0 = 0; c0 < HALF; c0 += C::EPW) {
                             const int col0 = n0 + half * HALF + c0;
-                            warp_rows_store<C::EPW>(stg, *reinterpret_cast<const float(*)[C::EPW]>(&acc[c0]), obase, outp,
-                                                    col0, p.Ngemm, s2shift(col0), lane, tp.zf1, tp.zf2);
+                            if (tp.tstore)
+                                warp_rows_tstore<C::EPW>(stg, *reinterpret_cast<const float(*)[C::EPW]>(&acc[c0]), &tp.mapY,
+                                                         col0, ts_pix, ts_n0, ts_ok, lane);
+                            else
+                                warp_rows_store<C::EPW>(stg, *reinterpret_cast<const float(*)[C::EPW]>(&acc[c0]), obase,
+                                                        outp, col0, p.Ngemm, s2shift(col0), lane, tp.zf1, tp.zf2);
                         }
                         stored = true;
                     }
@@ -1097,7 +1147,11 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
 #pragma unroll
                                 for (int e = 0; e < C::EPW; ++e) f[e] = __uint_as_float(v[p0 + e]);
                                 const int col0 = n0 + half * HALF + c0 + p0;
-                                warp_rows_store<C::EPW>(stg, f, obase, outp, col0, p.Ngemm, s2shift(col0), lane, tp.zf1, tp.zf2);
+                                if (tp.tstore)
+                                    warp_rows_tstore<C::EPW>(stg, f, &tp.mapY, col0, ts_pix, ts_n0, ts_ok, lane);
+                                else
+                                    warp_rows_store<C::EPW>(stg, f, obase, outp, col0, p.Ngemm, s2shift(col0), lane, tp.zf1,
+                                                            tp.zf2);
                             }
                             continue;
                         }
@@ -1130,6 +1184,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
         }
     }
 
+    if (warp < C::NEPI && lane == 0 && tp.tstore) bulk_wait_group0();  // the epilogue's TMA stores are done
     if (trc && tid == 0) trace_mark(trc, 7);
     tc_fence_before();
     __syncthreads();
