@@ -22,9 +22,21 @@ namespace {
 const int g_knob_chunk_s = getenv("SMCONV_TMA_CHUNK") ? atoi(getenv("SMCONV_TMA_CHUNK")) : 8;
 const int g_knob_coalesce_s = getenv("SMCONV_COALESCE") ? atoi(getenv("SMCONV_COALESCE")) : 1;
 
+const int g_knob_tstore_s = getenv("SMCONV_TSTORE") ? atoi(getenv("SMCONV_TSTORE")) : 1;
+
 template <int OP, int BN, int PLANES, int R, bool PAIR = false>
-int launch_t(const StripParams& sp, const GenParams& g, cudaStream_t st, char* err, size_t errlen) {
+int launch_t(const StripParams& sp0, const GenParams& g, cudaStream_t st, char* err, size_t errlen) {
     using C = StripCfg<OP, BN, PLANES, R, PAIR>;
+    StripParams sp = sp0;
+    sp.tstore = 0;
+    if (C::EPW > 0 && sp.coalesce && g_knob_tstore_s && g.split_stride == 0) {  // TMA-store epilogue (DESIGN 6d)
+        const uint64_t Cc = OP == OP_FWD ? g.OC : g.IC, P = OP == OP_FWD ? (uint64_t)g.OH * g.OW : (uint64_t)g.IH * g.IW;
+        uint64_t dy[3] = {Cc, P, (uint64_t)g.N}, sy[2] = {Cc * 4, P * Cc * 4};
+        uint32_t by[3] = {(uint32_t)(C::EPW > 0 ? C::EPW : 16), 1, 32};
+        if (tma_encode_f32(&sp.mapY, g.out, 3, dy, sy, by,
+                           C::EPW == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
+            sp.tstore = 1;
+    }
     static std::atomic<unsigned long long> attr_done{0};
     int dev = 0;
     cudaGetDevice(&dev);

@@ -42,6 +42,8 @@ struct __align__(64) StripParams {
     int pair;          // work items are pair tiles (two 32-image groups), kernel template PAIR
     FastDiv fd_ntiles, fd_strips, fd_OHo;
     int coalesce;      // row-coalesced epilogue stores (StripCfg::EPW)
+    int tstore;        // ... leaving by TMA tensor store (conv_tma.cuh warp_rows_tstore): mapY = output (C, pixels, N)
+    CUtensorMap mapY;
 };
 
 template <int OP, int BN, int PLANES, int R, bool PAIR = false>
@@ -471,8 +473,14 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
                                                     obase[j] >= 0 && col0 + q < p.Ngemm ? obase[j] + col0 + q : -1,
                                                     col0 + q, p.Ngemm, strip_grp<R>(sp, t, j, qd), lane);
                                 }
-                                warp_rows_store<C::EPW>(stg, *reinterpret_cast<const float(*)[C::EPW]>(&acc[j][c0]), obase[j],
-                                                        outp, col0, p.Ngemm, 0, lane);
+                                if (sp.tstore) {
+                                    const int ocol = t.s * 4 * R + 4 * j + qd;
+                                    warp_rows_tstore<C::EPW>(stg, *reinterpret_cast<const float(*)[C::EPW]>(&acc[j][c0]), &sp.mapY,
+                                                             col0, t.orow * sp.OWo + ocol, t.g * 32, ocol < sp.OWo, lane);
+                                } else {
+                                    warp_rows_store<C::EPW>(stg, *reinterpret_cast<const float(*)[C::EPW]>(&acc[j][c0]), obase[j],
+                                                            outp, col0, p.Ngemm, 0, lane);
+                                }
                             }
                         stored = true;
                     }
@@ -548,7 +556,13 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
                                         for (int e = 0; e < 16; ++e) f[q + e] = v[e];
                                     }
                                 }
-                                warp_rows_store<C::EPW>(stg, f, obase[j], outp, col0, p.Ngemm, 0, lane);
+                                if (sp.tstore) {
+                                    const int ocol = t.s * 4 * R + 4 * j + qd;
+                                    warp_rows_tstore<C::EPW>(stg, f, &sp.mapY, col0, t.orow * sp.OWo + ocol, t.g * 32,
+                                                             ocol < sp.OWo, lane);
+                                } else {
+                                    warp_rows_store<C::EPW>(stg, f, obase[j], outp, col0, p.Ngemm, 0, lane);
+                                }
                             }
                             continue;
                         }
@@ -594,6 +608,7 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
     }
 
 strip_done:
+    if (warp < C::NEPI && lane == 0 && sp.tstore) bulk_wait_group0();  // the epilogue's TMA stores are done
     tc_fence_before();
     __syncthreads();
     if (PAIR) cluster_sync_all();  // the peer's MMAs / arrivals are done before TMEM is released
