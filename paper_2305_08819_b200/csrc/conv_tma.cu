@@ -27,6 +27,7 @@ const int g_knob_chunk = env_int("SMCONV_TMA_CHUNK", 8);
 const int g_knob_coalesce = env_int("SMCONV_COALESCE", 1);
 // SMCONV_TSTORE=0: the row-coalesced fwd / dX epilogue stores per thread instead of by TMA (A/B)
 const int g_knob_tstore = env_int("SMCONV_TSTORE", 1);
+const int g_knob_tstore_s2 = env_int("SMCONV_TSTORE_S2DX", 1);  // ... for the super-pixel dX too
 // 3xTF32 TMA dW with bf16 cross terms (TmaCfg::HYBW; SMCONV_DW_HYB=0: three TF32 MMAs).  Measured
 // r02bl: isolated l2-l4 dW -4..7 %, ResNet-18 b4096 step 54.5 -> 53.6 ms in three same-box A/B pairs
 // (the step is power-capped: 2 instead of 3 MMA-equivalents per product is less energy per step)
@@ -348,11 +349,13 @@ int tma_launch(int op, int BN, int planes, const GenParams& g, TmaParams& tp, di
     }
     // TMA-store epilogue (TmaParams::tstore): plain fwd / dX rows that go straight to the output tensor
     tp.tstore = 0;
-    if ((op == CONV_OP_FWD || op == CONV_OP_BWD_DATA) && g_knob_tstore && tp.coalesce && !tp.csk && !g.s2dx &&
-        !tp.zf1 && g.split_stride == 0 && !g.mc_out && g.N % 32 == 0) {
+    if ((op == CONV_OP_FWD || op == CONV_OP_BWD_DATA) && g_knob_tstore && tp.coalesce && !tp.csk &&
+        (!g.s2dx || g_knob_tstore_s2) && !tp.zf1 && g.split_stride == 0 && !g.mc_out && g.N % 32 == 0) {
         const int epw = tma_epw(op, BN, planes, tp.pair);
         if (epw == 16 || epw == 32) {
-            const uint64_t C = op == CONV_OP_FWD ? OC : IC, P = op == CONV_OP_FWD ? OH * OW : IH * IW;
+            // s2dx: the super-pixel fwd conv's output is dX itself (IC, IH x IW pixels, N)
+            const uint64_t C = g.s2dx ? (uint64_t)g.s2_IC : op == CONV_OP_FWD ? OC : IC;
+            const uint64_t P = g.s2dx ? (uint64_t)g.s2_IH * g.s2_IW : op == CONV_OP_FWD ? OH * OW : IH * IW;
             uint64_t dy[3] = {C, P, N}, sy[2] = {C * 4, P * C * 4};
             uint32_t by[3] = {(uint32_t)epw, 1, 32};
             if (encode(&tp.mapY, g.out, 3, dy, sy, by,

@@ -966,6 +966,11 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                 ts_n0 = __shfl_sync(0xffffffffu, ri.n, 0);
                 ts_pix = __shfl_sync(0xffffffffu, ri.orow - ri.n * P_, 0);
                 ts_ok = __shfl_sync(0xffffffffu, (int)ri.ok, 0) != 0;
+                if (OP == OP_FWD && p.s2dx) {  // super-pixel (i', j') -> dX pixel (2i'-2, 2j'-2) of column block q = 0
+                    const int i1 = ts_pix / p.OW, j1 = ts_pix - i1 * p.OW;
+                    ts_ok = ts_ok && i1 >= 1 && j1 >= 1;
+                    ts_pix = (2 * i1 - 2) * p.s2_IW + 2 * j1 - 2;
+                }
                 if (OP == OP_FWD && p.s2dx) {
                     if (ri.ok) {
                         const int pos = ri.orow - ri.n * p.OH * p.OW, oh = pos / p.OW, ow = pos - oh * p.OW;
@@ -988,6 +993,18 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             // row-coalesced stores (TmaCfg::EPW): s2dx columns (pi = 1, pj, ic) land one dX row further
             auto s2shift = [&](int col0) -> long long {
                 return (OP == OP_FWD && p.s2dx && col0 >= 2 * p.s2_IC) ? (long long)(p.s2_IW - 2) * p.s2_IC : 0;
+            };
+            // TMA-store coordinates of the piece starting at GEMM column col0: (channel, pixel); s2dx columns
+            // (pi, pj, ic) land on dX pixel (2i'-2+pi, 2j'-2+pj) (IC % 64 == 0: a piece never straddles)
+            auto ts_c = [&](int col0) -> int {
+                return (OP == OP_FWD && p.s2dx) ? col0 - (col0 / p.s2_IC) * p.s2_IC : col0;
+            };
+            auto ts_p = [&](int col0) -> int {
+                if (OP == OP_FWD && p.s2dx) {
+                    const int q = col0 / p.s2_IC;
+                    return ts_pix + (q >> 1) * p.s2_IW + (q & 1);
+                }
+                return ts_pix;
             };
             // 4 consecutive GEMM columns of this thread's row -> output
             auto st4 = [&](int col, float x, float y, float z, float w4) {
@@ -1068,7 +1085,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                             const int col0 = n0 + half * HALF + c0;
                             if (tp.tstore)
                                 warp_rows_tstore<C::EPW>(stg, *reinterpret_cast<const float(*)[C::EPW]>(&acc[c0]), &tp.mapY,
-                                                         col0, ts_pix, ts_n0, ts_ok, lane);
+                                                         ts_c(col0), ts_p(col0), ts_n0, ts_ok, lane);
                             else
                                 warp_rows_store<C::EPW>(stg, *reinterpret_cast<const float(*)[C::EPW]>(&acc[c0]), obase,
                                                         outp, col0, p.Ngemm, s2shift(col0), lane, tp.zf1, tp.zf2);
@@ -1148,7 +1165,7 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                                 for (int e = 0; e < C::EPW; ++e) f[e] = __uint_as_float(v[p0 + e]);
                                 const int col0 = n0 + half * HALF + c0 + p0;
                                 if (tp.tstore)
-                                    warp_rows_tstore<C::EPW>(stg, f, &tp.mapY, col0, ts_pix, ts_n0, ts_ok, lane);
+                                    warp_rows_tstore<C::EPW>(stg, f, &tp.mapY, ts_c(col0), ts_p(col0), ts_n0, ts_ok, lane);
                                 else
                                     warp_rows_store<C::EPW>(stg, f, obase, outp, col0, p.Ngemm, s2shift(col0), lane, tp.zf1,
                                                             tp.zf2);
