@@ -47,10 +47,11 @@ def parse():
     ap.add_argument("--epi", action="store_true",
                     help="fused epilogues (include/smconv_epi.h): fwd emits BatchNorm statistics, dX applies the "
                          "LeakyReLU backward and emits the BN-backward statistics (PAPER.md:52 block)")
-    ap.add_argument("--graph", default="off", choices=["auto", "on", "off"],
-                    help="replay the timed steps as one CUDA graph (auto: on at 1 GPU).  Measured: no gain at "
-                         "batch 4096/512 or VGG b128 (the GPU, not the host, bounds the step), and per-call "
-                         "event nodes inside a graph are less reliable, so the default stays eager")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay the timed steps as one CUDA graph, with programmatic dependent launch for every "
+                         "kernel.  auto: on at 1 GPU below 1024 images per GPU (measured r02bt: VGG-16 b128 TF32 "
+                         "0.79 -> 0.72 ms, 3xTF32 1.27 -> 1.24 ms, AlexNet b256 0.34 -> 0.28 ms: launch-bound small "
+                         "calls; ResNet-18 b4096 unchanged, so it stays eager there)")
     ap.add_argument("--dw-stream", default="auto", choices=["auto", "on", "off"],
                     help="run every dW on a second stream beside the dX chain (dp.ConvNetStep dw_stream); "
                          "measured r02aa/r02z: VGG-16 b128 -4..5 %%, ResNet-18 b512 -4.3 %%, b4096 -0.4 %% step "
@@ -266,11 +267,18 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
         pg = dist.group.WORLD
-    build.build()
-    sm.lib()
     if a.global_batch % world:
         raise SystemExit("global batch %d not divisible by %d ranks" % (a.global_batch, world))
     B = a.global_batch // world
+    use_graph = a.graph == "on" or (a.graph == "auto" and world == 1 and B < 1024)
+    # Programmatic dependent launch for every kernel when the step is a CUDA graph (launch.cuh: by default
+    # only the plain-TF32 plans use it).  Same-box A/B, VGG-16 b128 3xTF32 (r02bt): eager 1.27 ms, eager +
+    # PDL 1.34, graph 1.38, graph + PDL 1.24.  Set before the library's first launch reads SMCONV_PDL.
+    pdl_note = os.environ.get("SMCONV_PDL")
+    if use_graph and pdl_note is None:
+        os.environ["SMCONV_PDL"] = "2"
+    build.build()
+    sm.lib()
     dw_stream = a.dw_stream == "on" or (a.dw_stream == "auto" and B < 1024)
     # filters replicated (rank-independent seed); activations / loss gradients differ per shard
     step = dp.ConvNetStep(a.net, B, dev, math=a.math, seed=1, bucket_mb=a.bucket_mb, rank=rank, epi=a.epi,
@@ -311,7 +319,6 @@ def main():
     barrier()
     torch.cuda.synchronize()
     events = []
-    use_graph = a.graph == "on" or (a.graph == "auto" and world == 1)
     graph = None
     if use_graph:
         # the K timed steps captured as ONE CUDA graph (per-call timing events are event-record
@@ -431,6 +438,8 @@ def main():
                       "epilogue": ("fused: fwd + BN statistics, dX + LeakyReLU backward + BN-backward statistics"
                                    if a.epi else "none (plain conv outputs)"),
                       "cuda_graph": graph is not None, "dw_stream": dw_stream,
+                      "pdl": {"0": "off", "1": "plain-TF32 plans", "2": "all kernels"}.get(
+                          os.environ.get("SMCONV_PDL", "1"), os.environ.get("SMCONV_PDL")),
                       "parallelism": "dp%d" % world,
                       "dw_allreduce": ("fused in the dW kernels (NVLink multicast multimem.red)" if a.fused_allreduce
                                        else "NCCL all_reduce SUM, bucketed, async" if world > 1 else "none (1 GPU)"), "l2": "inputs larger than L2 (per-step working set "
