@@ -15,13 +15,17 @@ CASES = [  # (variant, op, dims)
     ("tma-pair", 0, (256, 4, 4, 128, 128, 3, 3, 1, 1, 1, 1)),
     ("tma-pair", 2, (64, 4, 4, 128, 256, 3, 3, 1, 1, 1, 1)),
     ("tma-ragged", 2, (32, 6, 6, 48, 112, 3, 3, 1, 1, 1, 1)),
+    ("tma-pair", 1, (256, 4, 4, 128, 128, 3, 3, 1, 1, 1, 1)),          # TMA-store epilogue, K-major dX filter
+    ("tma-zfill", 1, (64, 8, 8, 64, 128, 1, 1, 2, 2, 0, 0)),            # 1x1 s2 dX: zero phases from the epilogue
+    ("tma-s2dx", 1, (32, 32, 32, 64, 64, 3, 3, 2, 2, 1, 1)),            # super-pixel dX (automatic plan)
     ("strip", 0, (64, 8, 8, 64, 64, 3, 3, 1, 1, 1, 1)),
     ("strip", 1, (64, 8, 8, 64, 64, 3, 3, 1, 1, 1, 1)),
     ("dws", 2, (32, 8, 8, 64, 64, 3, 3, 1, 1, 1, 1)),
     ("direct", 0, (32, 8, 8, 4, 64, 3, 3, 1, 1, 1, 1)),
     ("generic", 1, (8, 8, 8, 4, 64, 3, 3, 1, 1, 1, 1)),
 ]
-VARIANT = {"tma": 2, "tma-csk": 0, "tma-pair": 0, "tma-ragged": 0, "strip": 3, "dws": 5, "direct": 4, "generic": 1}
+VARIANT = {"tma": 2, "tma-csk": 0, "tma-pair": 0, "tma-ragged": 0, "tma-zfill": 2, "tma-s2dx": 0, "strip": 3, "dws": 5,
+           "direct": 4, "generic": 1}
 
 
 def main():
@@ -44,9 +48,9 @@ def main():
                 sm.conv2d_bwd_data(dy, w, (IH, IW), (sh, sw), (ph, pw), math=math)
             else:
                 sm.conv2d_bwd_filter(x, dy, (FH, FW), (sh, sw), (ph, pw), math=math)
-            sm.force_variant(op, 0)
             torch.cuda.synchronize()
             print(name, op, math, sm.plan_describe(op, d, sm.MATH[math]), flush=True)
+            sm.force_variant(op, 0)
 
 
 if __name__ == "__main__":
