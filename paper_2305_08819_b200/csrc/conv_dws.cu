@@ -438,6 +438,288 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
     }
 }
 
+// ------------------------------------------------------------------ CTA-pair form (cta_group::2)
+// The 64-channel dW runs N = 64 MMAs, which a single CTA issues at ~60 % of the N = 128 rate, while a CTA
+// pair (M = 256) runs them at full rate (tools/pair_bench.cu: 894 vs 507 TFLOP/s TF32 at the power cap).
+// Here the two m-tiles of a group are the two CTAs of a cluster: CTA r converts m-tile r (taps 4g+2r,
+// 4g+2r+1) into its own TMEM and stages its half of the dY k-block (32 of the 64 output channels); CTA 0
+// issues ONE M = 256 MMA per k-step for both.  With one m-tile per CTA a TMEM A slot is 32 * PLANES
+// columns, so the converter -> MMA ring is 7 (3xTF32) / 8 (TF32) slots deep instead of 3 / 6 -- the
+// single-CTA pair attempt of round 1 (1.82 -> 2.53 ms) kept the shallow ring and stalled on the
+// cross-CTA hand-offs.  Group 2 (tap 8) leaves CTA 1's rows empty (1/9 of the work at a quarter of
+// the pair's rows).
+template <int PLANES, int OW>
+struct DwsPairCfg {
+    static constexpr int RB = 32 / OW, XW = OW + 2;
+    static constexpr int BN = 64;                   // OC (both CTAs)
+    static constexpr int Y_BYTES = 32 * 32 * 4;     // this CTA's dY half: [32 px][32 oc]
+    static constexpr int Y_OFF_LO = Y_BYTES;
+    static constexpr int ROW_BYTES = XW * 256;
+    static constexpr int XA_OFF = PLANES * Y_BYTES;
+    static constexpr int XA_BYTES = ROW_BYTES;
+    static constexpr int XB_OFF = XA_OFF + XA_BYTES;
+    static constexpr int XB_BYTES = RB * ROW_BYTES;
+    static constexpr int STAGE_BYTES = ((XB_OFF + XB_BYTES + 1023) / 1024) * 1024;
+    static constexpr int SS_RAW = (200 * 1024) / STAGE_BYTES;
+    static constexpr int SS = SS_RAW > 8 ? 8 : SS_RAW;
+    static constexpr int ACC_COLS = 64;             // this CTA's 128 rows x 64 fp32 columns, single buffer
+    static constexpr int SLOT_COLS = 32 * PLANES;   // one m-tile's A per k-block: hi 32 (| lo 32)
+    static constexpr int ST_RAW = (512 - ACC_COLS) / SLOT_COLS;
+    static constexpr int ST = ST_RAW > 8 ? 8 : ST_RAW;
+    static constexpr int NEPI = 8, TMA_W = 8, MMA_W = 9, CONV_W0 = 10, NCONV = 8;
+    static constexpr int NTHREADS = (10 + NCONV) * 32;
+    static constexpr int SMEM_BYTES = 1024 + SS * STAGE_BYTES + 1024;
+    static_assert(SS >= 2 && ST >= 2, "DWS pair pipeline does not fit");
+};
+
+template <int PLANES, int OW>
+__global__ void __launch_bounds__(DwsPairCfg<PLANES, OW>::NTHREADS, 1)
+    conv_dws_pair_kernel(const __grid_constant__ DwsParams dp, const __grid_constant__ GenParams p) {
+    using C = DwsPairCfg<PLANES, OW>;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    const uint32_t tiles_addr = (raw_addr + 1023u) & ~1023u;
+    uint8_t* tiles_ptr = smem_raw + (tiles_addr - raw_addr);
+    DwsAux* aux = reinterpret_cast<DwsAux*>(tiles_ptr + C::SS * C::STAGE_BYTES);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int CHK = PLANES == 2 ? dp.chunk_kb : (1 << 30);
+    const int rank = (int)cluster_ctarank();
+    const int wfirst = (int)(blockIdx.x >> 1), wstep = (int)(gridDim.x >> 1);
+
+    if (tid == 0) {
+        for (int s = 0; s < C::SS; ++s) {
+            mbar_init(&aux->full[s], 1);
+            mbar_init(&aux->empty[s], 1 + C::NCONV / 2);  // multicast MMA commit + the next k-block's 4 converter warps
+        }
+        for (int t = 0; t < C::ST; ++t) {
+            mbar_init(&aux->conv[t], C::NCONV);  // CTA 0's: one arrival per converter warp of a k-block, both CTAs
+            mbar_init(&aux->tfree[t], 1);
+        }
+        mbar_init(&aux->tfull, 1);
+        mbar_init(&aux->tempty, 2 * C::NEPI);  // CTA 0's: one arrival per epilogue warp of both CTAs
+        fence_mbar_init();
+    }
+    if (warp == C::TMA_W && lane == 0) {
+        prefetch_tmap(&dp.mapXA);
+        prefetch_tmap(&dp.mapXB);
+        prefetch_tmap(&dp.mapY);
+    }
+    if (warp == C::MMA_W) tmem_alloc2(&aux->tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();  // the peer's barriers exist before any remote arrival
+    tc_fence_after();
+    const uint32_t tmem = aux->tmem_base;
+    pdl_trigger();
+    pdl_wait();
+
+    if (warp == C::TMA_W) {
+        // ======================= TMA producer: this CTA's dY half + the activation slab, per k-block
+        int s = 0;
+        uint32_t r = 0;
+        for (int w = wfirst; w < dp.work; w += wstep) {
+            DwsItem it;
+            it.init(dp, w);
+            for (int kb = it.kb0; kb < it.kb1; ++kb) {
+                if (r > 0) mbar_wait(&aux->empty[s], (r - 1) & 1);
+                const int ncb = kb / dp.ohb, oh0 = (kb - ncb * dp.ohb) * dp.RB;
+                const int n = ncb / dp.cbs, cb = ncb - n * dp.cbs, ow0 = cb * 32;
+                const int ih0 = oh0 + it.fh_lo - dp.ph;
+                const bool fresh = (kb == it.kb0) || (oh0 == 0);
+                const uint32_t sY = tiles_addr + s * C::STAGE_BYTES;
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(&aux->full[s], C::Y_BYTES + C::XB_BYTES + (fresh ? C::XA_BYTES : 0));
+                    tma_load_5d(sY, &dp.mapY, &aux->full[s], 0, ow0, oh0, n, rank);  // oc block `rank`
+                    tma_load_4d(sY + C::XB_OFF, &dp.mapXB, &aux->full[s], 0, ow0 - dp.pw, ih0 + 1, n);
+                    if (fresh) tma_load_4d(sY + C::XA_OFF, &dp.mapXA, &aux->full[s], 0, ow0 - dp.pw, ih0, n);
+                }
+                __syncwarp();
+                if (++s == C::SS) {
+                    s = 0;
+                    ++r;
+                }
+            }
+        }
+    } else if (warp == C::MMA_W) {
+        // ======================= MMA issuer (CTA 0): 4 k-steps x (3 | 1) M = 256 MMAs per k-block
+        if (rank == 0) {
+            constexpr uint32_t IDESC = idesc_tf32(256, C::BN, false, true);  // A from TMEM, B (dY) MN-major
+            const uint64_t bd0 = make_sdesc(tiles_addr, 4096u, 512u, kLayoutSW128Base32);
+            constexpr uint64_t B_LO = C::Y_BYTES >> 4;
+            uint32_t q = 0, c = 0;
+            int in_chunk = 0;
+            for (int w = wfirst; w < dp.work; w += wstep) {
+                DwsItem it;
+                it.init(dp, w);
+                const int nkb = it.kb1 - it.kb0;
+                for (int i = 0; i < nkb; ++i, ++q) {
+                    const uint32_t s = q % C::SS, t = q % C::ST, rt = q / C::ST;
+                    if (in_chunk == 0 && c >= 1) {
+                        mbar_wait(&aux->tempty, (c - 1) & 1);  // both CTAs' epilogues drained the previous chunk
+                        tc_fence_after();
+                    }
+                    const bool last = (in_chunk + 1 == CHK || i == nkb - 1);
+                    mbar_wait(&aux->conv[t], rt & 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint64_t so = (uint64_t)(s * C::STAGE_BYTES) >> 4;
+#pragma unroll
+                        for (int g4 = 0; g4 < 4; ++g4) {
+                            const uint64_t bdH = bd0 + so + g4 * 64;  // 8 K-rows x 128 B
+                            const uint32_t acc0 = (in_chunk > 0 || g4 > 0) ? 1u : 0u;
+                            const uint32_t ahi = tmem + (uint32_t)(C::ACC_COLS + t * C::SLOT_COLS + g4 * 8);
+                            if (PLANES == 2) {
+                                mma2_tf32_ts(tmem, ahi + 32, bdH, IDESC, acc0);  // a_lo * b_hi
+                                mma2_tf32_ts(tmem, ahi, bdH + B_LO, IDESC, 1u);  // a_hi * b_lo
+                                mma2_tf32_ts(tmem, ahi, bdH, IDESC, 1u);         // a_hi * b_hi
+                            } else {
+                                mma2_tf32_ts(tmem, ahi, bdH, IDESC, acc0);
+                            }
+                        }
+                        mma2_commit_both(&aux->empty[s]);
+                        mma2_commit_both(&aux->tfree[t]);
+                        if (last) mma2_commit_both(&aux->tfull);
+                    }
+                    __syncwarp();
+                    if (last) {
+                        ++c;
+                        in_chunk = 0;
+                    } else {
+                        ++in_chunk;
+                    }
+                }
+            }
+        }
+    } else if (warp >= C::CONV_W0) {
+        // ======================= converters: this CTA's m-tile (taps 4g+2r, 4g+2r+1) -> TMEM; dY half -> b_lo.
+        // Two groups of 4 warps take alternate k-blocks (warp = one TMEM lane quadrant, all 32 pixels of the
+        // k-block): the per-k-block chain LDS -> split -> tcgen05.st -> wait -> arrive bounded the pair at one
+        // k-block per chain latency with all 8 warps on the same k-block (r02bw: 0.49 us per k-block)
+        const int grp = (warp - C::CONV_W0) >> 2;
+        const int ct4 = tid - (C::CONV_W0 + 4 * grp) * 32;  // 0..127 within the group
+        const int qd = warp & 3;
+        const int ts = qd >> 1, icb = qd & 1;
+        uint32_t q = 0;
+        for (int w = wfirst; w < dp.work; w += wstep) {
+            DwsItem it;
+            it.init(dp, w);
+            const int nkb = it.kb1 - it.kb0;
+            const int tap = 4 * it.g + 2 * rank + ts;
+            const int fh = tap / 3, fw = tap - 3 * fh;
+            for (int i = 0; i < nkb; ++i, ++q) {
+                if ((int)(q & 1u) != grp) continue;
+                const uint32_t s = q % C::SS, rs = q / C::SS, t = q % C::ST, rt = q / C::ST;
+                const uint32_t sp = (s + C::SS - 1) % C::SS;
+                const int kb = it.kb0 + i;
+                const bool fresh = (i == 0) || (kb % dp.ohb == 0);
+                mbar_wait(&aux->full[s], rs & 1);
+                // slab row 0 comes from the previous k-block's stage, whose TMA the OTHER group waited for: wait
+                // for it here too (it cannot be refilled before this group's arrival on empty[sp] below)
+                if (!fresh) mbar_wait(&aux->full[sp], ((q - 1) / C::SS) & 1);
+                uint8_t* st = tiles_ptr + s * C::STAGE_BYTES;
+                if (PLANES == 2) {  // b_lo of this CTA's dY half (4 KB: two float4 per thread of the group)
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) {
+                        const float4 v = reinterpret_cast<const float4*>(st)[ct4 + 128 * e2];
+                        float4 o;
+                        o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                        o.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                        o.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                        o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                        reinterpret_cast<float4*>(st + C::Y_OFF_LO)[ct4 + 128 * e2] = o;
+                    }
+                }
+                const uint8_t* row0 = fresh ? st + C::XA_OFF
+                                            : tiles_ptr + sp * C::STAGE_BYTES + C::XB_OFF + (C::RB - 1) * C::ROW_BYTES;
+                const uint8_t* row1 = st + C::XB_OFF;
+                if (rt > 0) mbar_wait(&aux->tfree[t], (rt - 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {  // pixels 16h .. 16h+15 of the k-block
+                    uint32_t hi[16], lo[16];
+                    const int bsr = tap < kDwsTaps ? fh - it.fh_lo + (16 * h) / OW : -1;
+                    const int coff = (fw + (16 * h) % OW) * 256 + icb * 128 + lane * 4;
+                    if (bsr >= 0) {
+                        const uint8_t* p0 = (bsr == 0 ? row0 : row1 + (bsr - 1) * C::ROW_BYTES) + coff;
+                        const uint8_t* p1 = row1 + bsr * C::ROW_BYTES + coff;
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) {
+                            const float e = (k / OW == 0) ? *reinterpret_cast<const float*>(p0 + (k % OW) * 256)
+                                                          : *reinterpret_cast<const float*>(
+                                                                p1 + (k / OW - 1) * C::ROW_BYTES + (k % OW) * 256);
+                            if (PLANES == 2) {
+                                const uint32_t hb = __float_as_uint(e) & 0xFFFFE000u;
+                                hi[k] = hb;
+                                lo[k] = __float_as_uint(e - __uint_as_float(hb));
+                            } else {
+                                hi[k] = __float_as_uint(e);
+                                lo[k] = 0u;
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) hi[k] = lo[k] = 0u;  // taps 9..11 of group 2: empty rows
+                    }
+                    const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(C::ACC_COLS + t * C::SLOT_COLS + h * 16);
+                    tmem_st_32x32b_x16(ta, hi);
+                    if (PLANES == 2) tmem_st_32x32b_x16(ta + 32, lo);
+                }
+                tmem_st_wait();
+                fence_proxy_async_smem();  // b_lo before the release
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(&aux->conv[t], 0);  // on CTA 0's barrier (it issues the MMAs)
+                if (lane == 0 && q > 0) mbar_arrive(&aux->empty[sp]);  // previous stage: its row RB was read
+            }
+        }
+    } else {
+        // ======================= epilogue warps 0-7: promote chunks, write this CTA's m-tile partial
+        const int qd = warp & 3, half = warp >> 2;
+        const uint32_t lane_addr = (uint32_t)(qd * 32) << 16;
+        const int M = kDwsTaps * 64;
+        uint32_t c = 0;
+        for (int w = wfirst; w < dp.work; w += wstep) {
+            DwsItem it;
+            it.init(dp, w);
+            const int nkb = it.kb1 - it.kb0;
+            const int nch = nkb > 0 ? (nkb + CHK - 1) / CHK : 0;
+            float acc[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+            for (int k = 0; k < nch; ++k, ++c) {
+                mbar_wait(&aux->tfull, c & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int c0 = 0; c0 < 32; c0 += 16) {
+                    uint32_t v[16];
+                    tmem_ld_32x32b_x16(tmem + lane_addr + (uint32_t)(half * 32 + c0), v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(&aux->tempty, 0);
+            }
+            float* outp = p.out + (long long)it.split * p.split_stride;
+            const int tap = 4 * it.g + 2 * rank + (qd >> 1);
+            if (tap < kDwsTaps) {
+                float* o = outp + tap * 64 + (qd & 1) * 32 + lane + (long long)(half * 32) * M;
+#pragma unroll
+                for (int e = 0; e < 32; ++e) o[(long long)e * M] = acc[e];
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();  // the peer's MMAs / arrivals are done before TMEM is released
+    if (warp == C::MMA_W) {
+        tc_fence_after();
+        tmem_dealloc2(tmem, 512);
+    }
+}
+
 namespace {
 
 const int g_knob_chunk_d = getenv("SMCONV_TMA_CHUNK") ? atoi(getenv("SMCONV_TMA_CHUNK")) : 8;
@@ -472,6 +754,38 @@ int launch_t(const DwsParams& dp, const GenParams& g, cudaStream_t st, char* err
 
 }  // namespace
 
+template <int PLANES, int OW>
+int launch_pair_t(const DwsParams& dp, const GenParams& g, cudaStream_t st, char* err, size_t errlen) {
+    using C = DwsPairCfg<PLANES, OW>;
+    static std::atomic<unsigned long long> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_done.load() & bit)) {
+        if (cudaFuncSetAttribute(conv_dws_pair_kernel<PLANES, OW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::SMEM_BYTES) != cudaSuccess) {
+            snprintf(err, errlen, "cudaFuncSetAttribute(dws pair smem=%d): %s", C::SMEM_BYTES,
+                     cudaGetErrorString(cudaGetLastError()));
+            return CONV_ECUDA;
+        }
+        attr_done.fetch_or(bit);
+    }
+    const int pairs = dp.work < 74 ? dp.work : 74;
+    const cudaError_t e = launch_k(conv_dws_pair_kernel<PLANES, OW>, dim3(2 * pairs), dim3(C::NTHREADS), C::SMEM_BYTES,
+                                   st, 2, dp, g);
+    if (e != cudaSuccess) {
+        snprintf(err, errlen, "cudaLaunchKernelEx(dws pair): %s", cudaGetErrorString(e));
+        return CONV_ECUDA;
+    }
+    return CONV_OK;
+}
+
+// SMCONV_DWS_PAIR=0: the single-CTA DWS kernel (A/B)
+int dws_pair_mode() {
+    static const int m = getenv("SMCONV_DWS_PAIR") ? atoi(getenv("SMCONV_DWS_PAIR")) : 0;
+    return m;
+}
+
 bool dws_supported(int op, int IC, int OC, int FH, int FW, int sh, int sw, int OH, int OW) {
     if (op != CONV_OP_BWD_FILTER) return false;
     if (IC != 64 || OC != 64 || FH != 3 || FW != 3 || sh != 1 || sw != 1) return false;
@@ -483,15 +797,16 @@ bool dws_supported(int op, int IC, int OC, int FH, int FW, int sh, int sw, int O
 // number of work items (3 groups per split) that fills whole rounds of the 148-CTA persistent grid,
 // at least 4 rounds: with 300 items (2.03 rounds) two thirds of the CTAs idled through the last one.
 int dws_splits(int N, int OH, int OW, int* kb_per_split) {
+    const long long ctas = dws_pair_mode() ? 74 : 148;  // work items are per CTA, or per CTA pair
     const int RB = OW >= 32 ? 1 : 32 / OW;
     const long long kb_total = (long long)N * (OH / RB) * (OW >= 32 ? OW / 32 : 1);
     const long long need = (kb_total + 255) / 256;
     // at least min_rounds waves of (3 x splits) CTAs; 4 cost the small batches a 196-split workspace
     // round trip: VGG b128 vgg2 dW 101 us at 4, 77 us at 2, 64.5 us at 1 (r02z); b4096 needs 11 anyway
     static const int min_rounds = getenv("SMCONV_DWS_MIN_ROUNDS") ? atoi(getenv("SMCONV_DWS_MIN_ROUNDS")) : 1;
-    long long rounds = (3 * need + 147) / 148;
+    long long rounds = (3 * need + ctas - 1) / ctas;
     if (rounds < min_rounds) rounds = min_rounds;
-    long long smax = rounds * 148 / 3;
+    long long smax = rounds * ctas / 3;
     if (smax > kb_total) smax = kb_total;
     if (smax < 1) smax = 1;
     const long long kps = (kb_total + smax - 1) / smax;
@@ -524,11 +839,22 @@ int dws_launch(int planes, const GenParams& g, int splits, int kb_per_split, cud
     bool ok = tma_encode_f32(&dp.mapXA, g.B, 4, dx, sx, bxa, CU_TENSOR_MAP_SWIZZLE_NONE);
     ok &= tma_encode_f32(&dp.mapXB, g.B, 4, dx, sx, bxb, CU_TENSOR_MAP_SWIZZLE_NONE);
     uint64_t dy[5] = {32, OW, OH, N, OC / 32}, sy[4] = {OC * 4, OW * OC * 4, OH * OW * OC * 4, 128};
-    uint32_t by[5] = {32, (uint32_t)wow, (uint32_t)dp.RB, 1, (uint32_t)(OC / 32)};
+    const bool pair = dws_pair_mode() != 0;
+    uint32_t by[5] = {32, (uint32_t)wow, (uint32_t)dp.RB, 1, (uint32_t)(pair ? 1 : OC / 32)};  // pair: one oc block per CTA
     ok &= tma_encode_f32(&dp.mapY, g.A, 5, dy, sy, by, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     if (!ok) {
         snprintf(err, errlen, "dws: cuTensorMapEncodeTiled failed");
         return CONV_ECUDA;
+    }
+    if (pair) {
+        if (planes == 2) {
+            if (g.OW >= 32) return launch_pair_t<2, 32>(dp, g, st, err, errlen);
+            if (g.OW == 16) return launch_pair_t<2, 16>(dp, g, st, err, errlen);
+            return launch_pair_t<2, 8>(dp, g, st, err, errlen);
+        }
+        if (g.OW >= 32) return launch_pair_t<1, 32>(dp, g, st, err, errlen);
+        if (g.OW == 16) return launch_pair_t<1, 16>(dp, g, st, err, errlen);
+        return launch_pair_t<1, 8>(dp, g, st, err, errlen);
     }
     if (planes == 2 && g_dws_hyb) {
         if (g.OW >= 32) return launch_t<2, 32, true>(dp, g, st, err, errlen);

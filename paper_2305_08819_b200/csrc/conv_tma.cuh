@@ -1071,7 +1071,6 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
                 bool stored = false;
                 if constexpr (C::EPW > 0) {
                     if (coal) {
-#pragma unroll
                         if (p.epi.mode != EPI_NONE) {  // in place on acc, 16 columns at a time
 #pragma unroll
                             for (int c0 = 0; c0 < HALF; c0 += 16) {

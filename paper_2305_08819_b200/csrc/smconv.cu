@@ -30,6 +30,7 @@ int tma_set_pair(int on);
 int tma_get_pair();
 bool dws_supported(int op, int IC, int OC, int FH, int FW, int sh, int sw, int OH, int OW);
 int dws_splits(int N, int OH, int OW, int* kb_per_split);
+int dws_pair_mode();
 int dws_launch(int planes, const GenParams& g, int splits, int kb_per_split, cudaStream_t st, char* err,
                size_t errlen);
 bool stem_supported(int op, int IC, int OC, int FH, int FW);
@@ -1289,7 +1290,8 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
                  : pl.variant == CONV_VARIANT_TMA   ? "tma"
                                                     : "generic",
                  ((pl.variant == CONV_VARIANT_TMA && pl.tp.pair) ||
-                  (pl.variant == CONV_VARIANT_STRIP && strip_pair(op, N, pl.BN, pl.planes)))
+                  (pl.variant == CONV_VARIANT_STRIP && strip_pair(op, N, pl.BN, pl.planes)) ||
+                  (pl.variant == CONV_VARIANT_DWS && dws_pair_mode()))
                      ? " pair=2cta"
                      : "", pl.gp.csk ? " csk" : "",
                  (pl.variant == CONV_VARIANT_TMA && pl.planes == 2 && op != CONV_OP_BWD_FILTER && !pl.gp.hyb) ? " 3mma"
