@@ -56,6 +56,7 @@ struct __align__(64) DwsParams {
                           // per output row; k-block = (image, column block, output row), rows innermost
     int kb_total, kb_per_split, splits, work, chunk_kb;
     int ph, pw;
+    int alt_conv;  // converter warps in two groups on alternate k-blocks (one-CTA kernel, not the hybrid form)
 };
 
 constexpr int kDwsGroups = 3;  // taps {0..3}, {4..7}, {8}
@@ -130,13 +131,14 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
     if (tid == 0) {
         for (int s = 0; s < C::SS; ++s) {
             mbar_init(&aux->full[s], 1);
-            mbar_init(&aux->empty[s], 1 + C::NCONV);  // MMA commit + next k-block's converter warps
+            // MMA commit + next k-block's converter warps (DwsParams::alt_conv: one group of NCONV / 2)
+            mbar_init(&aux->empty[s], 1 + (dp.alt_conv ? C::NCONV / 2 : C::NCONV));
         }
         for (int t = 0; t < C::ST; ++t) {
             // one barrier per (slot, m-tile): the MMAs of m-tile 0 start while m-tile 1 is being split;
             // one elected arrival per converter warp
-            mbar_init(&aux->conv[2 * t], C::NCONV);
-            mbar_init(&aux->conv[2 * t + 1], C::NCONV);
+            mbar_init(&aux->conv[2 * t], dp.alt_conv ? C::NCONV / 2 : C::NCONV);
+            mbar_init(&aux->conv[2 * t + 1], dp.alt_conv ? C::NCONV / 2 : C::NCONV);
             mbar_init(&aux->tfree[t], 1);
         }
         mbar_init(&aux->tfull, 1);
@@ -255,6 +257,125 @@ __global__ void __launch_bounds__(DwsCfg<PLANES, OW>::NTHREADS, 1)
                 } else {
                     ++in_chunk;
                 }
+            }
+        }
+    } else if (warp >= C::CONV_W0 && dp.alt_conv) {
+        // ======================= converters, two groups of 4 warps on alternate k-blocks (DwsParams::alt_conv):
+        // a warp = one TMEM lane quadrant, both K halves of both m-tiles of its k-block.  With all 8 warps on
+        // every k-block the per-k-block chain LDS -> split -> tcgen05.st -> wait -> arrive ran one k-block at a
+        // time (the pair kernel: 2.59 -> 2.02 ms with the groups, r02bx)
+        const int grp = (warp - C::CONV_W0) >> 2;
+        const int ct4 = tid - (C::CONV_W0 + 4 * grp) * 32;  // 0..127 within the group
+        const int qd = warp & 3;
+        const int ts = qd >> 1, icb = qd & 1;
+        uint32_t q = 0;
+        for (int w = blockIdx.x; w < dp.work; w += gridDim.x) {
+            DwsItem it;
+            it.init(dp, w);
+            const int nkb = it.kb1 - it.kb0;
+            for (int i = 0; i < nkb; ++i, ++q) {
+                if ((int)(q & 1u) != grp) continue;
+                const uint32_t s = q % C::SS, rs = q / C::SS, t = q % C::ST, rt = q / C::ST;
+                const uint32_t sp = (s + C::SS - 1) % C::SS;
+                const int kb = it.kb0 + i;
+                const bool fresh = (i == 0) || (kb % dp.ohb == 0);
+                mbar_wait(&aux->full[s], rs & 1);
+                // slab row 0 of a non-fresh k-block is the previous stage's last row, loaded for the OTHER group
+                if (!fresh) mbar_wait(&aux->full[sp], ((q - 1) / C::SS) & 1);
+                uint8_t* st = tiles_ptr + s * C::STAGE_BYTES;
+                if (PLANES == 2 && HYB) {  // B' = [bf16(b_lo) ; bf16(b)] MN-major plane from the dY k-block
+#pragma unroll
+                    for (int e2 = 0; e2 < 4; ++e2) {
+                        const uint32_t i = (uint32_t)(ct4 + 128 * e2);
+                        const uint32_t k = (i & 255u) >> 3, c32 = (i & 7u) >> 1;
+                        const uint32_t mn = (i >> 8) * 32u + ((c32 ^ (k & 3u)) << 3) + ((i & 1u) << 2);
+                        const float4 b = reinterpret_cast<const float4*>(st)[i];
+                        const float l0 = b.x - __uint_as_float(__float_as_uint(b.x) & 0xFFFFE000u);
+                        const float l1 = b.y - __uint_as_float(__float_as_uint(b.y) & 0xFFFFE000u);
+                        const float l2 = b.z - __uint_as_float(__float_as_uint(b.z) & 0xFFFFE000u);
+                        const float l3 = b.w - __uint_as_float(__float_as_uint(b.w) & 0xFFFFE000u);
+                        *reinterpret_cast<uint2*>(st + C::Y_OFF_LO + mnmaj16_off(k, mn)) =
+                            make_uint2(pack_bf16x2(l0, l1), pack_bf16x2(l2, l3));
+                        *reinterpret_cast<uint2*>(st + C::Y_OFF_LO + mnmaj16_off(k + 32u, mn)) =
+                            make_uint2(pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+                    }
+                } else if (PLANES == 2) {  // b_lo of the dY k-block (8 KB: four float4 per thread of the group)
+#pragma unroll
+                    for (int e2 = 0; e2 < 4; ++e2) {
+                        const float4 v = reinterpret_cast<const float4*>(st)[ct4 + 128 * e2];
+                        float4 o;
+                        o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                        o.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                        o.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                        o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                        reinterpret_cast<float4*>(st + C::Y_OFF_LO)[ct4 + 128 * e2] = o;
+                    }
+                }
+                const uint8_t* row0 = fresh ? st + C::XA_OFF
+                                            : tiles_ptr + sp * C::STAGE_BYTES + C::XB_OFF + (C::RB - 1) * C::ROW_BYTES;
+                const uint8_t* row1 = st + C::XB_OFF;
+                if (rt > 0) mbar_wait(&aux->tfree[t], (rt - 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    if (j < it.ntile) {
+                        const int tap = 4 * it.g + 2 * j + ts;
+                        const int fh = tap / 3, fw = tap - 3 * fh;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            uint32_t hi[16], lo[16];
+                            float ev[16];
+                            const int bsr = tap < kDwsTaps ? fh - it.fh_lo + (16 * h) / OW : -1;
+                            const int coff = (fw + (16 * h) % OW) * 256 + icb * 128 + lane * 4;
+                            if (bsr >= 0) {
+                                const uint8_t* p0 = (bsr == 0 ? row0 : row1 + (bsr - 1) * C::ROW_BYTES) + coff;
+                                const uint8_t* p1 = row1 + bsr * C::ROW_BYTES + coff;
+#pragma unroll
+                                for (int k = 0; k < 16; ++k) {
+                                    const float e = (k / OW == 0)
+                                                        ? *reinterpret_cast<const float*>(p0 + (k % OW) * 256)
+                                                        : *reinterpret_cast<const float*>(
+                                                              p1 + (k / OW - 1) * C::ROW_BYTES + (k % OW) * 256);
+                                    ev[k] = e;
+                                    if (PLANES == 2) {
+                                        const uint32_t hb = __float_as_uint(e) & 0xFFFFE000u;
+                                        hi[k] = hb;
+                                        lo[k] = __float_as_uint(e - __uint_as_float(hb));
+                                    } else {
+                                        hi[k] = __float_as_uint(e);
+                                        lo[k] = 0u;
+                                    }
+                                }
+                            } else {
+#pragma unroll
+                                for (int k = 0; k < 16; ++k) {  // half-empty last m-tile
+                                    hi[k] = lo[k] = 0u;
+                                    ev[k] = 0.f;
+                                }
+                            }
+                            const uint32_t tb = tmem + ((uint32_t)(qd * 32) << 16) +
+                                                (uint32_t)(C::ACC_COLS + t * C::SLOT_COLS + j * C::TILE_COLS);
+                            if (PLANES == 2 && HYB) {
+                                // slot columns [0,32) a_hi, [32,48) bf16(a_hi) pairs, [48,64) bf16(a_lo) pairs
+                                uint32_t xh[8], xl[8];
+                                split_a16(ev, hi, xh, xl);
+                                tmem_st_32x32b_x16(tb + h * 16, hi);
+                                tmem_st_32x32b_x8(tb + 32 + h * 8, xh);
+                                tmem_st_32x32b_x8(tb + 48 + h * 8, xl);
+                            } else {
+                                tmem_st_32x32b_x16(tb + h * 16, hi);
+                                if (PLANES == 2) tmem_st_32x32b_x16(tb + 32 + h * 16, lo);
+                            }
+                        }
+                        tmem_st_wait();
+                    }
+                    if (j == 0) fence_proxy_async_smem();  // b_lo (written above) before the first release
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&aux->conv[2 * t + j]);  // per warp; also for empty m-tiles
+                }
+                __syncwarp();
+                if (lane == 0 && q > 0) mbar_arrive(&aux->empty[sp]);  // previous stage: its row RB was read
             }
         }
     } else if (warp >= C::CONV_W0) {
@@ -725,6 +846,8 @@ namespace {
 const int g_knob_chunk_d = getenv("SMCONV_TMA_CHUNK") ? atoi(getenv("SMCONV_TMA_CHUNK")) : 8;
 
 const int g_dws_hyb = getenv("SMCONV_DWS_HYB") ? atoi(getenv("SMCONV_DWS_HYB")) : 0;
+// SMCONV_DWS_ALT=0: all 8 converter warps on every k-block (DwsParams::alt_conv)
+const int g_dws_alt = getenv("SMCONV_DWS_ALT") ? atoi(getenv("SMCONV_DWS_ALT")) : 1;
 
 template <int PLANES, int OW, bool HYB>
 int launch_t(const DwsParams& dp, const GenParams& g, cudaStream_t st, char* err, size_t errlen) {
@@ -829,6 +952,7 @@ int dws_launch(int planes, const GenParams& g, int splits, int kb_per_split, cud
     dp.splits = splits;
     dp.work = splits * kDwsGroups;
     dp.chunk_kb = g_knob_chunk_d > 0 ? g_knob_chunk_d : 8;
+    dp.alt_conv = g_dws_alt;
     dp.ph = g.ph;
     dp.pw = g.pw;
     const uint64_t N = g.N, IH = g.IH, IW = g.IW, IC = g.IC, OC = g.OC, OH = g.OH, OW = g.OW;
