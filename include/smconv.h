@@ -50,12 +50,13 @@
  *                          STRIP / DWS variants; a_hi = rna_tf32(a), a_lo = rna_tf32(a - a_hi) on the
  *                          GENERIC variant.  The a_lo*b_lo term (~2^-22 relative) is dropped.
  *                          Products per k-step:
- *                          - dW on the DWS / STEM / GENERIC variants, the transposed-GEMM dW (OC <= 64)
+ *                          - dW on the STEM / GENERIC variants, the transposed-GEMM dW (OC <= 64)
  *                            and every op on the GENERIC variant: three TF32 MMAs,
  *                            a_lo*b_hi + a_hi*b_lo + a_hi*b_hi (strict 3xTF32);
  *                          - fwd / dX on the TMA and STRIP variants (the default for 32x-channel
- *                            layers) and dW on the TMA variant (OC > 64; SMCONV_DW_HYB=0 restores
- *                            three TF32 MMAs there): one TF32 MMA a_hi*b_hi plus ONE bf16 MMA of doubled K computing
+ *                            layers) and dW on the TMA (OC > 64) and DWS variants (SMCONV_DW_HYB=0 /
+ *                            SMCONV_DWS_HYB=0 restore three TF32 MMAs there; plan text "hybw"):
+ *                            one TF32 MMA a_hi*b_hi plus ONE bf16 MMA of doubled K computing
  *                            [bf16(a_hi) | bf16(a_lo)] . [bf16(b_lo) | bf16(b)] = the two cross terms
  *                            (+ a_lo*b_lo) with each cross term rounded to bf16 (<= 2^-9 relative on a
  *                            term <= 2^-10 of |a||b|, i.e. ~2^-19 of |a||b| per product, random sign),

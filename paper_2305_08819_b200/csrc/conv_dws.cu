@@ -845,7 +845,11 @@ namespace {
 
 const int g_knob_chunk_d = getenv("SMCONV_TMA_CHUNK") ? atoi(getenv("SMCONV_TMA_CHUNK")) : 8;
 
-const int g_dws_hyb = getenv("SMCONV_DWS_HYB") ? atoi(getenv("SMCONV_DWS_HYB")) : 0;
+// bf16 cross terms (the hybrid 3xTF32 form) for the DWS dW; SMCONV_DWS_HYB=0: three TF32 MMAs.  With the
+// alternate-k-block converters it wins in the power-capped step (r02cb: l1.0a dW 1722 -> 1637 us isolated,
+// 6.50 -> 6.11 pJ / flop, ResNet-18 b4096 step -0.2..1.3 ms in three same-box pairs); without them it lost
+// (converter-bound, r02bj)
+const int g_dws_hyb = getenv("SMCONV_DWS_HYB") ? atoi(getenv("SMCONV_DWS_HYB")) : 1;
 // SMCONV_DWS_ALT=0: all 8 converter warps on every k-block (DwsParams::alt_conv)
 const int g_dws_alt = getenv("SMCONV_DWS_ALT") ? atoi(getenv("SMCONV_DWS_ALT")) : 1;
 
@@ -902,6 +906,8 @@ int launch_pair_t(const DwsParams& dp, const GenParams& g, cudaStream_t st, char
     }
     return CONV_OK;
 }
+
+int dws_hyb_mode() { return g_dws_hyb; }
 
 // SMCONV_DWS_PAIR=0: the single-CTA DWS kernel (A/B)
 int dws_pair_mode() {

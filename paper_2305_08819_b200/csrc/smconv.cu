@@ -31,6 +31,7 @@ int tma_get_pair();
 bool dws_supported(int op, int IC, int OC, int FH, int FW, int sh, int sw, int OH, int OW);
 int dws_splits(int N, int OH, int OW, int* kb_per_split);
 int dws_pair_mode();
+int dws_hyb_mode();
 int dws_launch(int planes, const GenParams& g, int splits, int kb_per_split, cudaStream_t st, char* err,
                size_t errlen);
 bool stem_supported(int op, int IC, int OC, int FH, int FW);
@@ -1297,7 +1298,8 @@ int conv2d_plan_describe(int op, int N, int IH, int IW, int IC, int OC, int FH, 
                  (pl.variant == CONV_VARIANT_TMA && pl.planes == 2 && op != CONV_OP_BWD_FILTER && !pl.gp.hyb) ? " 3mma"
                                                                                                               : "",
                  (pl.variant == CONV_VARIANT_TMA && pl.tp.zf1) ? " zfill"
-                 : (pl.variant == CONV_VARIANT_TMA && pl.tp.dw_hyb) ? " hybw" : "",
+                 : ((pl.variant == CONV_VARIANT_TMA && pl.tp.dw_hyb) ||
+                    (pl.variant == CONV_VARIANT_DWS && pl.planes == 2 && dws_hyb_mode())) ? " hybw" : "",
                  pl.BN, pl.planes, pl.splits, pl.grid.x,
                  pl.grid.y, pl.grid.z, pl.ws_bytes, plan_kernel_count(pl));
     return CONV_OK;
