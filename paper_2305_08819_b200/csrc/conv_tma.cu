@@ -25,6 +25,9 @@ const int g_knob_promo = env_int("SMCONV_TMA_L2PROMO", 3);
 const int g_knob_chunk = env_int("SMCONV_TMA_CHUNK", 8);
 // SMCONV_COALESCE=0: fwd / dX epilogue stores straight from the TMEM lanes (A/B experiments)
 const int g_knob_coalesce = env_int("SMCONV_COALESCE", 1);
+// 3xTF32 converter warps in two groups on alternate k-blocks (TmaParams::alt_conv; SMCONV_TMA_ALT=0: all 8 warps
+// on every k-block).  r02cc: isolated l2-l4 dX -5..7 %, dW -2..7 %; ResNet-18 b4096 step -1.0 ms (three pairs)
+const int g_knob_alt_conv = env_int("SMCONV_TMA_ALT", 1);
 // SMCONV_TSTORE=0: the row-coalesced fwd / dX epilogue stores per thread instead of by TMA (A/B)
 const int g_knob_tstore = env_int("SMCONV_TSTORE", 1);
 const int g_knob_tstore_s2 = env_int("SMCONV_TSTORE_S2DX", 1);  // ... for the super-pixel dX too
@@ -197,6 +200,7 @@ int tma_make_plan(int op, GenParams& g, int& BN, int planes, TmaParams& tp, dim3
     if (g_knob_G == 32) tp.G = 32;
     tp.chunk_kb = g_knob_chunk > 0 ? g_knob_chunk : 8;
     tp.coalesce = g_knob_coalesce;
+    tp.alt_conv = planes == 2 ? g_knob_alt_conv : 0;
     tp.dw_hyb = (op == CONV_OP_BWD_FILTER && !g.dwt && planes == 2) ? g_knob_dw_hyb : 0;
     if (planes == 2 && BN > 128) {
         snprintf(err, errlen, "tma plan: BN %d > 128 in 3xTF32", BN);

@@ -79,6 +79,7 @@ struct __align__(64) TmaParams {
     // SWIZZLE_128B, instead of the MN-major 32-B-atom view of W
     int dx_bk;
     int dw_hyb;  // dW cross terms in bf16 (TmaCfg::HYBW)
+    int alt_conv;  // 3xTF32 converter warps in two groups on alternate k-blocks
     // fwd / dX: the row-coalesced epilogue's pieces leave by TMA tensor store (cp.async.bulk.tensor) from
     // the warp's staging slice instead of LDS + SHFL + STG per thread: mapY views the output as
     // (C, pixels, N), box (EPW, 1, 32 images); the staging slice already holds the TMA's 64B / 128B
@@ -513,7 +514,10 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             mbar_init(&aux->empty[s], 1);
         }
         for (int t = 0; t < C::NT; ++t) {
-            mbar_init(&aux->conv[t], PAIR ? 2 * C::NCONV : C::NCONV * 32);
+            // per-warp arrivals of both CTAs (pairs) / per-thread arrivals; TmaParams::alt_conv: one group of
+            // NCONV / 2 warps per k-block
+            const int nconv = tp.alt_conv ? C::NCONV / 2 : C::NCONV;
+            mbar_init(&aux->conv[t], PAIR ? 2 * nconv : nconv * 32);
             mbar_init(&aux->tfree[t], 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -805,6 +809,117 @@ __global__ void __launch_bounds__(TmaCfg<OP, BN, PLANES, PAIR>::NTHREADS, 1)
             }
         }
         __syncwarp();
+    } else if (warp >= C::CONV_W0 && tp.alt_conv) {
+        // ======================= 3xTF32 converters in two groups of 4 warps on alternate k-blocks
+        // (TmaParams::alt_conv): a warp = one TMEM lane quadrant, both K halves.  With all 8 warps on every
+        // k-block the chain LDS -> split -> tcgen05.st -> wait -> arrive ran one k-block at a time (the same
+        // split made the DWS dW converters 18 % faster in TF32, r02ca)
+        const int grp = (warp - C::CONV_W0) >> 2;
+        const int ct4 = tid - (C::CONV_W0 + 4 * grp) * 32;  // 0..127 within the group
+        constexpr int NCT2 = C::NCONV > 0 ? C::NCONV * 16 : 32;
+        const int qd = warp & 3;
+        const int row = qd * 32 + lane;
+        uint32_t q = 0;
+        for (int w = wfirst; w < tp.work; w += wstep) {
+            TileInfo<OP> ti;
+            ti.init(tp, p, w, rank);
+            const int nkb = ti.nkb_eff;
+            for (int it = 0; it < nkb; ++it, ++q) {
+                if ((int)(q & 1u) != grp) continue;
+                const int s = q % C::STAGES;
+                const uint32_t r = q / C::STAGES;
+                const uint32_t t = q % C::NT, rt = q / C::NT;  // TMEM A slot
+                mbar_wait(&aux->full[s], r & 1);
+                if (rt > 0) {  // slot t's previous k-block has been multiplied
+                    if (PAIR) mbar_wait_cluster(&aux->tfree[t], (rt - 1) & 1);
+                    else mbar_wait(&aux->tfree[t], (rt - 1) & 1);
+                    tc_fence_after();
+                }
+                uint8_t* st = tiles_ptr + s * C::STAGE_BYTES;
+                constexpr int NB2 = C::B_BYTES / 16 / NCT2;
+                static_assert(!C::A_TMEM || NB2 * NCT2 * 16 == C::B_BYTES, "converter split");
+                const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(C::A_TCOL0 + t * 64);
+                const bool hyb_a = (C::HYB && p.hyb) || (C::HYBW && tp.dw_hyb);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    float e[16];
+                    if (C::A_MN) {  // MN-major A tile [32 k][128 m]: one 4-byte element per k
+#pragma unroll
+                        for (int k = 0; k < 16; ++k)
+                            e[k] = *reinterpret_cast<const float*>(st + mnmaj_off((uint32_t)(16 * h + k), (uint32_t)(row & ~3)) +
+                                                                   (row & 3) * 4);
+                    } else {  // K-major A tile [128 m][32 k]: four 16-B chunks of this row
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const float4 v =
+                                *reinterpret_cast<const float4*>(st + kmaj_off((uint32_t)row, (uint32_t)(4 * h + c)));
+                            e[4 * c] = v.x;
+                            e[4 * c + 1] = v.y;
+                            e[4 * c + 2] = v.z;
+                            e[4 * c + 3] = v.w;
+                        }
+                    }
+                    if (hyb_a) {
+                        uint32_t hi[16], xh[8], xl[8];
+                        split_a16(e, hi, xh, xl);
+                        tmem_st_32x32b_x16(ta + h * 16, hi);
+                        tmem_st_32x32b_x8(ta + 32 + h * 8, xh);
+                        tmem_st_32x32b_x8(ta + 48 + h * 8, xl);
+                    } else {
+                        uint32_t hi[16], lo[16];
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) {
+                            const uint32_t hb = __float_as_uint(e[k]) & 0xFFFFE000u;
+                            hi[k] = hb;
+                            lo[k] = __float_as_uint(e[k] - __uint_as_float(hb));
+                        }
+                        tmem_st_32x32b_x16(ta + h * 16, hi);
+                        tmem_st_32x32b_x16(ta + 32 + h * 16, lo);
+                    }
+                }
+                if (C::HYBW && tp.dw_hyb) {  // dW: B' = [bf16(b_lo) ; bf16(b)] (as the 8-warp path below)
+                    const float4* bH = reinterpret_cast<const float4*>(st + C::B_OFF);
+                    uint8_t* bX = st + C::B_OFF + C::B_BYTES;
+#pragma unroll
+                    for (int e2 = 0; e2 < NB2; ++e2) {
+                        const uint32_t i = (uint32_t)(ct4 + e2 * NCT2);
+                        const uint32_t k = (i & 255u) >> 3, c32 = (i & 7u) >> 1;
+                        const uint32_t mn = (i >> 8) * 32u + ((c32 ^ (k & 3u)) << 3) + ((i & 1u) << 2);
+                        const float4 b = bH[i];
+                        const float lx = b.x - __uint_as_float(__float_as_uint(b.x) & 0xFFFFE000u);
+                        const float ly = b.y - __uint_as_float(__float_as_uint(b.y) & 0xFFFFE000u);
+                        const float lz = b.z - __uint_as_float(__float_as_uint(b.z) & 0xFFFFE000u);
+                        const float lw = b.w - __uint_as_float(__float_as_uint(b.w) & 0xFFFFE000u);
+                        *reinterpret_cast<uint2*>(bX + mnmaj16_off(k, mn, 64u)) =
+                            make_uint2(pack_bf16x2(lx, ly), pack_bf16x2(lz, lw));
+                        *reinterpret_cast<uint2*>(bX + mnmaj16_off(k + 32u, mn, 64u)) =
+                            make_uint2(pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+                    }
+                } else if (!(C::HYB && p.hyb)) {  // b_lo plane (dW three-MMA form, fwd / dX without the W' plane)
+                    const float4* bH = reinterpret_cast<const float4*>(st + C::B_OFF);
+                    float4* bL = reinterpret_cast<float4*>(st + C::B_OFF + C::B_BYTES);
+#pragma unroll
+                    for (int e2 = 0; e2 < NB2; ++e2) {
+                        const float4 v = bH[ct4 + e2 * NCT2];
+                        float4 o;
+                        o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                        o.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                        o.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                        o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                        bL[ct4 + e2 * NCT2] = o;
+                    }
+                }
+                tmem_st_wait();
+                if (!(C::HYB && p.hyb)) fence_proxy_async_smem();  // b_lo / B' planes -> the MMA's async proxy
+                tc_fence_before();
+                if (PAIR) {  // one arrival per warp, on CTA 0's barrier (it issues the MMAs)
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(&aux->conv[t], 0);
+                } else {
+                    mbar_arrive(&aux->conv[t]);
+                }
+            }
+        }
     } else if (warp >= C::CONV_W0) {
         // ======================= 3xTF32 split converters: lo = a - trunc_tf32(a)
         const int ct = tid - C::CONV_W0 * 32;
