@@ -21,6 +21,8 @@ namespace {
 
 const int g_knob_chunk_s = getenv("SMCONV_TMA_CHUNK") ? atoi(getenv("SMCONV_TMA_CHUNK")) : 8;
 const int g_knob_coalesce_s = getenv("SMCONV_COALESCE") ? atoi(getenv("SMCONV_COALESCE")) : 1;
+// SMCONV_STRIP_ALT=1: 3xTF32 converter warps in two groups on alternate stages (StripParams::alt_conv)
+const int g_knob_alt_s = getenv("SMCONV_STRIP_ALT") ? atoi(getenv("SMCONV_STRIP_ALT")) : 0;
 
 const int g_knob_tstore_s = getenv("SMCONV_TSTORE") ? atoi(getenv("SMCONV_TSTORE")) : 1;
 
@@ -114,6 +116,7 @@ int strip_launch(int op, int BN, int planes, const GenParams& g, cudaStream_t st
     const uint64_t C = fwd ? g.IC : g.OC;                 // channels of the activation operand
     const uint64_t H = fwd ? g.IH : g.OH, W = fwd ? g.IW : g.OW;
     sp.coalesce = g_knob_coalesce_s;
+    sp.alt_conv = planes == 2 ? g_knob_alt_s : 0;
     sp.CB = (int)(C / 32);
     sp.NG = g.N / 32;
     sp.OHo = fwd ? g.OH : g.IH;

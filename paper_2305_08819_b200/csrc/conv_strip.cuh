@@ -42,6 +42,7 @@ struct __align__(64) StripParams {
     int pair;          // work items are pair tiles (two 32-image groups), kernel template PAIR
     FastDiv fd_ntiles, fd_strips, fd_OHo;
     int coalesce;      // row-coalesced epilogue stores (StripCfg::EPW)
+    int alt_conv;      // 3xTF32 converter warps in two groups on alternate stages
     int tstore;        // ... leaving by TMA tensor store (conv_tma.cuh warp_rows_tstore): mapY = output (C, pixels, N)
     CUtensorMap mapY;
 };
@@ -143,7 +144,8 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
         // 3xTF32: one conv barrier per (slot, filter column) so the MMAs of window 0 start while
         // windows 1 and 2 are still being split (the converters' per-stage latency bounded the strip)
         for (int t = 0; t < (C::A_TMEM ? C::NT * C::FW : C::NT); ++t)
-            mbar_init(&aux->conv[t], PAIR ? 2 * C::NCONV : C::NCONV * 32);
+            mbar_init(&aux->conv[t], PAIR ? 2 * (sp.alt_conv ? C::NCONV / 2 : C::NCONV)
+                                          : (sp.alt_conv ? C::NCONV / 2 : C::NCONV) * 32);
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&aux->full[s], 1);
             mbar_init(&aux->empty[s], 1);
@@ -304,6 +306,60 @@ __global__ void __launch_bounds__(StripCfg<OP, BN, PLANES, R, PAIR>::NTHREADS, 1
                 if (++s == C::STAGES) {
                     s = 0;
                     ++r;
+                }
+            }
+        }
+    } else if (warp >= C::CONV_W0 && C::A_TMEM && sp.alt_conv) {
+        // ======================= 3xTF32 converters in two groups of 4 warps on alternate stages (conv_tma.cuh
+        // TmaParams::alt_conv): a warp = one TMEM lane quadrant, both K halves of each window
+        const int grp = (warp - C::CONV_W0) >> 2;
+        const int qd = warp & 3;
+        uint32_t q = 0;
+        for (int w = wfirst; w < sp.work; w += wstep) {
+            StripTile t;
+            t.init(sp, w, rank);
+            const int nkb = strip_rows<OP>(sp, p, t.orow) * sp.CB;
+            for (int it = 0; it < nkb; ++it, ++q) {
+                if ((int)(q & 1u) != grp) continue;
+                const int s = q % C::STAGES;
+                const uint32_t r = q / C::STAGES;
+                const uint32_t ts = q % C::NT, rts = q / C::NT;  // TMEM A-window slot
+                mbar_wait(&aux->full[s], r & 1);
+                if (rts > 0) {  // the slot's previous windows have been multiplied
+                    if (PAIR) mbar_wait_cluster(&aux->tfree[ts], (rts - 1) & 1);
+                    else mbar_wait(&aux->tfree[ts], (rts - 1) & 1);
+                    tc_fence_after();
+                }
+                const uint8_t* st = tiles_ptr + s * C::STAGE_BYTES;
+#pragma unroll
+                for (int fw = 0; fw < C::FW; ++fw) {
+                    const int woff = OP == OP_FWD ? fw : C::FW - 1 - fw;
+                    const uint8_t* slab = st + (woff + qd) * 4096;
+                    const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) +
+                                        (uint32_t)(C::A_TCOL0 + ts * C::A_SLOT_COLS + fw * 64);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        float e[16];
+#pragma unroll
+                        for (int cq = 0; cq < 4; ++cq) {
+                            const float4 v = *reinterpret_cast<const float4*>(
+                                slab + kmaj_off((uint32_t)lane, (uint32_t)(4 * h + cq)));
+                            e[4 * cq] = v.x, e[4 * cq + 1] = v.y, e[4 * cq + 2] = v.z, e[4 * cq + 3] = v.w;
+                        }
+                        uint32_t hi[16], xh[8], xl[8];
+                        split_a16(e, hi, xh, xl);
+                        tmem_st_32x32b_x16(ta + h * 16, hi);
+                        tmem_st_32x32b_x8(ta + 32 + h * 8, xh);
+                        tmem_st_32x32b_x8(ta + 48 + h * 8, xl);
+                    }
+                    tmem_st_wait();
+                    tc_fence_before();
+                    if (PAIR) {  // one arrival per warp, on CTA 0's barrier (it issues the MMAs)
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_remote(&aux->conv[ts * C::FW + fw], 0);
+                    } else {
+                        mbar_arrive(&aux->conv[ts * C::FW + fw]);
+                    }
                 }
             }
         }
