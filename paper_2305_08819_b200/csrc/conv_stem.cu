@@ -62,6 +62,7 @@ struct __align__(64) StemParams {
     long long M;       // N * OH * OW
     int tiles;         // fwd: ceil(M / 128); dW: k-blocks of 32 pixels
     int kb_per_cta;    // dW
+    int ts;            // dW 3xTF32: A (dY^T) in TMEM, TS-form MMAs (StemDwCfg::TS; SMCONV_STEM_TS=0: SS form)
     FastDiv fd_OW, fd_OHOW;
 };
 
@@ -339,12 +340,19 @@ struct StemDwCfg {
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
     static constexpr int CHUNK = 8;                    // promotion interval (k-blocks)
     static constexpr int PAD = (4 - OCB) * 4096;       // the last stage's junk-row reads stay inside the allocation
-    static constexpr int SMEM = 1024 + STAGES * STAGE + PAD + 256;
+    static constexpr int SMEM = 1024 + STAGES * STAGE + PAD + 512;
     static_assert(STAGES >= NBLD, "builders own k-blocks mod 4: the ring must be at least that deep");
+    // 3xTF32 (TS form): the converter warps write dY^T as a_hi | a_lo (32 + 32 columns per k-block) into
+    // a TMEM slot ring, so the MMAs read only B from shared memory.  The SS form read the 128-row A tile
+    // (half of it the junk rows of OC = 64) from shared memory for every one of the 12 MMAs per k-block:
+    // ~100 KB of shared-memory traffic per k-block, the kernel's bound (r02bb ncu: l1tex 63 %, 0.33 of HBM)
+    static constexpr bool TS = PLANES == 2;
+    static constexpr int NTS = 6;                      // TMEM A slots (64 columns each) after 2 x 64 accumulators
+    static constexpr int TCOLS = TS ? 512 : 128;
 };
 
 struct StemDwAux {
-    uint64_t afull[8], cfull[8], bfull[8], sfree[8], accfull[2], accfree[2];
+    uint64_t afull[8], cfull[8], bfull[8], sfree[8], accfull[2], accfree[2], tfree[8];
     uint32_t tmem_base;
 };
 
@@ -375,9 +383,12 @@ __global__ void __launch_bounds__(StemDwCfg<PLANES, OCB>::NTHREADS, 1)
             mbar_init(&aux->accfull[b], 1);
             mbar_init(&aux->accfree[b], 4);
         }
+        for (int t = 0; t < C::NTS; ++t) {
+            mbar_init(&aux->tfree[t], 1);
+        }
         fence_mbar_init();
     }
-    if (warp == C::MMA_W) tmem_alloc(&aux->tmem_base, 128);
+    if (warp == C::MMA_W) tmem_alloc(&aux->tmem_base, C::TCOLS);
     if (warp == C::TMA_W && lane == 0)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     tc_fence_before();
@@ -404,11 +415,13 @@ __global__ void __launch_bounds__(StemDwCfg<PLANES, OCB>::NTHREADS, 1)
         }
     } else if (warp == C::MMA_W) {
         constexpr uint32_t IDESC = idesc_tf32(128, kDwN, true, false);  // A MN-major, B K-major
+        constexpr uint32_t IDESC_TS = idesc_tf32(128, kDwN, false, false);  // A in TMEM (K along columns)
         const uint64_t ad0 = make_sdesc(base, 4096u, 512u, kLayoutSW128Base32);
         const uint64_t bd0 = make_sdesc(base + PLANES * C::A_BYTES, 16u, 1024u, kLayoutSW128);
         int c = 0;
         for (int it = 0; it < nkb; ++it) {
             const int s = it % C::STAGES, ic = it % C::CHUNK, b = c & 1;
+            const int ts = it % C::NTS;
             if (ic == 0 && c >= 2) {
                 mbar_wait(&aux->accfree[b], ((c >> 1) - 1) & 1);
                 tc_fence_after();
@@ -425,12 +438,20 @@ __global__ void __launch_bounds__(StemDwCfg<PLANES, OCB>::NTHREADS, 1)
                 for (int j = 0; j < 4; ++j) {
                     const uint64_t ah = ad0 + so + (uint64_t)j * 64;  // 8 px = 1024 B of the MN-major tile
                     const uint64_t bh = bd0 + so + (uint64_t)j * 2;   // 8 k = 32 B of the K-major tile
-                    mma_tf32_ss(d, ah, bh, IDESC, (ic > 0 || j > 0) ? 1u : 0u);
-                    if (PLANES == 2) {
-                        mma_tf32_ss(d, ah, bh + (uint64_t)(C::B_BYTES >> 4), IDESC, 1u);
-                        mma_tf32_ss(d, ah + (uint64_t)(C::A_BYTES >> 4), bh, IDESC, 1u);
+                    if (C::TS && p.ts) {  // a_hi | a_lo of this k-block in TMEM slot ts (columns 128 + 64 ts ..)
+                        const uint32_t ahi = tmem + (uint32_t)(128 + ts * 64 + j * 8);
+                        mma_tf32_ts(d, ahi, bh, IDESC_TS, (ic > 0 || j > 0) ? 1u : 0u);
+                        mma_tf32_ts(d, ahi, bh + (uint64_t)(C::B_BYTES >> 4), IDESC_TS, 1u);
+                        mma_tf32_ts(d, ahi + 32, bh, IDESC_TS, 1u);
+                    } else {
+                        mma_tf32_ss(d, ah, bh, IDESC, (ic > 0 || j > 0) ? 1u : 0u);
+                        if (PLANES == 2) {
+                            mma_tf32_ss(d, ah, bh + (uint64_t)(C::B_BYTES >> 4), IDESC, 1u);
+                            mma_tf32_ss(d, ah + (uint64_t)(C::A_BYTES >> 4), bh, IDESC, 1u);
+                        }
                     }
                 }
+                if (C::TS && p.ts) mma_commit(&aux->tfree[ts]);
                 mma_commit(&aux->sfree[s]);
                 if (last) mma_commit(&aux->accfull[b]);
             }
@@ -467,8 +488,43 @@ __global__ void __launch_bounds__(StemDwCfg<PLANES, OCB>::NTHREADS, 1)
             for (int k = 0; k < kKP; ++k) e[k] = en[k];
         }
     } else if (warp >= C::CONV_W0 && warp < C::CONV_W0 + 4) {
-        // 3xTF32: a_lo plane of the dY tile, same layout (elementwise)
-        if (PLANES == 2) {
+        // 3xTF32 (TS form): dY^T -> TMEM slot it % NTS as a_hi | a_lo.  The thread owning TMEM lane
+        // oc_l = 32 (warp % 4) + lane reads dY[px][oc_l] of the MN-major tile for the 32 pixels
+        if (C::TS && p.ts) {
+            const int qd = warp & 3;
+            const int ocl = 32 * qd + lane;
+            const uint32_t lanebase = (uint32_t)(qd * 32) << 16;
+            for (int it = 0; it < nkb; ++it) {
+                const int s = it % C::STAGES, ts = it % C::NTS;
+                mbar_wait(&aux->afull[s], (it / C::STAGES) & 1);
+                if (it >= C::NTS) {
+                    mbar_wait(&aux->tfree[ts], ((it / C::NTS) - 1) & 1);
+                    tc_fence_after();
+                }
+                if (qd < nblk) {  // rows >= 32 nblk are the m-tile's junk rows (OC < 128): never stored
+                    const uint8_t* tile = bptr + s * C::STAGE;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t hi[16], lo[16];
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) {
+                            const float e = *reinterpret_cast<const float*>(
+                                tile + mnmaj_off((uint32_t)(16 * h + k), (uint32_t)(ocl & ~3)) + (ocl & 3) * 4);
+                            const uint32_t hb = __float_as_uint(e) & 0xFFFFE000u;
+                            hi[k] = hb;
+                            lo[k] = __float_as_uint(e - __uint_as_float(hb));
+                        }
+                        const uint32_t ta = tmem + lanebase + (uint32_t)(128 + ts * 64);
+                        tmem_st_32x32b_x16(ta + h * 16, hi);
+                        tmem_st_32x32b_x16(ta + 32 + h * 16, lo);
+                    }
+                    tmem_st_wait();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&aux->cfull[s]);
+            }
+        } else if (PLANES == 2) {
             const int ct = tid - C::CONV_W0 * 32;
             for (int it = 0; it < nkb; ++it) {
                 const int s = it % C::STAGES;
@@ -523,7 +579,7 @@ __global__ void __launch_bounds__(StemDwCfg<PLANES, OCB>::NTHREADS, 1)
     __syncthreads();
     if (warp == C::MMA_W) {
         tc_fence_after();
-        tmem_dealloc(tmem, 128);
+        tmem_dealloc(tmem, C::TCOLS);
     }
 }
 
@@ -607,6 +663,8 @@ int stem_launch(int op, int planes, const GenParams& g, int splits, int kb_per_s
     p.out = g.out;
     p.tiles = (int)((p.M + 31) / 32);
     p.kb_per_cta = kb_per_split;
+    static const int ts_knob = getenv("SMCONV_STEM_TS") ? atoi(getenv("SMCONV_STEM_TS")) : 1;
+    p.ts = ts_knob;
     CUtensorMap mapA;  // dY viewed [M][OC], box (32 oc, 32 px), MN-major A blocks
     {
         uint64_t dims[2] = {(uint64_t)g.OC, (uint64_t)p.M}, strides[1] = {(uint64_t)g.OC * 4};
