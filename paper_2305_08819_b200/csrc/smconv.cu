@@ -190,6 +190,8 @@ constexpr int kMaxKbPerChain = 256;
 constexpr int kGenMaxKbPerChain3x = 16;  // GENERIC 3xTF32 (no chunked promotion)
 // largest cluster split-K (TMA fwd / dX on small maps); SMCONV_CSK=0 turns it off (A/B experiments)
 const int g_csk_max = getenv("SMCONV_CSK") ? atoi(getenv("SMCONV_CSK")) : 8;
+// SMCONV_CSK_BN64=1: BN = 64 cluster-split tiles for the smallest maps (see make_plan)
+const int g_csk_bn64 = getenv("SMCONV_CSK_BN64") ? atoi(getenv("SMCONV_CSK_BN64")) : 0;
 // SMCONV_DX_BK=0: 3xTF32 TMA dX reads the MN-major view of W instead of the transposed plane (A/B)
 const int g_dx_bk = getenv("SMCONV_DX_BK") ? atoi(getenv("SMCONV_DX_BK")) : 1;
 // SMCONV_ZFILL=0: keep zero_phases_kernel for the 1x1 stride-2 dX (A/B experiments)
@@ -663,11 +665,27 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
             pl.BN = 128;
             n_tiles = (g.Ngemm + pl.BN - 1) / pl.BN;
         }
-        const int t2 = m_tiles * n_tiles;
+        int t2 = m_tiles * n_tiles;
         // S capped by max_clusters (one wave of co-resident clusters)
-        int S = 1;
-        for (int S2 = 2; S2 <= g_csk_max && t2 * S2 <= kSMs && t2 <= max_clusters(S2) && 2 * S2 <= nkb_est; S2 *= 2)
-            S = S2;
+        auto pick_s = [&](int tt) {
+            int S_ = 1;
+            for (int S2 = 2; S2 <= g_csk_max && tt * S2 <= kSMs && tt <= max_clusters(S2) && 2 * S2 <= nkb_est; S2 *= 2)
+                S_ = S2;
+            return S_;
+        };
+        int S = pick_s(t2);
+        // SMCONV_CSK_BN64: while the cluster split fills at most half of the SMs (2x2 maps at batch 128: 16
+        // tiles x 4 = 64 CTAs), halve BN (down to 64): twice the CTAs with the same split
+        while (g_csk_bn64 && pl.BN >= 128 && t2 * S <= kSMs / 2 && g.Ngemm % (pl.BN / 2) == 0) {
+            const int bh = pl.BN / 2;
+            const int th = m_tiles * ((g.Ngemm + bh - 1) / bh);
+            const int Sh = pick_s(th);
+            if (Sh < 2 || th * Sh <= t2 * S) break;
+            pl.BN = bh;
+            n_tiles = (g.Ngemm + bh - 1) / bh;
+            t2 = th;
+            S = Sh;
+        }
         if (S >= 2) {
             splits = S;
             g.csk = S;
