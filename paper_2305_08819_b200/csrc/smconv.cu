@@ -190,6 +190,8 @@ constexpr int kMaxKbPerChain = 256;
 constexpr int kGenMaxKbPerChain3x = 16;  // GENERIC 3xTF32 (no chunked promotion)
 // largest cluster split-K (TMA fwd / dX on small maps); SMCONV_CSK=0 turns it off (A/B experiments)
 const int g_csk_max = getenv("SMCONV_CSK") ? atoi(getenv("SMCONV_CSK")) : 8;
+// make_plan_s2dx: BN cap for the virtual fwd conv it plans (0: none); thread-local, set around one call
+thread_local int t_fwd_bn_cap = 0;
 // SMCONV_CSK_BN64=1: BN = 64 cluster-split tiles for the smallest maps (see make_plan)
 const int g_csk_bn64 = getenv("SMCONV_CSK_BN64") ? atoi(getenv("SMCONV_CSK_BN64")) : 0;
 // SMCONV_DX_BK=0: 3xTF32 TMA dX reads the MN-major view of W instead of the transposed plane (A/B)
@@ -290,6 +292,9 @@ Dims mk(int N, int IH, int IW, int IC, int OC, int FH, int FW, int sh, int sw, i
 const int g_s2dx = getenv("SMCONV_S2DX") ? atoi(getenv("SMCONV_S2DX")) : 1;
 // SMCONV_S2DX_SKIP=0: issue the all-zero W2 blocks too (A/B experiments)
 const int g_s2dx_skip = getenv("SMCONV_S2DX_SKIP") ? atoi(getenv("SMCONV_S2DX_SKIP")) : 1;
+// SMCONV_S2DX_BN=64: super-pixel dX with one stride phase (IC columns) per n-tile, so no n-tile issues
+// MMAs for another phase's all-zero W2 blocks (25 % fewer MACs at IC = 64), at N = 64 (pair) tiles
+const int g_s2dx_bn = getenv("SMCONV_S2DX_BN") ? atoi(getenv("SMCONV_S2DX_BN")) : 0;
 
 int make_plan_s2dx(const Dims& d, int math, Plan& pl) {
     if (!g_s2dx || g_force[CONV_OP_BWD_DATA].load() != CONV_VARIANT_AUTO) return -1;
@@ -303,7 +308,10 @@ int make_plan_s2dx(const Dims& d, int math, Plan& pl) {
     Dims v = mk(d.N, d.OH, d.OW, d.OC, 4 * d.IC, 2, 2, 1, 1, 1, 1);
     v.OH = d.OH + 1;  // (OH + 2 - 2) / 1 + 1
     v.OW = d.OW + 1;
-    if (make_plan_base(CONV_OP_FWD, v, math, pl)) return -1;
+    t_fwd_bn_cap = (g_s2dx_bn > 0 && d.IC % g_s2dx_bn == 0) ? g_s2dx_bn : 0;
+    const int rcb = make_plan_base(CONV_OP_FWD, v, math, pl);
+    t_fwd_bn_cap = 0;
+    if (rcb) return -1;
     if (pl.variant != CONV_VARIANT_TMA || pl.splits != 1 || pl.zero_mask) return -1;
     pl.s2dx = 1;
     pl.gp.s2dx = 1;
@@ -532,6 +540,7 @@ int make_plan_base(int op, const Dims& d, int math, Plan& pl) {
         g.Ngemm = d.OC;
         m_tiles = (g.M + 127) / 128;
         pl.BN = bn_for(g.Ngemm);
+        if (t_fwd_bn_cap > 0 && pl.BN > t_fwd_bn_cap) pl.BN = t_fwd_bn_cap;  // make_plan_s2dx
         n_tiles = (g.Ngemm + pl.BN - 1) / pl.BN;
         out_elems = (long long)d.N * d.OH * d.OW * d.OC;
         nkb_est = (est_taps(d) * d.IC + 31) / 32;
